@@ -150,8 +150,8 @@ def generate(cfg: dict, seed: int | None = None) -> dict:
     mean_turns = np.array([CAT_SPEC[c]["turns"] for c in CATS])
     ws = mix / mean_turns
     ws /= ws.sum()
-    # two calibration rounds so that REQUEST shares match Table 2 after edge truncation
-    for _ in range(3):
+    # calibration rounds so that REQUEST shares match Table 2 after edge truncation
+    for _ in range(12):
         rng = np.random.default_rng([seed & M64, 1])
         cat, turns, sess, tidx, t = _sessions(cfg, rng, ws)
         us = np.rint(t * 1e6).astype(np.int64)
