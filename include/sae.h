@@ -1,0 +1,232 @@
+/*
+ * sae.h — C ABI v1 of the SAECache hot path on B200 (sm_100a).
+ *
+ * The operation is the batched trace replay of the SAECache prefix-cache
+ * eviction policy (arxiv 2605.18825, /root/reference/PAPER.md, cited "P:<line>"):
+ *   (a) chained block hashing + strict prefix lookup
+ *   (b) per-round scoring of every resident block, Eq.(1)-(3)
+ *   (c) victim selection: Alg.1 Evict (EF first by num_tokens, then the global
+ *       argmin of Eq.(3)), segmented per queue/class with a total-order tie-break
+ *       on (P, last, id)
+ *   (d) the online learners driven by eviction feedback
+ * Readings of silent / conflicting passages: DESIGN.md "Readings".
+ *
+ * Conventions
+ *  - Every call returns sae_status (0 = SAE_OK, < 0 = error).  Host-detectable
+ *    errors (NULL pointers, ABI mismatch, capacity 0, bad sizes) return
+ *    immediately.  Errors found on the device (arrival time going backwards,
+ *    empty prompt, output overflow, replica not grouped) set a STICKY flag that
+ *    the next synchronising call (sae_stats, sae_sync) returns, as CUDA does for
+ *    asynchronous errors; sae_last_error() gives the text.
+ *  - A ctx is single-threaded; one ctx per device per process.  It owns ALL
+ *    device state (block SoA, hash tables, ghost rings, counters, parameters,
+ *    scratch); it is allocated in sae_create.  Per-batch scratch grows with
+ *    stream-ordered allocation when a larger batch arrives.
+ *  - sae_batch / sae_admit_out pointers are DEVICE pointers owned by the caller;
+ *    they must stay valid until the stream passes the call.  Calls are
+ *    stream-ordered and asynchronous except sae_create, sae_destroy,
+ *    sae_batch_blocks, sae_stats, sae_sync and the sae_get_* readers.
+ *  - Numerics: fp64, every + - * / sqrt a single IEEE round-to-nearest op
+ *    (no FMA contraction), our own ln/exp/erfc (fdlibm 5.3 algorithms); integer
+ *    counters u64 with the 0.99 decay done as floor(99 x / 100).  Results are
+ *    bit-identical to the CPU oracle (oracle/, test infrastructure only).
+ */
+#ifndef SAE_H_
+#define SAE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SAE_ABI_VERSION 1u
+
+typedef struct sae_ctx sae_ctx;
+typedef int sae_status;
+typedef struct CUstream_st* sae_stream;  /* == cudaStream_t; NULL = legacy default stream */
+
+enum {
+  SAE_OK = 0,
+  SAE_E_INVAL = -1,          /* bad argument / empty prompt (O1: L >= 1)            */
+  SAE_E_CAPACITY_ZERO = -2,  /* capacity_blocks == 0                        */
+  SAE_E_EMPTY = -3,          /* sae_evict ran out of evictable blocks       */
+  SAE_E_NOT_RESIDENT = -4,   /* reserved                                           */
+  SAE_E_TIME = -5,           /* arrival earlier than the replica's current time     */
+  SAE_E_OVERFLOW = -6,       /* victim buffer too small / 2^32 block ids exhausted  */
+  SAE_E_OOM = -7,
+  SAE_E_CUDA = -8,
+  SAE_E_ABI = -9
+};
+
+/* queues and token types */
+enum { SAE_Q_EF = 0, SAE_Q_CHAT = 1, SAE_Q_AGENT = 2, SAE_Q_STRUCT = 3 };
+enum { SAE_T_SYS = 0, SAE_T_USER = 1, SAE_T_TOOL = 2, SAE_T_RESP = 3, SAE_T_COT = 4, SAE_T_DECODE = 5 };
+
+/* learner flags: which learners run at each firing (a disabled learner is skipped
+ * entirely: no update, no counter decay, no reset) and which rule variant. */
+enum {
+  SAE_L_TOKENS = 1,          /* TokenWeights */
+  SAE_L_QUEUES = 2,          /* QueueWeights */
+  SAE_L_LOGNORMAL = 4,       /* LognormalParams */
+  SAE_L_DECAY = 8,           /* decay power */
+  SAE_L_TOKEN_MULT = 16,     /* multiplicative token rule (Alg. P:725) instead of P:703-707 */
+  SAE_L_QUEUE_RELATIVE = 32  /* relative queue rule P:814-817 instead of Alg. P:583-593 */
+};
+
+/* Learned values and meta-parameters, fp64.  Index order: w[sys,user,tool,resp,cot],
+ * alpha[chat,agent,struct], mu/sigma[chat,agent].  beta_* weight the NEW value. */
+typedef struct {
+  double w[5], alpha[3], mu[2], sigma[2], gamma;
+  double eta, a_miss, b_reuse, T, beta_q, beta_ln, beta_gamma;
+  uint32_t learn_flags;
+  uint32_t _pad;
+} sae_params;
+
+typedef struct {
+  uint32_t abi_version;       /* must be SAE_ABI_VERSION */
+  uint32_t block_tokens;      /* 16; 1..16 supported */
+  uint32_t capacity_blocks;   /* C, per replica */
+  uint32_t n_replicas;        /* R independent caches in this ctx */
+  uint32_t ghost_capacity;    /* G, recently_evicted FIFO length (A30) */
+  uint32_t K;                 /* learners fire when evictions reach a multiple of K (A14) */
+  uint32_t interval_ring;     /* R_max ring of ln(dt) samples (A25), <= 4096 */
+  uint32_t interval_keep;     /* 200 */
+  uint32_t interval_min;      /* 20: update when > interval_min samples */
+  uint32_t n_pos_bins;        /* 10 positional bins (A27), <= 16 */
+  uint32_t ctas_per_replica;  /* 0 = auto (1 for small pools, the whole GPU for one huge pool) */
+  uint32_t traj_capacity;     /* learner-trajectory snapshots kept per replica (0 = none) */
+  uint64_t hash_seed;         /* H_{-1} of every chain (A1) */
+  double dt_eps;              /* dt floor, 1e-3 s (A7) */
+  double z_cut;               /* survival := 0 when z > z_cut (A36) */
+  sae_params init;            /* initial parameters of every replica */
+  int32_t device;
+  uint32_t _pad;
+} sae_config;
+
+/* One batch of requests.  DEVICE pointers, caller-owned, read-only.
+ * Requests of one replica must be contiguous and in arrival order; replicas may
+ * appear in any order.  Request i's prompt tokens are tokens[prompt_off[i] ..
+ * + prompt_len[i]) with per-token types types[...] (0 sys,1 user,2 tool,3 resp,
+ * 4 cot); its decode span is tokens[decode_off[i] .. + decode_len[i]) (blocks of
+ * type decode, chained after the last prompt block, A34).  flags: b0
+ * is_multi_turn (predicted for turn 0), b1 is_agentic, b2 has conversation id.
+ * shared_prefix_blocks[i] = number of leading template blocks (is_shared_prefix). */
+typedef struct {
+  uint32_t n;
+  uint32_t _pad;
+  uint64_t total_blocks;      /* sum_i ceil(prompt_len/B) + ceil(decode_len/B); see sae_batch_blocks */
+  const uint32_t* replica;
+  const double* arrival;
+  const uint64_t* prompt_off;
+  const uint32_t* prompt_len;
+  const uint64_t* decode_off;
+  const uint32_t* decode_len;
+  const uint32_t* tokens;
+  const uint8_t* types;
+  const uint8_t* flags;
+  const uint32_t* shared_prefix_blocks;
+} sae_batch;
+
+/* Outputs of sae_admit_batch.  DEVICE pointers, caller-allocated, written by the
+ * library.  Per request i: hit_blocks = length h of the resident chained prefix,
+ * miss_blocks = n_i - h, matched_tokens = tokens in prompt blocks j < h (A41),
+ * n_victims = blocks evicted to admit it; its victim ids (admission counters, in
+ * eviction order) are victim_ids[victim_off[i] .. + n_victims[i]).  victim_off[i]
+ * is the request's first block index (so victim_cap >= total_blocks suffices).
+ * block_hash / block_tau (optional, may be NULL) receive every block's chained
+ * hash and type tau at block_off[i] + j (block_off = victim_off). */
+typedef struct {
+  uint32_t* hit_blocks;
+  uint32_t* miss_blocks;
+  uint32_t* matched_tokens;
+  uint32_t* n_victims;
+  uint64_t* victim_off;       /* [n+1] */
+  uint32_t* victim_ids;
+  uint64_t victim_cap;
+  uint64_t* block_hash;       /* optional [total_blocks] */
+  uint8_t* block_tau;         /* optional [total_blocks] */
+} sae_admit_out;
+
+typedef struct {
+  uint64_t requests, blocks_looked_up, hit_blocks, hit_tokens, prompt_tokens;
+  uint64_t evictions, evict_by_queue[4], evict_by_type[6], mae_by_type[6];
+  uint64_t learner_firings, eviction_rounds, blocks_scored;
+  uint64_t resident, resident_by_queue[4];
+  uint64_t E, next_id, gseq;
+  double now;
+  uint64_t ts_ev[5], ts_mae[5], ts_hit[5], ts_acc[5];  /* token_stats */
+  uint64_t qh[3], qe[3];                             /* queue_hits / queue_evictions */
+  uint64_t pb_hit[16], pb_acc[16];                   /* positional bins */
+  uint64_t iv_len[2];                                /* reuse_intervals sizes */
+  uint64_t traj_count;
+  sae_params params;
+} sae_replica_stats;
+
+/* Trajectory snapshot taken at each learner firing. */
+typedef struct {
+  uint64_t E, request;
+  double w[5], alpha[3], mu[2], sigma[2], gamma;
+} sae_traj;
+
+/* Allocate a ctx with all device state on cfg->device.  SAE_E_ABI on version
+ * mismatch, SAE_E_CAPACITY_ZERO if capacity_blocks == 0, SAE_E_INVAL on other
+ * bad sizes, SAE_E_OOM / SAE_E_CUDA on allocation failure. */
+sae_status sae_create(const sae_config* cfg, sae_ctx** out);
+sae_status sae_destroy(sae_ctx* ctx);
+
+/* Replace one replica's parameters (sweeps, C5); p is a HOST pointer (synchronous).
+ * The cached structural priorities are refreshed if gamma changes. */
+sae_status sae_set_params(sae_ctx* ctx, uint32_t replica, const sae_params* p, sae_stream s);
+/* Copy every replica's parameters into dev_out[n_replicas] (device), stream-ordered,
+ * e.g. for an NCCL all-gather of the learned token-type weights. */
+sae_status sae_params_gather(sae_ctx* ctx, sae_params* dev_out, sae_stream s);
+/* Replace every replica's parameters from dev_in[n_replicas] (device), stream-ordered. */
+sae_status sae_params_scatter(sae_ctx* ctx, const sae_params* dev_in, sae_stream s);
+
+/* Synchronously compute batch->total_blocks (reads prompt/decode lengths on the device). */
+sae_status sae_batch_blocks(sae_ctx* ctx, const sae_batch* batch, uint64_t* total_blocks, sae_stream s);
+
+/* Replay a batch: for every request, steps a1..a7 (hash, lookup+touch, classify,
+ * score, select, evict, learn) exactly as Alg.1 Add/Evict/Classify + the learners,
+ * replicas in parallel, requests of a replica in order. */
+sae_status sae_admit_batch(sae_ctx* ctx, const sae_batch* batch, sae_admit_out* out, sae_stream s);
+
+/* Read-only probe: hit_blocks[i] = resident chained-prefix length of request i
+ * against the CURRENT state of its replica.  No touch, no counters. */
+sae_status sae_lookup(sae_ctx* ctx, const sae_batch* batch, uint32_t* hit_blocks, sae_stream s);
+
+/* Alg.1 Evict() x k on one replica at time `now` (>= the replica's time; advances
+ * it) with an empty pin set and full accounting (ghost push, counters, K trigger).
+ * victim_ids (device, >= k) receive the ids, *n_out (device u32) the count.  If
+ * fewer than k blocks are resident the sticky error SAE_E_EMPTY is raised. */
+sae_status sae_evict(sae_ctx* ctx, uint32_t replica, uint32_t k, double now,
+                     uint32_t* victim_ids, uint32_t* n_out, sae_stream s);
+
+/* Run the learners now (UINT32_MAX = all replicas); E is unchanged. */
+sae_status sae_update(sae_ctx* ctx, uint32_t replica, sae_stream s);
+
+/* Synchronous: copy one replica's counters/parameters to host_out; returns and
+ * clears the sticky device error if one was raised. */
+sae_status sae_stats(sae_ctx* ctx, uint32_t replica, sae_replica_stats* host_out, sae_stream s);
+/* Synchronous: copy up to cap trajectory snapshots of a replica (oldest first). */
+sae_status sae_get_traj(sae_ctx* ctx, uint32_t replica, sae_traj* host_out, uint64_t cap,
+                        uint64_t* n_out, sae_stream s);
+/* Synchronize the stream and return (and clear) the sticky device error. */
+sae_status sae_sync(sae_ctx* ctx, sae_stream s);
+const char* sae_last_error(const sae_ctx* ctx);
+
+/* Synthetic-trace token materialisation (input generator, not the method):
+ * tokens[dst[p] + i] = SM(SM(seed ^ SM(stream[p])) ^ (start[p] + i)) mod 2^17 and
+ * types[dst[p] + i] = type[p] for every piece p, i < len[p]. Device pointers. */
+sae_status sae_gen_tokens(uint64_t seed, uint64_t n_pieces, const uint64_t* stream,
+                          const uint64_t* start, const uint32_t* len, const uint64_t* dst,
+                          const uint8_t* type, uint32_t* tokens, uint8_t* types, sae_stream s);
+
+/* Counts of device kernels launched by this ctx so far (for bench accounting). */
+uint64_t sae_launch_count(const sae_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SAE_H_ */

@@ -1,0 +1,1549 @@
+// sae.cu — SAECache hot path on B200 (sm_100a): kernels + C ABI (include/sae.h).
+//
+// Paper: arxiv 2605.18825, /root/reference/PAPER.md ("P:<line>").  Readings of
+// silent/conflicting passages: DESIGN.md "Readings".
+//
+// Device layout: per replica r a struct-of-
+// arrays block table of C slots (hash u64, last f64, id u32, meta u32 =
+// q|tau|ntok|live, ob u32, omax u32, p_struct f64 cached per gamma-epoch,
+// acc u32, pin-stamp u32), an open-addressing resident table (u64 key -> slot,
+// tombstones + rebuild), a free-slot stack, the ghost ring (recently_evicted,
+// P:535) with its own hash index, the ln(dt) interval rings, and a scalar
+// state record (counters, learned parameters, E, ids).
+//
+// Kernels:
+//   k_nblocks / k_scan*   block offsets of the batch
+//   k_runs                per-replica request runs
+//   k_hash      (K1)      chained XXH64 + tau (median token) per block, one thread per request
+//   k_replay    (K2-K5)   persistent: one CTA owns one replica and replays its requests in
+//                         order: probe+touch+stats -> fused score/select -> apply -> learn
+//   k_lookup              read-only probes, one warp per request
+//   k_gen_tokens (K7)     synthetic token materialisation (input generator)
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sae.h"
+#include "dmath.cuh"
+#include "xxh64.cuh"
+
+namespace sae {
+
+constexpr uint64_t KEY_EMPTY = ~0ull;
+constexpr uint64_t KEY_TOMB = ~0ull - 1;
+constexpr int NT = 512;            // threads per replay CTA
+constexpr int NW = NT / 32;
+constexpr int CAND_MAX = 4096;     // candidate buffer (smem) per CTA
+constexpr int RMAX = 4096;         // max interval ring
+constexpr uint32_t SLOT_MASK = 0x0FFFFFFFu;
+constexpr double INV_SQRT2 = 0.70710678118654757;  // 0x3FE6A09E667F3BCD
+
+enum { Q_EF = 0, Q_CHAT = 1, Q_AGENT = 2, Q_STRUCT = 3 };
+enum { M_LIVE = 1u << 10 };
+
+__host__ __device__ inline uint32_t meta_pack(uint32_t q, uint32_t tau, uint32_t ntok) {
+  return q | (tau << 2) | (ntok << 5) | M_LIVE;
+}
+__device__ inline uint32_t meta_q(uint32_t m) { return m & 3u; }
+__device__ inline uint32_t meta_tau(uint32_t m) { return (m >> 2) & 7u; }
+__device__ inline uint32_t meta_ntok(uint32_t m) { return (m >> 5) & 31u; }
+
+// Replica scalar state (counters, learned params, bookkeeping).  Lives in global
+// memory between launches and in the owning CTA's shared memory during a replay.
+struct RState {
+  double now;
+  uint32_t has_now, err;
+  uint64_t E, next_id, gseq, round;
+  uint32_t live, free_top, tbl_used, gtbl_used;
+  uint32_t iv_head[2], iv_len[2];
+  uint64_t ts_ev[5], ts_mae[5], ts_hit[5], ts_acc[5];
+  uint64_t qh[3], qe[3];
+  uint64_t pb_hit[16], pb_acc[16];
+  uint64_t traj_n;
+  // statistics
+  uint64_t requests, blocks_looked_up, hit_blocks, hit_tokens, prompt_tokens, evictions;
+  uint64_t evict_by_queue[4], evict_by_type[6], mae_by_type[6];
+  uint64_t learner_firings, eviction_rounds, blocks_scored;
+  sae_params par;
+};
+
+struct Cand {           // one candidate victim: sort key (seg|tier, k0, k1, k2) + slot
+  uint64_t k0, k1;
+  uint32_t k2, ss;      // ss = slot | seg << 28
+};
+
+struct Dev {
+  uint32_t R, C, tmask, G, gmask, K, iv_ring, iv_keep, iv_min, nbins, B, traj_cap;
+  uint64_t hash_seed;
+  double dt_eps, z_cut;
+  RState* st;
+  uint64_t* bhash;
+  double* blast;
+  uint32_t* bid;
+  uint32_t* bmeta;
+  uint32_t* bob;
+  uint32_t* bomax;
+  double* bps;
+  uint32_t* bacc;
+  uint32_t* bpin;
+  uint32_t* freestk;
+  uint64_t* tkey;
+  uint32_t* tval;
+  uint64_t* ghash;
+  uint8_t* gtau;
+  uint8_t* glive;
+  uint32_t* gtslot;
+  uint64_t* gkey;
+  uint32_t* gval;
+  double* iv;
+  sae_traj* traj;
+  uint32_t* err;      // sticky first error (as -status), global
+};
+
+struct BatchDev {
+  uint32_t n;
+  const uint32_t* replica;
+  const double* arrival;
+  const uint64_t* poff;
+  const uint32_t* plen;
+  const uint64_t* doff;
+  const uint32_t* dlen;
+  const uint32_t* tokens;
+  const uint8_t* types;
+  const uint8_t* flags;
+  const uint32_t* spb;
+  uint64_t* boff;         // [n+1]
+  uint64_t* h;            // [TB]
+  uint8_t* tau;
+  uint8_t* ntok;
+  int32_t* slot;
+  uint8_t* q;
+  int32_t* nrank;
+  uint32_t* run_start;    // [R]
+  uint32_t* run_end;
+  // outputs
+  uint32_t* o_hit;
+  uint32_t* o_miss;
+  uint32_t* o_matched;
+  uint32_t* o_nvict;
+  uint64_t* o_voff;
+  uint32_t* o_vids;
+  uint64_t vcap;
+};
+
+__device__ inline void raise_err(const Dev& d, int status) {
+  atomicCAS(d.err, 0u, (uint32_t)(-status));
+}
+
+// ordered-bits transform: u64 order == double order (non-NaN)
+__device__ __forceinline__ uint64_t obits(double x) {
+  uint64_t b = (uint64_t)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | (1ull << 63));
+}
+__device__ __forceinline__ double from_obits(uint64_t o) {
+  uint64_t b = (o >> 63) ? (o & ~(1ull << 63)) : ~o;
+  return __longlong_as_double((long long)b);
+}
+
+// ---------------------------------------------------------------------------
+// Policy arithmetic (fixed op order, explicit RN intrinsics; SURVEY c.4)
+// ---------------------------------------------------------------------------
+// Eq.(1): p = 1 - F_LN(dt) = 0.5*erfc(z/sqrt2), z = (ln dt - mu)/sigma (A36)
+__device__ double survival(double dt, double mu, double sg, double z_cut) {
+  double z = __ddiv_rn(__dsub_rn(dm::ln(dt), mu), sg);
+  if (z > z_cut) return 0.0;
+  return __dmul_rn(0.5, dm::erfc(__dmul_rn(z, INV_SQRT2)));
+}
+// Eq.(2): p = 1 - (o/o_max)^gamma with pow(x,y) = exp(y ln x)
+__device__ double p_struct(uint32_t ob, uint32_t omax, double gam) {
+  if (ob == 0) return 1.0;
+  double r = __ddiv_rn((double)ob, (double)omax);
+  return __dsub_rn(1.0, dm::ex(__dmul_rn(gam, dm::ln(r))));
+}
+// Alg.1 Classify
+__device__ __forceinline__ uint32_t classify(uint32_t tau, bool mt, bool ag, bool cid, bool is_struct,
+                                             bool untempl) {
+  if (tau == 4 || tau == 5 || untempl) return Q_EF;
+  if (mt && ag) return Q_AGENT;
+  if (mt || cid) return Q_CHAT;
+  if (is_struct || tau == 0) return Q_STRUCT;
+  return Q_EF;
+}
+
+// ---------------------------------------------------------------------------
+// Open-addressing tables (linear probing; EMPTY / TOMB sentinels)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t home(uint64_t h, uint32_t mask) {
+  return (uint32_t)(h ^ (h >> 29)) & mask;
+}
+__device__ int32_t tbl_find(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                            uint32_t mask, uint64_t h) {
+  uint32_t i = home(h, mask);
+  while (true) {
+    uint64_t k = keys[i];
+    if (k == h) return (int32_t)vals[i];
+    if (k == KEY_EMPTY) return -1;
+    i = (i + 1) & mask;
+  }
+}
+__device__ int32_t tbl_find_pos(const uint64_t* __restrict__ keys, uint32_t mask, uint64_t h) {
+  uint32_t i = home(h, mask);
+  while (true) {
+    uint64_t k = keys[i];
+    if (k == h) return (int32_t)i;
+    if (k == KEY_EMPTY) return -1;
+    i = (i + 1) & mask;
+  }
+}
+// Insert a key known to be absent.  Concurrent inserts of distinct keys are safe;
+// no lookups run concurrently.  Returns the position; *fresh = consumed an EMPTY.
+__device__ uint32_t tbl_insert(uint64_t* keys, uint32_t* vals, uint32_t mask, uint64_t h, uint32_t v,
+                               uint32_t* used) {
+  uint32_t i = home(h, mask);
+  while (true) {
+    uint64_t k = keys[i];
+    if (k == KEY_EMPTY || k == KEY_TOMB) {
+      unsigned long long prev = atomicCAS((unsigned long long*)&keys[i], (unsigned long long)k,
+                                          (unsigned long long)h);
+      if (prev == k) {
+        vals[i] = v;
+        if (k == KEY_EMPTY) atomicAdd(used, 1u);
+        return i;
+      }
+      continue;  // lost the race: re-examine slot i
+    }
+    i = (i + 1) & mask;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Block-wide helpers (NT threads)
+// ---------------------------------------------------------------------------
+// exclusive scan of up to 3 flags per thread; returns ranks; totals in tot[3]
+__device__ __forceinline__ void block_scan3(uint32_t a, uint32_t b, uint32_t c, uint32_t& ra,
+                                            uint32_t& rb, uint32_t& rc, uint32_t* tot,
+                                            uint32_t* wsum /* [3*NW] smem */) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t ba = __ballot_sync(~0u, a), bb = __ballot_sync(~0u, b), bc = __ballot_sync(~0u, c);
+  uint32_t lm = (1u << lane) - 1u;
+  ra = __popc(ba & lm); rb = __popc(bb & lm); rc = __popc(bc & lm);
+  if (lane == 0) { wsum[w] = __popc(ba); wsum[NW + w] = __popc(bb); wsum[2 * NW + w] = __popc(bc); }
+  __syncthreads();
+  uint32_t oa = 0, ob = 0, oc = 0, ta = 0, tb = 0, tc = 0;
+  for (int i = 0; i < NW; ++i) {
+    uint32_t x = wsum[i], y = wsum[NW + i], z = wsum[2 * NW + i];
+    if (i < w) { oa += x; ob += y; oc += z; }
+    ta += x; tb += y; tc += z;
+  }
+  ra += oa; rb += ob; rc += oc;
+  tot[0] = ta; tot[1] = tb; tot[2] = tc;
+  __syncthreads();
+}
+
+__device__ __forceinline__ bool cand_less(const Cand& a, const Cand& b) {
+  uint32_t sa = a.ss >> 28, sb = b.ss >> 28;
+  if (sa != sb) return sa < sb;
+  if (a.k0 != b.k0) return a.k0 < b.k0;
+  if (a.k1 != b.k1) return a.k1 < b.k1;
+  return a.k2 < b.k2;
+}
+
+// bitonic sort of cand[0..N), N a power of two, ascending by (seg, k0, k1, k2)
+__device__ void block_sort(Cand* cand, int N) {
+  for (int k = 2; k <= N; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < N; i += NT) {
+        int ixj = i ^ j;
+        if (ixj > i) {
+          Cand x = cand[i], y = cand[ixj];
+          bool up = (i & k) == 0;
+          if (cand_less(y, x) == up) { cand[i] = y; cand[ixj] = x; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Batch preparation kernels
+// ---------------------------------------------------------------------------
+__global__ void k_nblocks(BatchDev b, uint32_t B, uint64_t* cnt) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < b.n) cnt[i] = (uint64_t)((b.plen[i] + B - 1) / B) + (uint64_t)((b.dlen[i] + B - 1) / B);
+}
+
+// exclusive scan of n u64 values (in place into out[0..n], out[n] = total); 3 phases
+constexpr int SCAN_TILE = 4096;
+__global__ void k_scan_reduce(const uint64_t* in, uint64_t n, uint64_t* part) {
+  __shared__ uint64_t s[32];
+  uint64_t base = (uint64_t)blockIdx.x * SCAN_TILE;
+  uint64_t acc = 0;
+  for (uint64_t i = base + threadIdx.x; i < base + SCAN_TILE && i < n; i += blockDim.x) acc += in[i];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(~0u, acc, o);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+    part[blockIdx.x] = t;
+  }
+}
+__global__ void k_scan_parts(uint64_t* part, uint32_t np) {
+  if (threadIdx.x == 0) {
+    uint64_t run = 0;
+    for (uint32_t i = 0; i < np; ++i) { uint64_t v = part[i]; part[i] = run; run += v; }
+    part[np] = run;
+  }
+}
+__global__ void k_scan_apply(const uint64_t* in, uint64_t n, const uint64_t* part, uint64_t* out,
+                             uint32_t np) {
+  // one CTA per tile, 1024 threads x 4 items, sequential within thread then block scan
+  __shared__ uint64_t s[1024];
+  uint64_t base = (uint64_t)blockIdx.x * SCAN_TILE;
+  uint64_t v[4], loc = 0;
+  for (int k = 0; k < 4; ++k) {
+    uint64_t i = base + threadIdx.x * 4 + k;
+    v[k] = i < n ? in[i] : 0;
+    loc += v[k];
+  }
+  s[threadIdx.x] = loc;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    uint64_t t = threadIdx.x >= o ? s[threadIdx.x - o] : 0;
+    __syncthreads();
+    s[threadIdx.x] += t;
+    __syncthreads();
+  }
+  uint64_t run = part[blockIdx.x] + s[threadIdx.x] - loc;
+  for (int k = 0; k < 4; ++k) {
+    uint64_t i = base + threadIdx.x * 4 + k;
+    if (i < n) out[i] = run;
+    run += v[k];
+  }
+  if (blockIdx.x == np - 1 && threadIdx.x == 0) out[n] = part[np];
+}
+
+__global__ void k_runs(BatchDev b, Dev d) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= b.n) return;
+  uint32_t r = b.replica[i];
+  if (r >= d.R) { raise_err(d, SAE_E_INVAL); return; }
+  if (i == 0 || b.replica[i - 1] != r) {
+    if (atomicCAS(&b.run_start[r], 0xFFFFFFFFu, i) != 0xFFFFFFFFu) raise_err(d, SAE_E_INVAL);
+  }
+  if (i == b.n - 1 || b.replica[i + 1] != r) b.run_end[r] = i + 1;
+}
+
+// K1: chained hashing + tau (A1-A4, A34). One thread per request.
+__global__ void __launch_bounds__(128) k_hash(BatchDev b, Dev d) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= b.n) return;
+  const uint32_t B = d.B;
+  uint32_t L = b.plen[i], O = b.dlen[i];
+  uint32_t np = (L + B - 1) / B, nd = (O + B - 1) / B;
+  uint64_t bo = b.boff[i];
+  const uint32_t* pt = b.tokens + b.poff[i];
+  const uint8_t* py = b.types + b.poff[i];
+  uint64_t prev = d.hash_seed;
+  for (uint32_t j = 0; j < np; ++j) {
+    uint32_t s = j * B, nj = min(B, L - s);
+    prev = xx::block(prev, pt + s, (int)nj);
+    b.h[bo + j] = prev;
+    b.tau[bo + j] = py[s + nj / 2];
+    b.ntok[bo + j] = (uint8_t)nj;
+  }
+  const uint32_t* dt = b.tokens + b.doff[i];
+  for (uint32_t j = 0; j < nd; ++j) {
+    uint32_t s = j * B, nj = min(B, O - s);
+    prev = xx::block(prev, dt + s, (int)nj);
+    b.h[bo + np + j] = prev;
+    b.tau[bo + np + j] = 5;
+    b.ntok[bo + np + j] = (uint8_t)nj;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Replay CTA: shared state
+// ---------------------------------------------------------------------------
+struct Smem {
+  RState st;
+  double cw[3][5];         // alpha_q * w_tau per scored queue (CHAT, AGENT, STRUCT)
+  uint32_t wsum[3 * NW];
+  uint32_t tot[3];
+  uint32_t cnt[16], start[16];
+  uint32_t ncand;
+  int32_t h;
+  uint32_t npin, matched, nnew;
+  uint64_t k, admit;
+  uint32_t flag;
+  double red[NW];
+};
+
+struct Ctx {               // per-CTA view of one replica
+  const Dev* d;
+  Smem* s;
+  Cand* cand;
+  uint32_t r;
+  uint64_t base;           // r * C
+};
+
+__device__ void recompute_cw(Smem& s) {
+  if (threadIdx.x < 15) {
+    int q = threadIdx.x / 5, t = threadIdx.x % 5;
+    s.cw[q][t] = __dmul_rn(s.st.par.alpha[q], s.st.par.w[t]);
+  }
+}
+
+// Recompute the cached structural priority of every live STRUCT block (gamma changed).
+__device__ void refresh_pstruct(Ctx& c) {
+  const Dev& d = *c.d;
+  const double gam = c.s->st.par.gamma;
+  for (uint32_t sl = threadIdx.x; sl < d.C; sl += NT) {
+    uint64_t gi = c.base + sl;
+    uint32_t m = d.bmeta[gi];
+    if ((m & M_LIVE) && meta_q(m) == Q_STRUCT) d.bps[gi] = p_struct(d.bob[gi], d.bomax[gi], gam);
+  }
+}
+
+// stride-halving tree sum over y[0..P) in smem (SURVEY c.3 TREE)
+__device__ double tree_sum(double* y, int P) {
+  for (int h = P >> 1; h >= 1; h >>= 1) {
+    for (int i = threadIdx.x; i < h; i += NT) y[i] = __dadd_rn(y[i], y[i + h]);
+    __syncthreads();
+  }
+  double r = y[0];
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ double clampd(double x, double lo, double hi) {
+  return x < lo ? lo : (x > hi ? hi : x);
+}
+
+// LEARN (SURVEY c.3): TokenWeights -> QueueWeights -> LognormalParams -> DecayPower.
+__device__ void learn(Ctx& c) {
+  const Dev& d = *c.d;
+  Smem& s = *c.s;
+  RState& st = s.st;
+  sae_params& p = st.par;
+  const uint32_t f = p.learn_flags;
+  const double gamma_old = p.gamma;
+  // L1 TokenWeights (A16, A17)
+  if ((f & SAE_L_TOKENS) && threadIdx.x == 0) {
+    for (int t = 0; t < 5; ++t) {
+      if (st.ts_ev[t] > 10) {
+        double rm = __ddiv_rn((double)st.ts_mae[t], (double)st.ts_ev[t]);
+        double rr = st.ts_acc[t] > 0 ? __ddiv_rn((double)st.ts_hit[t], (double)st.ts_acc[t]) : 0.0;
+        if (f & SAE_L_TOKEN_MULT) {
+          p.w[t] = __dmul_rn(p.w[t], __dadd_rn(1.0, __dmul_rn(p.eta, rm)));
+        } else {
+          double tgt = __dadd_rn(__dadd_rn(1.0, __dmul_rn(rm, p.a_miss)), __dmul_rn(rr, p.b_reuse));
+          p.w[t] = __dadd_rn(__dmul_rn(__dsub_rn(1.0, p.eta), p.w[t]), __dmul_rn(p.eta, tgt));
+        }
+        p.w[t] = clampd(p.w[t], 0.1, 5.0);
+      }
+    }
+    for (int t = 0; t < 5; ++t) {
+      st.ts_ev[t] = (99ull * st.ts_ev[t]) / 100ull;
+      st.ts_mae[t] = (99ull * st.ts_mae[t]) / 100ull;
+      st.ts_hit[t] = (99ull * st.ts_hit[t]) / 100ull;
+      st.ts_acc[t] = (99ull * st.ts_acc[t]) / 100ull;
+    }
+  }
+  // L2 QueueWeights (Alg. P:575-597 or relative rule P:814-817)
+  if (f & SAE_L_QUEUES) {
+    if (f & SAE_L_QUEUE_RELATIVE) {
+      if (threadIdx.x < 3) s.cnt[threadIdx.x] = 0;
+      __syncthreads();
+      for (uint32_t sl = threadIdx.x; sl < d.C; sl += NT) {
+        uint32_t m = d.bmeta[c.base + sl];
+        if ((m & M_LIVE) && meta_q(m) != Q_EF) atomicAdd(&s.cnt[meta_q(m) - 1], 1u);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double Eq[3];
+        bool def[3];
+        double sum = 0.0;
+        int nd = 0;
+        for (int q = 0; q < 3; ++q) {
+          double frac = __ddiv_rn((double)s.cnt[q], (double)d.C);
+          def[q] = frac > 0.0;
+          if (def[q]) { Eq[q] = __ddiv_rn((double)st.qh[q], frac); sum = __dadd_rn(sum, Eq[q]); nd++; }
+        }
+        if (nd > 0) {
+          double Ebar = __ddiv_rn(sum, (double)nd);
+          if (Ebar > 0.0) {
+            for (int q = 0; q < 3; ++q) {
+              if (!def[q]) continue;
+              double x = __ddiv_rn(Eq[q], Ebar);
+              double pw = (x == 0.0) ? 0.0 : dm::ex(__ddiv_rn(dm::ln(x), p.T));
+              p.alpha[q] = __dadd_rn(p.alpha[q], __dmul_rn(p.beta_q, __dsub_rn(pw, p.alpha[q])));
+              p.alpha[q] = clampd(p.alpha[q], 0.1, 3.0);
+            }
+          }
+        }
+        for (int q = 0; q < 3; ++q) { st.qh[q] = 0; st.qe[q] = 0; }
+      }
+    } else if (threadIdx.x == 0) {
+      for (int q = 0; q < 3; ++q) {
+        if (st.qe[q] > 5) {
+          double eff = __ddiv_rn((double)st.qh[q], (double)st.qe[q]);
+          double tgt = __dadd_rn(1.0, __ddiv_rn(eff, p.T));
+          p.alpha[q] = __dadd_rn(p.alpha[q], __dmul_rn(p.beta_q, __dsub_rn(tgt, p.alpha[q])));
+          p.alpha[q] = clampd(p.alpha[q], 0.1, 3.0);
+        }
+      }
+      for (int q = 0; q < 3; ++q) { st.qh[q] = 0; st.qe[q] = 0; }
+    }
+  }
+  __syncthreads();
+  // L3 LognormalParams (Alg. P:762-784; A23, A24, A25)
+  if (f & SAE_L_LOGNORMAL) {
+    double* y = reinterpret_cast<double*>(c.cand);
+    for (int sidx = 0; sidx < 2; ++sidx) {
+      uint32_t n = st.iv_len[sidx];
+      if (n > d.iv_min) {
+        int P = 1;
+        while ((uint32_t)P < n) P <<= 1;
+        const double* ring = d.iv + ((uint64_t)c.r * 2 + sidx) * RMAX;
+        uint32_t first = (st.iv_head[sidx] + RMAX - n) % RMAX;
+        for (int i = threadIdx.x; i < P; i += NT) y[i] = (uint32_t)i < n ? ring[(first + i) % RMAX] : 0.0;
+        __syncthreads();
+        double sum = tree_sum(y, P);
+        double m = __ddiv_rn(sum, (double)n);
+        for (int i = threadIdx.x; i < P; i += NT) {
+          double x = (uint32_t)i < n ? ring[(first + i) % RMAX] : 0.0;
+          double dd = __dsub_rn(x, m);
+          y[i] = (uint32_t)i < n ? __dmul_rn(dd, dd) : 0.0;
+        }
+        __syncthreads();
+        double v = __ddiv_rn(tree_sum(y, P), (double)n);
+        if (threadIdx.x == 0) {
+          double sd = __dsqrt_rn(v);
+          p.mu[sidx] = __dadd_rn(p.mu[sidx], __dmul_rn(p.beta_ln, __dsub_rn(m, p.mu[sidx])));
+          p.sigma[sidx] = __dadd_rn(p.sigma[sidx], __dmul_rn(p.beta_ln, __dsub_rn(sd, p.sigma[sidx])));
+          if (p.sigma[sidx] < 0.1) p.sigma[sidx] = 0.1;
+          if (n > d.iv_keep) st.iv_len[sidx] = d.iv_keep;
+        }
+        __syncthreads();
+      }
+    }
+  }
+  // L4 DecayPower (A27)
+  if ((f & SAE_L_DECAY) && threadIdx.x == 0) {
+    uint32_t NB = d.nbins, half = NB / 2;
+    double fs = 0.0, bs = 0.0;
+    int fc = 0, bc = 0;
+    for (uint32_t i = 0; i < NB; ++i) {
+      if (st.pb_acc[i] == 0) continue;
+      double rate = __ddiv_rn((double)st.pb_hit[i], (double)st.pb_acc[i]);
+      if (i < half) { fs = __dadd_rn(fs, rate); fc++; } else { bs = __dadd_rn(bs, rate); bc++; }
+    }
+    if (fc > 0 && bc > 0) {
+      double fa = __ddiv_rn(fs, (double)fc), ba = __ddiv_rn(bs, (double)bc);
+      if (fa > 0.0) {
+        double ratio = __ddiv_rn(ba, fa);
+        double est = __ddiv_rn(1.0, __dadd_rn(ratio, 0.1));
+        p.gamma = __dadd_rn(p.gamma, __dmul_rn(p.beta_gamma, __dsub_rn(est, p.gamma)));
+        p.gamma = clampd(p.gamma, 0.3, 3.0);
+      }
+    }
+    for (uint32_t i = 0; i < NB; ++i) {
+      st.pb_hit[i] = (99ull * st.pb_hit[i]) / 100ull;
+      st.pb_acc[i] = (99ull * st.pb_acc[i]) / 100ull;
+    }
+  }
+  __syncthreads();
+  if (p.gamma != gamma_old) refresh_pstruct(c);
+  recompute_cw(s);
+  if (threadIdx.x == 0) {
+    st.learner_firings++;
+    if (d.traj_cap > 0) {
+      sae_traj t;
+      t.E = st.E;
+      t.request = st.requests;
+      for (int i = 0; i < 5; ++i) t.w[i] = p.w[i];
+      for (int i = 0; i < 3; ++i) t.alpha[i] = p.alpha[i];
+      for (int i = 0; i < 2; ++i) { t.mu[i] = p.mu[i]; t.sigma[i] = p.sigma[i]; }
+      t.gamma = p.gamma;
+      d.traj[(uint64_t)c.r * d.traj_cap + (st.traj_n % d.traj_cap)] = t;
+      st.traj_n++;
+    }
+  }
+  __syncthreads();
+}
+
+// Rebuild the resident table (tombstone cleanup) from the live SoA.
+__device__ void rebuild_table(Ctx& c) {
+  const Dev& d = *c.d;
+  const uint64_t tb = (uint64_t)d.tmask + 1;
+  uint64_t* keys = d.tkey + (uint64_t)c.r * tb;
+  uint32_t* vals = d.tval + (uint64_t)c.r * tb;
+  for (uint64_t i = threadIdx.x; i < tb; i += NT) keys[i] = KEY_EMPTY;
+  if (threadIdx.x == 0) c.s->st.tbl_used = 0;
+  __syncthreads();
+  for (uint32_t sl = threadIdx.x; sl < d.C; sl += NT) {
+    uint64_t gi = c.base + sl;
+    if (d.bmeta[gi] & M_LIVE) tbl_insert(keys, vals, d.tmask, d.bhash[gi], sl, &c.s->st.tbl_used);
+  }
+  __syncthreads();
+}
+__device__ void rebuild_ghost(Ctx& c) {
+  const Dev& d = *c.d;
+  const uint64_t gt = (uint64_t)d.gmask + 1;
+  uint64_t* keys = d.gkey + (uint64_t)c.r * gt;
+  uint32_t* vals = d.gval + (uint64_t)c.r * gt;
+  for (uint64_t i = threadIdx.x; i < gt; i += NT) keys[i] = KEY_EMPTY;
+  if (threadIdx.x == 0) c.s->st.gtbl_used = 0;
+  __syncthreads();
+  const uint64_t gb = (uint64_t)c.r * d.G;
+  for (uint32_t p = threadIdx.x; p < d.G; p += NT) {
+    if (d.glive[gb + p]) d.gtslot[gb + p] = tbl_insert(keys, vals, d.gmask, d.ghash[gb + p], p, &c.s->st.gtbl_used);
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Fused score + select (a4 + a5) for one chunk of m victims (no learner firing
+// inside).  Exact: key = (tier, primary, last, id) per SURVEY c.2 O11.  Per
+// resident, unpinned block one pass computes its segment (EF / 8 multi-turn
+// classes (queue, tau) / STRUCT) and key: EF (ntok, id); multi-turn class
+// (last, id) (P strictly decreasing in dt within a class, §8(a) a4); STRUCT
+// (P, last, id) with the cached p_struct.  Candidates are sorted; EF victims come
+// first (Stage 1); the class heads get their exact Eq.(3) P and the
+// scored union is merged by (P, last, id) (Stage 2).
+// Output: victims' slots in eviction order in cand[0..m).
+// ---------------------------------------------------------------------------
+__device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp) {
+  const Dev& d = *c.d;
+  Smem& s = *c.s;
+  const double now = s.st.now;
+  if (threadIdx.x < 16) s.cnt[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s.ncand = 0;
+  __syncthreads();
+  for (uint32_t sl = threadIdx.x; sl < d.C; sl += NT) {
+    const uint64_t gi = c.base + sl;
+    const uint32_t meta = d.bmeta[gi];
+    if (!(meta & M_LIVE) || d.bpin[gi] == stamp) continue;
+    const uint32_t q = meta_q(meta), tau = meta_tau(meta);
+    Cand x;
+    uint32_t seg;
+    if (q == Q_EF) {
+      seg = 0;
+      x.k0 = ((uint64_t)meta_ntok(meta) << 32) | d.bid[gi];
+      x.k1 = 0;
+      x.k2 = 0;
+    } else if (q == Q_STRUCT) {
+      seg = 9;
+      double last = d.blast[gi];
+      double dt = __dsub_rn(now, last);
+      if (dt < d.dt_eps) dt = d.dt_eps;
+      double P = __ddiv_rn(__dmul_rn(s.cw[2][tau], d.bps[gi]), dt);
+      x.k0 = obits(P);
+      x.k1 = obits(last);
+      x.k2 = d.bid[gi];
+    } else {
+      seg = 1 + (q - 1) * 4 + (tau & 3);
+      x.k0 = obits(d.blast[gi]);
+      x.k1 = d.bid[gi];
+      x.k2 = 0;
+    }
+    x.ss = sl | (seg << 28);
+    uint32_t pos = atomicAdd(&s.ncand, 1u);
+    c.cand[pos] = x;
+    atomicAdd(&s.cnt[seg], 1u);
+  }
+  __syncthreads();
+  const uint32_t nc = s.ncand;
+  int N = 1;
+  while ((uint32_t)N < nc) N <<= 1;
+  for (uint32_t i = nc + threadIdx.x; i < (uint32_t)N; i += NT) {
+    c.cand[i].k0 = ~0ull; c.cand[i].k1 = ~0ull; c.cand[i].k2 = ~0u; c.cand[i].ss = 15u << 28;
+  }
+  if (threadIdx.x == 0) {
+    uint32_t run = 0;
+    for (int g = 0; g < 16; ++g) { s.start[g] = run; run += s.cnt[g]; }
+    s.st.blocks_scored += nc;
+  }
+  __syncthreads();
+  block_sort(c.cand, N);
+  const uint32_t e = min(m, s.cnt[0]);
+  const uint32_t mp = m - e;
+  // re-tier: 0 = EF head, 1 = scored candidate, 3 = out
+  for (uint32_t i = threadIdx.x; i < (uint32_t)N; i += NT) {
+    Cand x = c.cand[i];
+    uint32_t seg = x.ss >> 28, sl = x.ss & SLOT_MASK;
+    uint32_t rank = i - s.start[seg < 16 ? seg : 15];
+    uint32_t tier = 3;
+    if (seg == 0) {
+      tier = rank < e ? 0 : 3;
+    } else if (seg >= 1 && seg <= 8) {
+      if (rank < mp) {
+        tier = 1;
+        const uint32_t q = 1 + (seg - 1) / 4, tau = (seg - 1) & 3;
+        const double last = from_obits(x.k0);
+        double dt = __dsub_rn(now, last);
+        if (dt < d.dt_eps) dt = d.dt_eps;
+        const double p = survival(dt, s.st.par.mu[q - 1], s.st.par.sigma[q - 1], d.z_cut);
+        const double P = __ddiv_rn(__dmul_rn(s.cw[q - 1][tau], p), dt);
+        x.k2 = (uint32_t)x.k1;  // id
+        x.k1 = x.k0;            // last
+        x.k0 = obits(P);
+      }
+    } else if (seg == 9) {
+      tier = rank < mp ? 1 : 3;
+    }
+    if (tier == 3) { x.k0 = ~0ull; x.k1 = ~0ull; x.k2 = ~0u; }
+    x.ss = sl | (tier << 28);
+    c.cand[i] = x;
+  }
+  __syncthreads();
+  block_sort(c.cand, N);
+}
+
+// Apply a chunk of m victims (cand[0..m) in eviction order): SURVEY c.2 O11 steps 1-4.
+__device__ void apply_chunk(Ctx& c, uint32_t m, uint32_t* vids_out) {
+  const Dev& d = *c.d;
+  Smem& s = *c.s;
+  RState& st = s.st;
+  const uint64_t tb = (uint64_t)d.tmask + 1, gt = (uint64_t)d.gmask + 1;
+  uint64_t* tkey = d.tkey + (uint64_t)c.r * tb;
+  uint64_t* gkey = d.gkey + (uint64_t)c.r * gt;
+  uint32_t* gval = d.gval + (uint64_t)c.r * gt;
+  const uint64_t gb = (uint64_t)c.r * d.G;
+  for (uint32_t v0 = 0; v0 < m; v0 += d.G) {
+    const uint32_t mb = min(m - v0, d.G);
+    // phase 1: remove from the resident table, count, expire ghost slots
+    for (uint32_t v = threadIdx.x; v < mb; v += NT) {
+      const uint32_t sl = c.cand[v0 + v].ss & SLOT_MASK;
+      const uint64_t gi = c.base + sl;
+      const uint64_t H = d.bhash[gi];
+      const uint32_t meta = d.bmeta[gi];
+      const uint32_t q = meta_q(meta), tau = meta_tau(meta);
+      if (vids_out) vids_out[v0 + v] = d.bid[gi];
+      int32_t pos = tbl_find_pos(tkey, d.tmask, H);
+      if (pos >= 0) tkey[pos] = KEY_TOMB;
+      d.bmeta[gi] = 0;
+      if (tau < 5) atomicAdd((unsigned long long*)&st.ts_ev[tau], 1ull);
+      if (q != Q_EF) atomicAdd((unsigned long long*)&st.qe[q - 1], 1ull);
+      atomicAdd((unsigned long long*)&st.evict_by_queue[q], 1ull);
+      atomicAdd((unsigned long long*)&st.evict_by_type[tau], 1ull);
+      const uint32_t p = (uint32_t)((st.gseq + v0 + v) % d.G);
+      if (d.glive[gb + p]) {  // FIFO expiry of the oldest ghost (A30)
+        gkey[d.gtslot[gb + p]] = KEY_TOMB;
+        d.glive[gb + p] = 0;
+      }
+      d.ghash[gb + p] = H;
+      d.gtau[gb + p] = (uint8_t)tau;
+    }
+    __syncthreads();
+    // phase 2: ghost push (recently_evicted[hash] = tau), free the slot
+    for (uint32_t v = threadIdx.x; v < mb; v += NT) {
+      const uint32_t sl = c.cand[v0 + v].ss & SLOT_MASK;
+      const uint64_t gi = c.base + sl;
+      const uint32_t p = (uint32_t)((st.gseq + v0 + v) % d.G);
+      const uint64_t H = d.ghash[gb + p];
+      d.glive[gb + p] = 1;
+      d.gtslot[gb + p] = tbl_insert(gkey, gval, d.gmask, H, p, &st.gtbl_used);
+      d.freestk[c.base + st.free_top + v0 + v] = sl;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      st.free_top += mb;
+      st.live -= mb;
+      st.gseq += mb;
+      st.E += mb;
+      st.evictions += mb;
+    }
+    __syncthreads();
+  }
+}
+
+// Evict k victims with pin stamp (k <= unpinned residents), chunked at K crossings (A14).
+__device__ void evict_k(Ctx& c, uint64_t k, uint32_t stamp, uint32_t* vids_out) {
+  const Dev& d = *c.d;
+  Smem& s = *c.s;
+  uint64_t done = 0;
+  while (done < k) {
+    const uint64_t to_cross = d.K - (s.st.E % d.K);
+    const uint32_t m = (uint32_t)min(k - done, to_cross);
+    select_chunk(c, m, stamp);
+    apply_chunk(c, m, vids_out ? vids_out + done : nullptr);
+    done += m;
+    if (s.st.E % d.K == 0) learn(c);
+  }
+  if (s.st.gtbl_used > ((d.gmask + 1) / 4) * 3) rebuild_ghost(c);
+}
+
+__device__ void load_state(Ctx& c) {
+  const Dev& d = *c.d;
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(d.st + c.r);
+  uint32_t* dst = reinterpret_cast<uint32_t*>(&c.s->st);
+  for (int i = threadIdx.x; i < (int)(sizeof(RState) / 4); i += NT) dst[i] = src[i];
+  __syncthreads();
+  recompute_cw(*c.s);
+  __syncthreads();
+}
+__device__ void store_state(Ctx& c) {
+  __syncthreads();
+  const Dev& d = *c.d;
+  uint32_t* dst = reinterpret_cast<uint32_t*>(d.st + c.r);
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(&c.s->st);
+  for (int i = threadIdx.x; i < (int)(sizeof(RState) / 4); i += NT) dst[i] = src[i];
+}
+
+// One request round (SURVEY c.2 O1-O13).  Returns false on a sticky error.
+__device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
+  const Dev& d = *c.d;
+  Smem& s = *c.s;
+  RState& st = s.st;
+  const uint64_t tb = (uint64_t)d.tmask + 1, gt = (uint64_t)d.gmask + 1;
+  uint64_t* tkey = d.tkey + (uint64_t)c.r * tb;
+  uint32_t* tval = d.tval + (uint64_t)c.r * tb;
+  uint64_t* gkey = d.gkey + (uint64_t)c.r * gt;
+  uint32_t* gval = d.gval + (uint64_t)c.r * gt;
+  const uint64_t gb = (uint64_t)c.r * d.G;
+  const double now = b.arrival[i];
+  const uint32_t L = b.plen[i], O = b.dlen[i];
+  // O1 / time check
+  if (L < 1 || (st.has_now && now < st.now)) {
+    if (threadIdx.x == 0) {
+      st.err = L < 1 ? (uint32_t)(-SAE_E_INVAL) : (uint32_t)(-SAE_E_TIME);
+      raise_err(d, L < 1 ? SAE_E_INVAL : SAE_E_TIME);
+    }
+    __syncthreads();
+    return false;
+  }
+  const uint32_t B = d.B;
+  const uint32_t np = (L + B - 1) / B, n = np + (O + B - 1) / B;
+  const uint64_t bo = b.boff[i];
+  const uint32_t fl = b.flags[i], spb = b.spb[i];
+  const bool mt = fl & 1, ag = fl & 2, cid = fl & 4;
+  const bool untempl = !mt && spb == 0;             // A31
+  const uint32_t omax = np > 1 ? np - 1 : 1;         // A8
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    st.now = now;
+    st.has_now = 1;
+    st.round++;
+    s.h = (int32_t)n;
+    s.npin = 0;
+    s.matched = 0;
+  }
+  __syncthreads();
+  const uint32_t stamp = (uint32_t)st.round;
+  // ---- O4/O5 classify + probe (Alg.1 Classify P:550-564; strict prefix P:158)
+  for (uint32_t j = threadIdx.x; j < n; j += NT) {
+    const uint64_t H = b.h[bo + j];
+    const uint32_t tau = b.tau[bo + j];
+    const int32_t sl = tbl_find(tkey, tval, d.tmask, H);
+    b.slot[bo + j] = sl;
+    b.q[bo + j] = (uint8_t)classify(tau, mt, ag, cid, j < spb, untempl);
+    if (sl < 0) atomicMin(&s.h, (int32_t)j);
+    else atomicAdd(&s.npin, 1u);
+  }
+  __syncthreads();
+  const uint32_t h = (uint32_t)s.h;
+  // ---- O6-O9 stats, touch, orphans, miss-after-evict; ordered ranks by block scans
+  uint32_t new_base = 0;
+  for (uint32_t j0 = 0; j0 < n; j0 += NT) {
+    const uint32_t j = j0 + threadIdx.x;
+    const bool valid = j < n;
+    uint32_t fc = 0, fa = 0, fn = 0;
+    double lnv = 0.0;
+    if (valid) {
+      const int32_t sl = b.slot[bo + j];
+      const uint32_t q = b.q[bo + j], tau = b.tau[bo + j];
+      const uint32_t bin = min(d.nbins - 1, (d.nbins * j) / omax);
+      if (tau < 5) atomicAdd((unsigned long long*)&st.ts_acc[tau], 1ull);
+      if (q == Q_STRUCT) atomicAdd((unsigned long long*)&st.pb_acc[bin], 1ull);
+      if (sl >= 0) {
+        const uint64_t gi = c.base + (uint32_t)sl;
+        d.bpin[gi] = stamp;
+        const uint32_t meta = d.bmeta[gi];
+        if (j < h) {  // O7 hit (A9: credited to the old queue before re-routing)
+          double dt = __dsub_rn(now, d.blast[gi]);
+          if (dt < d.dt_eps) dt = d.dt_eps;
+          const uint32_t qo = meta_q(meta);
+          if (qo == Q_CHAT || qo == Q_AGENT) {
+            atomicAdd((unsigned long long*)&st.qh[qo - 1], 1ull);
+            lnv = dm::ln(dt);
+            if (qo == Q_CHAT) fc = 1; else fa = 1;
+          } else if (qo == Q_STRUCT) {
+            atomicAdd((unsigned long long*)&st.qh[2], 1ull);
+          }
+          if (tau < 5) atomicAdd((unsigned long long*)&st.ts_hit[tau], 1ull);
+          if (q == Q_STRUCT) atomicAdd((unsigned long long*)&st.pb_hit[bin], 1ull);
+          if (j < np) atomicAdd(&s.matched, (uint32_t)b.ntok[bo + j]);
+          d.bacc[gi] += 1;
+        }
+        // O7/O8 touch: last = now, hint overwritten (A9, A10)
+        d.blast[gi] = now;
+        d.bmeta[gi] = meta_pack(q, tau, meta_ntok(meta));
+        d.bob[gi] = j;
+        d.bomax[gi] = omax;
+        if (q == Q_STRUCT) d.bps[gi] = p_struct(j, omax, st.par.gamma);
+      } else if (j >= h) {  // O9 miss-after-evict, consumed (A30)
+        const uint64_t H = b.h[bo + j];
+        const int32_t gp = tbl_find_pos(gkey, d.gmask, H);
+        if (gp >= 0) {
+          const uint32_t rp = gval[gp];
+          const uint32_t gtau = d.gtau[gb + rp];
+          if (gtau < 5) atomicAdd((unsigned long long*)&st.ts_mae[gtau], 1ull);
+          atomicAdd((unsigned long long*)&st.mae_by_type[gtau], 1ull);
+          gkey[gp] = KEY_TOMB;
+          d.glive[gb + rp] = 0;
+        }
+        fn = 1;
+      }
+    }
+    uint32_t rc, ra, rn;
+    block_scan3(fc, fa, fn, rc, ra, rn, s.tot, s.wsum);
+    if (fc) d.iv[((uint64_t)c.r * 2 + 0) * RMAX + (st.iv_head[0] + rc) % RMAX] = lnv;
+    if (fa) d.iv[((uint64_t)c.r * 2 + 1) * RMAX + (st.iv_head[1] + ra) % RMAX] = lnv;
+    if (valid) b.nrank[bo + j] = fn ? (int32_t)(new_base + rn) : -1;
+    new_base += s.tot[2];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int q = 0; q < 2; ++q) {
+        st.iv_head[q] = (st.iv_head[q] + s.tot[q]) % RMAX;
+        st.iv_len[q] = min(d.iv_ring, st.iv_len[q] + s.tot[q]);
+      }
+    }
+    __syncthreads();
+  }
+  // ---- O10 admission size (A11)
+  if (threadIdx.x == 0) {
+    const uint64_t f = d.C - st.live;
+    const uint64_t U = st.live - s.npin;
+    uint64_t k = new_base > f ? new_base - f : 0;
+    uint64_t admit = new_base;
+    if (k > U) { k = U; admit = f + U; }
+    s.k = k;
+    s.admit = admit;
+    if (k > 0) st.eviction_rounds++;
+    if (b.boff[i] + k > b.vcap) { st.err = (uint32_t)(-SAE_E_OVERFLOW); raise_err(d, SAE_E_OVERFLOW); }
+  }
+  __syncthreads();
+  if (st.err) return false;
+  const uint64_t k = s.k, admit = s.admit;
+  // ---- O11 evictions (Alg.1 Evict x k, chunked at K crossings)
+  if (k > 0) evict_k(c, k, stamp, b.o_vids ? b.o_vids + b.boff[i] : nullptr);
+  // ---- O12 insert New (Alg.1 Add: q.insert(b))
+  if (threadIdx.x == 0 && st.next_id + admit > 0xFFFFFFFFull) {
+    st.err = (uint32_t)(-SAE_E_OVERFLOW);
+    raise_err(d, SAE_E_OVERFLOW);
+  }
+  __syncthreads();
+  if (st.err) return false;
+  for (uint32_t j = threadIdx.x; j < n; j += NT) {
+    const int32_t rk = b.nrank[bo + j];
+    if (rk < 0 || (uint64_t)rk >= admit) continue;
+    const uint32_t sl = d.freestk[c.base + st.free_top - 1 - rk];
+    const uint64_t gi = c.base + sl;
+    const uint64_t H = b.h[bo + j];
+    const uint32_t q = b.q[bo + j], tau = b.tau[bo + j];
+    d.bhash[gi] = H;
+    d.blast[gi] = now;
+    d.bid[gi] = (uint32_t)(st.next_id + rk);
+    d.bacc[gi] = 1;
+    d.bmeta[gi] = meta_pack(q, tau, b.ntok[bo + j]);
+    d.bob[gi] = j;
+    d.bomax[gi] = omax;
+    d.bps[gi] = q == Q_STRUCT ? p_struct(j, omax, st.par.gamma) : 0.0;
+    tbl_insert(tkey, tval, d.tmask, H, sl, &st.tbl_used);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    st.free_top -= (uint32_t)admit;
+    st.live += (uint32_t)admit;
+    st.next_id += admit;
+    // ---- O13 outputs
+    if (b.o_hit) b.o_hit[i] = h;
+    if (b.o_miss) b.o_miss[i] = n - h;
+    if (b.o_matched) b.o_matched[i] = s.matched;
+    if (b.o_nvict) b.o_nvict[i] = (uint32_t)k;
+    st.requests++;
+    st.blocks_looked_up += n;
+    st.hit_blocks += h;
+    st.hit_tokens += s.matched;
+    st.prompt_tokens += L;
+  }
+  __syncthreads();
+  if (st.tbl_used > (d.tmask + 1) / 4 * 3) rebuild_table(c);
+  return true;
+}
+
+extern __shared__ __align__(16) unsigned char g_smem[];
+
+__device__ Ctx make_ctx(const Dev& d, uint32_t r) {
+  Ctx c;
+  c.d = &d;
+  c.s = reinterpret_cast<Smem*>(g_smem);
+  c.cand = reinterpret_cast<Cand*>(g_smem + ((sizeof(Smem) + 15) / 16) * 16);
+  c.r = r;
+  c.base = (uint64_t)r * d.C;
+  return c;
+}
+
+// Persistent replay: CTA r owns replica r and replays its run of the batch.
+__global__ void __launch_bounds__(NT, 1) k_replay(Dev d, BatchDev b) {
+  const uint32_t r = blockIdx.x;
+  if (r >= d.R) return;
+  Ctx c = make_ctx(d, r);
+  const uint32_t lo = b.run_start[r];
+  if (lo == 0xFFFFFFFFu) return;
+  const uint32_t hi = b.run_end[r];
+  load_state(c);
+  if (c.s->st.err == 0) {
+    for (uint32_t i = lo; i < hi; ++i)
+      if (!admit_one(c, b, i)) break;
+  }
+  store_state(c);
+}
+
+// sae_evict: Alg.1 Evict x k with an empty pin set.
+__global__ void __launch_bounds__(NT, 1) k_evict(Dev d, uint32_t r, uint32_t k, double now,
+                                                 uint32_t* vids, uint32_t* n_out) {
+  Ctx c = make_ctx(d, r);
+  load_state(c);
+  RState& st = c.s->st;
+  if (st.err == 0) {
+    if (st.has_now && now < st.now) {
+      if (threadIdx.x == 0) { st.err = (uint32_t)(-SAE_E_TIME); raise_err(d, SAE_E_TIME); }
+    } else {
+      __syncthreads();
+      if (threadIdx.x == 0) { st.now = now; st.has_now = 1; st.round++; }
+      __syncthreads();
+      const uint32_t kk = min(k, st.live);
+      if (kk > 0) {
+        if (threadIdx.x == 0) st.eviction_rounds++;
+        evict_k(c, kk, 0xFFFFFFFFu /* no block carries this stamp */, vids);
+      }
+      if (threadIdx.x == 0) {
+        if (n_out) *n_out = kk;
+        if (kk < k) raise_err(d, SAE_E_EMPTY);
+      }
+    }
+  }
+  store_state(c);
+}
+
+__global__ void __launch_bounds__(NT, 1) k_update(Dev d, uint32_t r0, uint32_t r1) {
+  const uint32_t r = r0 + blockIdx.x;
+  if (r >= r1) return;
+  Ctx c = make_ctx(d, r);
+  load_state(c);
+  learn(c);
+  store_state(c);
+}
+
+// read-only probe, one warp per request
+__global__ void k_lookup(Dev d, BatchDev b, uint32_t* out) {
+  const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= b.n) return;
+  const uint32_t r = b.replica[wid];
+  if (r >= d.R) return;
+  const uint32_t B = d.B;
+  const uint32_t n = (b.plen[wid] + B - 1) / B + (b.dlen[wid] + B - 1) / B;
+  const uint64_t bo = b.boff[wid], tb = (uint64_t)d.tmask + 1;
+  const uint64_t* tkey = d.tkey + (uint64_t)r * tb;
+  const uint32_t* tval = d.tval + (uint64_t)r * tb;
+  uint32_t h = n;
+  for (uint32_t j0 = 0; j0 < n; j0 += 32) {
+    const uint32_t j = j0 + lane;
+    bool miss = j < n && tbl_find(tkey, tval, d.tmask, b.h[bo + j]) < 0;
+    uint32_t bal = __ballot_sync(~0u, miss);
+    if (bal) { h = j0 + __ffs(bal) - 1; break; }
+  }
+  if (lane == 0) out[wid] = h;
+}
+
+__global__ void k_init(Dev d) {
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t RC = (uint64_t)d.R * d.C;
+  for (uint64_t i = tid; i < RC; i += stride) {
+    d.bmeta[i] = 0;
+    d.bpin[i] = 0;
+    d.freestk[i] = d.C - 1 - (uint32_t)(i % d.C);
+  }
+  const uint64_t TBn = (uint64_t)d.R * (d.tmask + 1ull);
+  for (uint64_t i = tid; i < TBn; i += stride) d.tkey[i] = KEY_EMPTY;
+  const uint64_t GTn = (uint64_t)d.R * (d.gmask + 1ull);
+  for (uint64_t i = tid; i < GTn; i += stride) d.gkey[i] = KEY_EMPTY;
+  const uint64_t RG = (uint64_t)d.R * d.G;
+  for (uint64_t i = tid; i < RG; i += stride) d.glive[i] = 0;
+}
+
+// params gather / scatter (all replicas) for multi-GPU parameter sync (NCCL all-gather)
+__global__ void k_params_gather(Dev d, sae_params* out) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < d.R; r += gridDim.x * blockDim.x)
+    out[r] = d.st[r].par;
+}
+// replace parameters; the cached p_struct of a replica is refreshed if its gamma changed
+__global__ void k_params_scatter(Dev d, const sae_params* in, uint32_t r0, uint32_t nr) {
+  const uint32_t r = r0 + blockIdx.y;
+  if (r >= d.R || blockIdx.y >= nr) return;
+  const double g_old = d.st[r].par.gamma;
+  const sae_params np = in[blockIdx.y];
+  __syncthreads();
+  const uint64_t base = (uint64_t)r * d.C;
+  if (np.gamma != g_old) {
+    for (uint32_t sl = blockIdx.x * blockDim.x + threadIdx.x; sl < d.C; sl += gridDim.x * blockDim.x) {
+      const uint32_t m = d.bmeta[base + sl];
+      if ((m & M_LIVE) && meta_q(m) == Q_STRUCT) d.bps[base + sl] = p_struct(d.bob[base + sl], d.bomax[base + sl], np.gamma);
+    }
+  }
+}
+__global__ void k_params_commit(Dev d, const sae_params* in, uint32_t r0, uint32_t nr) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += gridDim.x * blockDim.x)
+    if (r0 + i < d.R) d.st[r0 + i].par = in[i];
+}
+
+__global__ void k_count_queues(Dev d, uint32_t r, unsigned long long* out5) {
+  const uint64_t base = (uint64_t)r * d.C;
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < d.C; s += gridDim.x * blockDim.x) {
+    uint32_t m = d.bmeta[base + s];
+    if (m & M_LIVE) { atomicAdd(&out5[meta_q(m)], 1ull); atomicAdd(&out5[4], 1ull); }
+  }
+}
+
+__device__ __forceinline__ uint64_t sm64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+// K7: synthetic token materialisation, one CTA per piece (input generator)
+__global__ void k_gen_tokens(uint64_t seed, uint64_t np, const uint64_t* stream, const uint64_t* start,
+                             const uint32_t* len, const uint64_t* dst, const uint8_t* type,
+                             uint32_t* tokens, uint8_t* types) {
+  for (uint64_t p = blockIdx.x; p < np; p += gridDim.x) {
+    const uint64_t key = sm64(seed ^ sm64(stream[p]));
+    const uint64_t s0 = start[p], d0 = dst[p];
+    const uint32_t n = len[p];
+    const uint8_t ty = type[p];
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+      tokens[d0 + i] = (uint32_t)(sm64(key ^ (s0 + i)) & 0x1FFFFull);
+      types[d0 + i] = ty;
+    }
+  }
+}
+
+}  // namespace sae
+
+// ===========================================================================
+// Host side: C ABI
+// ===========================================================================
+using namespace sae;
+
+struct sae_ctx {
+  sae_config cfg;
+  Dev d;
+  int device;
+  std::string last_error;
+  uint64_t launches = 0;
+  // per-batch workspace (stream-ordered allocations)
+  void* ws = nullptr;
+  size_t ws_cap = 0;
+  std::vector<void*> allocs;
+};
+
+static uint32_t pow2_at_least(uint64_t x) {
+  uint64_t p = 1;
+  while (p < x) p <<= 1;
+  return (uint32_t)p;
+}
+
+#define CK(call)                                                        \
+  do {                                                                  \
+    cudaError_t e_ = (call);                                            \
+    if (e_ != cudaSuccess) {                                            \
+      if (ctx) ctx->last_error = std::string(#call ": ") + cudaGetErrorString(e_); \
+      return e_ == cudaErrorMemoryAllocation ? SAE_E_OOM : SAE_E_CUDA;  \
+    }                                                                   \
+  } while (0)
+
+template <class T>
+static cudaError_t dalloc(sae_ctx* ctx, T** p, uint64_t n) {
+  cudaError_t e = cudaMalloc((void**)p, (n ? n : 1) * sizeof(T));
+  if (e == cudaSuccess) ctx->allocs.push_back((void*)*p);
+  return e;
+}
+
+static size_t smem_bytes() {
+  return ((sizeof(Smem) + 15) / 16) * 16 + sizeof(Cand) * CAND_MAX;
+}
+
+extern "C" {
+
+sae_status sae_create(const sae_config* cfg, sae_ctx** out) {
+  sae_ctx* ctx = nullptr;
+  if (!cfg || !out) return SAE_E_INVAL;
+  if (cfg->abi_version != SAE_ABI_VERSION) return SAE_E_ABI;
+  if (cfg->capacity_blocks == 0) return SAE_E_CAPACITY_ZERO;
+  if (cfg->n_replicas == 0 || cfg->block_tokens == 0 || cfg->block_tokens > 16 || cfg->K == 0 ||
+      cfg->ghost_capacity == 0 || cfg->interval_ring == 0 || cfg->interval_ring > RMAX ||
+      cfg->n_pos_bins == 0 || cfg->n_pos_bins > 16 || cfg->capacity_blocks > SLOT_MASK)
+    return SAE_E_INVAL;
+  for (int q = 0; q < 2; ++q)
+    if (!(cfg->init.sigma[q] > 0.0)) return SAE_E_INVAL;
+  if (cfg->capacity_blocks > (uint32_t)CAND_MAX) return SAE_E_INVAL;  // v1: pool fits one CTA
+  ctx = new sae_ctx();
+  ctx->cfg = *cfg;
+  ctx->device = cfg->device;
+  CK(cudaSetDevice(cfg->device));
+  Dev& d = ctx->d;
+  std::memset(&d, 0, sizeof d);
+  d.R = cfg->n_replicas;
+  d.C = cfg->capacity_blocks;
+  d.G = cfg->ghost_capacity;
+  d.K = cfg->K;
+  d.iv_ring = cfg->interval_ring;
+  d.iv_keep = cfg->interval_keep;
+  d.iv_min = cfg->interval_min;
+  d.nbins = cfg->n_pos_bins;
+  d.B = cfg->block_tokens;
+  d.traj_cap = cfg->traj_capacity;
+  d.hash_seed = cfg->hash_seed;
+  d.dt_eps = cfg->dt_eps;
+  d.z_cut = cfg->z_cut;
+  const uint64_t TB = pow2_at_least(2ull * d.C), GT = pow2_at_least(2ull * d.G);
+  d.tmask = (uint32_t)(TB - 1);
+  d.gmask = (uint32_t)(GT - 1);
+  const uint64_t R = d.R, RC = R * d.C;
+  CK(dalloc(ctx, &d.st, R));
+  CK(dalloc(ctx, &d.bhash, RC));
+  CK(dalloc(ctx, &d.blast, RC));
+  CK(dalloc(ctx, &d.bid, RC));
+  CK(dalloc(ctx, &d.bmeta, RC));
+  CK(dalloc(ctx, &d.bob, RC));
+  CK(dalloc(ctx, &d.bomax, RC));
+  CK(dalloc(ctx, &d.bps, RC));
+  CK(dalloc(ctx, &d.bacc, RC));
+  CK(dalloc(ctx, &d.bpin, RC));
+  CK(dalloc(ctx, &d.freestk, RC));
+  CK(dalloc(ctx, &d.tkey, R * TB));
+  CK(dalloc(ctx, &d.tval, R * TB));
+  CK(dalloc(ctx, &d.ghash, R * d.G));
+  CK(dalloc(ctx, &d.gtau, R * d.G));
+  CK(dalloc(ctx, &d.glive, R * d.G));
+  CK(dalloc(ctx, &d.gtslot, R * d.G));
+  CK(dalloc(ctx, &d.gkey, R * GT));
+  CK(dalloc(ctx, &d.gval, R * GT));
+  CK(dalloc(ctx, &d.iv, R * 2 * RMAX));
+  CK(dalloc(ctx, &d.traj, R * (uint64_t)(d.traj_cap ? d.traj_cap : 1)));
+  CK(dalloc(ctx, &d.err, 1));
+  // initial scalar state
+  std::vector<RState> st(R);
+  for (uint64_t r = 0; r < R; ++r) {
+    RState s;
+    std::memset(&s, 0, sizeof s);
+    s.free_top = d.C;
+    s.par = cfg->init;
+    st[r] = s;
+  }
+  CK(cudaMemcpy(d.st, st.data(), R * sizeof(RState), cudaMemcpyHostToDevice));
+  CK(cudaMemset(d.err, 0, sizeof(uint32_t)));
+  k_init<<<1024, 256>>>(d);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  CK(cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes()));
+  CK(cudaFuncSetAttribute(k_evict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes()));
+  CK(cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes()));
+  CK(cudaDeviceSynchronize());
+  *out = ctx;
+  return SAE_OK;
+}
+
+sae_status sae_destroy(sae_ctx* ctx) {
+  if (!ctx) return SAE_E_INVAL;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  for (void* p : ctx->allocs) cudaFree(p);
+  if (ctx->ws) cudaFree(ctx->ws);
+  delete ctx;
+  return SAE_OK;
+}
+
+static sae_status scatter_params(sae_ctx* ctx, const sae_params* dev_in, uint32_t r0, uint32_t nr,
+                                 cudaStream_t s) {
+  dim3 grid(8, nr);
+  k_params_scatter<<<grid, 256, 0, s>>>(ctx->d, dev_in, r0, nr);
+  k_params_commit<<<(nr + 255) / 256, 256, 0, s>>>(ctx->d, dev_in, r0, nr);
+  ctx->launches += 2;
+  CK(cudaGetLastError());
+  return SAE_OK;
+}
+
+sae_status sae_set_params(sae_ctx* ctx, uint32_t replica, const sae_params* p, sae_stream st) {
+  if (!ctx || !p || replica >= ctx->d.R) return SAE_E_INVAL;
+  if (!(p->sigma[0] > 0.0) || !(p->sigma[1] > 0.0)) return SAE_E_INVAL;
+  cudaStream_t s = (cudaStream_t)st;
+  sae_params* tmp;
+  CK(cudaMallocAsync(&tmp, sizeof(sae_params), s));
+  CK(cudaMemcpyAsync(tmp, p, sizeof(sae_params), cudaMemcpyHostToDevice, s));
+  sae_status rc = scatter_params(ctx, tmp, replica, 1, s);
+  CK(cudaFreeAsync(tmp, s));
+  if (rc == SAE_OK) CK(cudaStreamSynchronize(s));  // p is a host pointer
+  return rc;
+}
+
+sae_status sae_params_gather(sae_ctx* ctx, sae_params* dev_out, sae_stream st) {
+  if (!ctx || !dev_out) return SAE_E_INVAL;
+  k_params_gather<<<(ctx->d.R + 255) / 256, 256, 0, (cudaStream_t)st>>>(ctx->d, dev_out);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  return SAE_OK;
+}
+
+sae_status sae_params_scatter(sae_ctx* ctx, const sae_params* dev_in, sae_stream st) {
+  if (!ctx || !dev_in) return SAE_E_INVAL;
+  return scatter_params(ctx, dev_in, 0, ctx->d.R, (cudaStream_t)st);
+}
+
+static BatchDev batch_dev(const sae_batch* b) {
+  BatchDev x;
+  std::memset(&x, 0, sizeof x);
+  x.n = b->n;
+  x.replica = b->replica;
+  x.arrival = b->arrival;
+  x.poff = b->prompt_off;
+  x.plen = b->prompt_len;
+  x.doff = b->decode_off;
+  x.dlen = b->decode_len;
+  x.tokens = b->tokens;
+  x.types = b->types;
+  x.flags = b->flags;
+  x.spb = b->shared_prefix_blocks;
+  return x;
+}
+
+// carve the per-batch workspace
+static sae_status prepare(sae_ctx* ctx, const sae_batch* b, BatchDev& x, cudaStream_t s,
+                          uint64_t total_blocks) {
+  const uint64_t n = b->n, R = ctx->d.R;
+  const uint32_t ntile = (uint32_t)((n + SCAN_TILE - 1) / SCAN_TILE);
+  auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
+  size_t need = al((n + 1) * 8) * 2 + al(ntile + 1) * 8 + al(total_blocks * 8) + al(total_blocks) * 3 +
+                al(total_blocks * 4) * 2 + al(R * 4) * 2;
+  if (need > ctx->ws_cap) {
+    if (ctx->ws) CK(cudaFreeAsync(ctx->ws, s));
+    ctx->ws = nullptr;
+    size_t cap = need + need / 4;
+    CK(cudaMallocAsync(&ctx->ws, cap, s));
+    ctx->ws_cap = cap;
+  }
+  char* p = (char*)ctx->ws;
+  auto take = [&](size_t bytes) { char* q = p; p += al(bytes); return (void*)q; };
+  uint64_t* cnt = (uint64_t*)take((n + 1) * 8);
+  x.boff = (uint64_t*)take((n + 1) * 8);
+  uint64_t* part = (uint64_t*)take((ntile + 1) * 8);
+  x.h = (uint64_t*)take(total_blocks * 8);
+  x.tau = (uint8_t*)take(total_blocks);
+  x.ntok = (uint8_t*)take(total_blocks);
+  x.q = (uint8_t*)take(total_blocks);
+  x.slot = (int32_t*)take(total_blocks * 4);
+  x.nrank = (int32_t*)take(total_blocks * 4);
+  x.run_start = (uint32_t*)take(R * 4);
+  x.run_end = (uint32_t*)take(R * 4);
+  if (n == 0) return SAE_OK;
+  k_nblocks<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, ctx->d.B, cnt);
+  k_scan_reduce<<<ntile, 1024, 0, s>>>(cnt, n, part);
+  k_scan_parts<<<1, 32, 0, s>>>(part, ntile);
+  k_scan_apply<<<ntile, 1024, 0, s>>>(cnt, n, part, x.boff, ntile);
+  CK(cudaMemsetAsync(x.run_start, 0xFF, R * 4, s));
+  CK(cudaMemsetAsync(x.run_end, 0, R * 4, s));
+  k_runs<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, ctx->d);
+  k_hash<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(x, ctx->d);
+  ctx->launches += 6;
+  CK(cudaGetLastError());
+  return SAE_OK;
+}
+
+sae_status sae_batch_blocks(sae_ctx* ctx, const sae_batch* b, uint64_t* total, sae_stream st) {
+  if (!ctx || !b || !total) return SAE_E_INVAL;
+  cudaStream_t s = (cudaStream_t)st;
+  const uint64_t n = b->n;
+  if (n == 0) { *total = 0; return SAE_OK; }
+  const uint32_t ntile = (uint32_t)((n + SCAN_TILE - 1) / SCAN_TILE);
+  uint64_t *cnt, *part;
+  CK(cudaMallocAsync(&cnt, (n + 1) * 8, s));
+  CK(cudaMallocAsync(&part, (ntile + 1) * 8, s));
+  BatchDev x = batch_dev(b);
+  k_nblocks<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, ctx->d.B, cnt);
+  k_scan_reduce<<<ntile, 1024, 0, s>>>(cnt, n, part);
+  k_scan_parts<<<1, 32, 0, s>>>(part, ntile);
+  ctx->launches += 3;
+  CK(cudaMemcpyAsync(total, part + ntile, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaFreeAsync(cnt, s));
+  CK(cudaFreeAsync(part, s));
+  CK(cudaStreamSynchronize(s));
+  return SAE_OK;
+}
+
+sae_status sae_admit_batch(sae_ctx* ctx, const sae_batch* b, sae_admit_out* o, sae_stream st) {
+  if (!ctx || !b || !o) return SAE_E_INVAL;
+  if (b->n && (!b->replica || !b->arrival || !b->prompt_off || !b->prompt_len || !b->decode_off ||
+               !b->decode_len || !b->tokens || !b->types || !b->flags || !b->shared_prefix_blocks))
+    return SAE_E_INVAL;
+  cudaStream_t s = (cudaStream_t)st;
+  CK(cudaSetDevice(ctx->device));
+  BatchDev x = batch_dev(b);
+  sae_status rc = prepare(ctx, b, x, s, b->total_blocks);
+  if (rc) return rc;
+  if (b->n == 0) return SAE_OK;
+  x.o_hit = o->hit_blocks;
+  x.o_miss = o->miss_blocks;
+  x.o_matched = o->matched_tokens;
+  x.o_nvict = o->n_victims;
+  x.o_voff = o->victim_off;
+  x.o_vids = o->victim_ids;
+  x.vcap = o->victim_ids ? o->victim_cap : ~0ull;
+  if (o->victim_off) CK(cudaMemcpyAsync(o->victim_off, x.boff, (b->n + 1) * 8, cudaMemcpyDeviceToDevice, s));
+  k_replay<<<ctx->d.R, NT, smem_bytes(), s>>>(ctx->d, x);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  if (o->block_hash) CK(cudaMemcpyAsync(o->block_hash, x.h, b->total_blocks * 8, cudaMemcpyDeviceToDevice, s));
+  if (o->block_tau) CK(cudaMemcpyAsync(o->block_tau, x.tau, b->total_blocks, cudaMemcpyDeviceToDevice, s));
+  return SAE_OK;
+}
+
+sae_status sae_lookup(sae_ctx* ctx, const sae_batch* b, uint32_t* hit, sae_stream st) {
+  if (!ctx || !b || !hit) return SAE_E_INVAL;
+  cudaStream_t s = (cudaStream_t)st;
+  BatchDev x = batch_dev(b);
+  sae_status rc = prepare(ctx, b, x, s, b->total_blocks);
+  if (rc) return rc;
+  if (b->n == 0) return SAE_OK;
+  k_lookup<<<(unsigned)((b->n * 32ull + 255) / 256), 256, 0, s>>>(ctx->d, x, hit);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  return SAE_OK;
+}
+
+sae_status sae_evict(sae_ctx* ctx, uint32_t replica, uint32_t k, double now, uint32_t* vids,
+                     uint32_t* n_out, sae_stream st) {
+  if (!ctx || replica >= ctx->d.R || (k > 0 && !vids)) return SAE_E_INVAL;
+  k_evict<<<1, NT, smem_bytes(), (cudaStream_t)st>>>(ctx->d, replica, k, now, vids, n_out);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  return SAE_OK;
+}
+
+sae_status sae_update(sae_ctx* ctx, uint32_t replica, sae_stream st) {
+  if (!ctx) return SAE_E_INVAL;
+  uint32_t r0 = replica, r1 = replica + 1;
+  if (replica == 0xFFFFFFFFu) { r0 = 0; r1 = ctx->d.R; }
+  else if (replica >= ctx->d.R) return SAE_E_INVAL;
+  k_update<<<r1 - r0, NT, smem_bytes(), (cudaStream_t)st>>>(ctx->d, r0, r1);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  return SAE_OK;
+}
+
+static sae_status take_sticky(sae_ctx* ctx, cudaStream_t s) {
+  uint32_t e = 0;
+  CK(cudaMemcpyAsync(&e, ctx->d.err, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (e) {
+    CK(cudaMemsetAsync(ctx->d.err, 0, 4, s));
+    CK(cudaStreamSynchronize(s));
+    ctx->last_error = "device error " + std::to_string(-(int)e);
+    return -(int)e;
+  }
+  return SAE_OK;
+}
+
+sae_status sae_sync(sae_ctx* ctx, sae_stream st) {
+  if (!ctx) return SAE_E_INVAL;
+  return take_sticky(ctx, (cudaStream_t)st);
+}
+
+sae_status sae_stats(sae_ctx* ctx, uint32_t replica, sae_replica_stats* out, sae_stream st) {
+  if (!ctx || !out || replica >= ctx->d.R) return SAE_E_INVAL;
+  cudaStream_t s = (cudaStream_t)st;
+  RState rs;
+  unsigned long long* q5;
+  CK(cudaMallocAsync(&q5, 5 * 8, s));
+  CK(cudaMemsetAsync(q5, 0, 5 * 8, s));
+  k_count_queues<<<64, 256, 0, s>>>(ctx->d, replica, q5);
+  ctx->launches++;
+  unsigned long long hq[5];
+  CK(cudaMemcpyAsync(hq, q5, 5 * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&rs, ctx->d.st + replica, sizeof rs, cudaMemcpyDeviceToHost, s));
+  CK(cudaFreeAsync(q5, s));
+  CK(cudaStreamSynchronize(s));
+  std::memset(out, 0, sizeof *out);
+  out->requests = rs.requests;
+  out->blocks_looked_up = rs.blocks_looked_up;
+  out->hit_blocks = rs.hit_blocks;
+  out->hit_tokens = rs.hit_tokens;
+  out->prompt_tokens = rs.prompt_tokens;
+  out->evictions = rs.evictions;
+  for (int i = 0; i < 4; ++i) out->evict_by_queue[i] = rs.evict_by_queue[i];
+  for (int i = 0; i < 6; ++i) { out->evict_by_type[i] = rs.evict_by_type[i]; out->mae_by_type[i] = rs.mae_by_type[i]; }
+  out->learner_firings = rs.learner_firings;
+  out->eviction_rounds = rs.eviction_rounds;
+  out->blocks_scored = rs.blocks_scored;
+  out->resident = hq[4];
+  for (int i = 0; i < 4; ++i) out->resident_by_queue[i] = hq[i];
+  out->E = rs.E;
+  out->next_id = rs.next_id;
+  out->gseq = rs.gseq;
+  out->now = rs.now;
+  for (int t = 0; t < 5; ++t) {
+    out->ts_ev[t] = rs.ts_ev[t]; out->ts_mae[t] = rs.ts_mae[t];
+    out->ts_hit[t] = rs.ts_hit[t]; out->ts_acc[t] = rs.ts_acc[t];
+  }
+  for (int q = 0; q < 3; ++q) { out->qh[q] = rs.qh[q]; out->qe[q] = rs.qe[q]; }
+  for (int i = 0; i < 16; ++i) { out->pb_hit[i] = rs.pb_hit[i]; out->pb_acc[i] = rs.pb_acc[i]; }
+  out->iv_len[0] = rs.iv_len[0];
+  out->iv_len[1] = rs.iv_len[1];
+  out->traj_count = rs.traj_n;
+  out->params = rs.par;
+  return take_sticky(ctx, s);
+}
+
+sae_status sae_get_traj(sae_ctx* ctx, uint32_t replica, sae_traj* out, uint64_t cap, uint64_t* n_out,
+                        sae_stream st) {
+  if (!ctx || replica >= ctx->d.R) return SAE_E_INVAL;
+  cudaStream_t s = (cudaStream_t)st;
+  RState rs;
+  CK(cudaMemcpyAsync(&rs, ctx->d.st + replica, sizeof rs, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const uint64_t tc = ctx->d.traj_cap;
+  uint64_t n = rs.traj_n < tc ? rs.traj_n : tc;
+  if (n > cap) n = cap;
+  if (n_out) *n_out = n;
+  if (!out || n == 0) return SAE_OK;
+  std::vector<sae_traj> all(tc);
+  CK(cudaMemcpyAsync(all.data(), ctx->d.traj + (uint64_t)replica * tc, tc * sizeof(sae_traj),
+                     cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  uint64_t first = rs.traj_n > tc ? rs.traj_n - tc : 0;
+  for (uint64_t i = 0; i < n; ++i) out[i] = all[(first + i) % tc];
+  return SAE_OK;
+}
+
+const char* sae_last_error(const sae_ctx* ctx) { return ctx ? ctx->last_error.c_str() : "null ctx"; }
+
+sae_status sae_gen_tokens(uint64_t seed, uint64_t n_pieces, const uint64_t* stream, const uint64_t* start,
+                          const uint32_t* len, const uint64_t* dst, const uint8_t* type, uint32_t* tokens,
+                          uint8_t* types, sae_stream st) {
+  sae_ctx* ctx = nullptr;
+  if (n_pieces == 0) return SAE_OK;
+  unsigned grid = (unsigned)(n_pieces < 65535ull * 8 ? n_pieces : 65535ull * 8);
+  k_gen_tokens<<<grid, 128, 0, (cudaStream_t)st>>>(seed, n_pieces, stream, start, len, dst, type, tokens, types);
+  CK(cudaGetLastError());
+  return SAE_OK;
+}
+
+uint64_t sae_launch_count(const sae_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+}  // extern "C"

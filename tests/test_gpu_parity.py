@@ -1,0 +1,176 @@
+"""-m gpu parity: the CUDA path (through the C ABI) vs the CPU oracle on the same
+seeded inputs, element by element: block hashes and types, per-request hit/miss/
+matched/victim counts, the victim-id sequence, every learner snapshot, final
+counters and parameters -- all bit-exact (SURVEY c.4: exactly one correct output)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2605_18825_b200 import configs as C
+from paper_2605_18825_b200 import sae as S
+from paper_2605_18825_b200 import tracegen as T
+from tests.gpu_helpers import (assert_params_equal, assert_stats_equal, assert_traj_equal,
+                               compare_replay, gpu_replay, u32, unpack)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c1():
+    return T.make("c1")
+
+
+@pytest.mark.parametrize("K", [8, 100])
+def test_c1_replay_bit_exact(c1, K):
+    compare_replay(c1, C.policy_config(64, K=K))
+
+
+@pytest.mark.parametrize("flags", [0, C.L_TOKENS, C.L_DEFAULT | C.L_TOKEN_MULT,
+                                   C.L_DEFAULT | C.L_QUEUE_RELATIVE])
+def test_c1_learner_variants(c1, flags):
+    p = dict(C.DEFAULT_PARAMS)
+    p["learn_flags"] = flags
+    compare_replay(c1, C.policy_config(64, K=8, params=p))
+
+
+def test_c1_small_ghost_and_tiny_capacity(c1):
+    compare_replay(c1, C.policy_config(16, K=5, ghost_capacity=7))
+
+
+def test_mix_traces_several_tiles_and_ragged():
+    # balanced and single-turn-dominant mixes, C spanning several 512-thread tiles
+    for mix, cap in ((C.MIX_BAL, 700), (C.MIX_ST, 1500), (C.MIX_MT, 2304)):
+        cfg = C.get("c2", n_requests=1500, mix=mix, seed=0x5AEC0100 + cap)
+        tr = T.generate(cfg)
+        T.materialize(tr)
+        compare_replay(tr, C.policy_config(cap, K=100))
+
+
+def test_c2_prefix_bit_exact():
+    tr = T.make("c2", n_requests=6000)
+    compare_replay(tr, C.policy_config(2304, K=100))
+
+
+def test_lookup_matches_oracle(c1):
+    pol = C.policy_config(64, K=8)
+    cache, b, out = gpu_replay(c1, pol, lo=0, hi=120)
+    R = oracle.Replica(pol)
+    R.replay(c1, 0, 120)
+    sub = T.single_batch(c1)
+    hits = u32(cache.lookup(S.batch_to_torch(sub)))
+    for i in range(c1["n"]):
+        po, pl = int(c1["prompt_off"][i]), int(c1["prompt_len"][i])
+        do, dl = int(c1["decode_off"][i]), int(c1["decode_len"][i])
+        assert hits[i] == R.lookup(c1["tokens"][po:po + pl], c1["types"][po:po + pl],
+                                   c1["tokens"][do:do + dl])
+    # lookup changes nothing
+    st = cache.stats(0)
+    assert st.requests == 120
+
+
+def test_evict_and_update_match_oracle(c1):
+    pol = C.policy_config(64, K=8)
+    cache, b, out = gpu_replay(c1, pol, lo=0, hi=100)
+    R = oracle.Replica(pol)
+    R.replay(c1, 0, 100)
+    now = float(c1["arrival"][99]) + 1.0
+    for k in (3, 10, 1):
+        ids, n = cache.evict(0, k, now)
+        rc, ref = R.evict(k, now)
+        assert rc == 0
+        assert int(n.item()) == len(ref)
+        assert list(u32(ids)[:len(ref)]) == list(ref)
+        now += 2.5
+    cache.update(0)
+    R.update()
+    st = cache.stats(0)
+    assert_params_equal(S.params_dict(st.params), R.params())
+    assert_stats_equal(st, R.stats())
+    assert_traj_equal(cache.traj(0), R.traj())
+
+
+def test_evict_empty_raises_sticky(c1):
+    pol = C.policy_config(64, K=8)
+    cache, b, out = gpu_replay(c1, pol, lo=0, hi=10)
+    live = cache.stats(0).resident
+    ids, n = cache.evict(0, int(live) + 5, float(c1["arrival"][9]) + 1)
+    with pytest.raises(S.SaeError) as e:
+        cache.sync()
+    assert e.value.status == -3
+    assert int(n.item()) == live
+
+
+def test_time_backwards_sticky(c1):
+    pol = C.policy_config(64, K=8)
+    cache, b, out = gpu_replay(c1, pol, lo=0, hi=20)
+    bad = T.single_batch(c1)
+    bad = {k: (v[:5] if hasattr(v, "__len__") and k not in ("tokens", "types") else v)
+           for k, v in bad.items()}
+    bad["n"] = 5
+    cache.admit_batch(S.batch_to_torch(bad))
+    with pytest.raises(S.SaeError) as e:
+        cache.sync()
+    assert e.value.status == -5
+
+
+def test_multi_replica_parameter_points():
+    """C5-shaped: several replicas (interleaved-free runs) with different parameter
+    points, each equal to its own oracle replay."""
+    cfg = C.get("c5", n_requests=800, capacity=256)
+    traces = []
+    for sd in range(2):
+        t = T.generate(C.get("c5", n_requests=800), seed=0x5AEC1000 + sd)
+        T.materialize(t)
+        traces.append(t)
+    R = 6
+    rep_of = [r % 2 for r in range(R)]
+    batch = T.replicate(traces, rep_of)
+    pol = C.policy_config(256, K=50)
+    cache = S.SaeCache(256, n_replicas=R, policy=pol, traj_capacity=1 << 14)
+    points = [0, 7, 29, 30, 31, 12]
+    for r in range(R):
+        cache.set_params(r, C.c5_point_params(points[r]))
+    b = S.batch_to_torch(batch)
+    out = cache.admit_batch(b)
+    torch.cuda.synchronize()
+    o4, _ = unpack(out, batch["n"])
+    vo = out["victim_off"].cpu().numpy()
+    vids = u32(out["victim_ids"])
+    off = 0
+    for r in range(R):
+        tr = traces[rep_of[r]]
+        p = dict(pol)
+        p["params"] = C.c5_point_params(points[r])
+        O = oracle.Replica(p)
+        ref = O.replay(tr)
+        n = tr["n"]
+        assert np.array_equal(o4[off:off + n], ref.out4), r
+        got = np.concatenate([vids[vo[off + i]:vo[off + i] + o4[off + i, 3]] for i in range(n)])
+        assert np.array_equal(got, ref.victims), r
+        st = cache.stats(r)
+        assert_stats_equal(st, ref.stats)
+        assert_traj_equal(cache.traj(r), ref.traj)
+        assert_params_equal(S.params_dict(st.params), O.params())
+        off += n
+
+
+def test_gen_tokens_matches_numpy():
+    tr = T.generate(C.get("c2", n_requests=500))
+    T.materialize(tr)
+    import numpy as np
+    P, D = tr["pieces"], tr["dpieces"]
+    # destination of each piece (same layout as tracegen.materialize)
+    def dst_of(pk, off, base):
+        po = tr[off]
+        req = np.repeat(np.arange(tr["n"]), np.diff(po))
+        cs = np.cumsum(tr[pk]["len"])
+        first = np.concatenate([[0], cs])[po[:-1]]
+        within = np.concatenate([[0], cs[:-1]]) - first[req]
+        return tr[base][req].astype(np.int64) + within
+    allp = {k: np.concatenate([P[k], D[k]]) for k in ("stream", "start", "len", "type")}
+    dst = np.concatenate([dst_of("pieces", "piece_off", "prompt_off"),
+                          dst_of("dpieces", "dpiece_off", "decode_off")])
+    tok, ty = S.gen_tokens(tr["tseed"], allp, dst, tr["n_tokens"])
+    assert np.array_equal(u32(tok)[:tr["n_tokens"]], tr["tokens"])
+    assert np.array_equal(ty.cpu().numpy()[:tr["n_tokens"]], tr["types"])
