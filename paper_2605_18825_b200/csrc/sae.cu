@@ -1519,9 +1519,13 @@ sae_status sae_get_traj(sae_ctx* ctx, uint32_t replica, sae_traj* out, uint64_t 
   CK(cudaStreamSynchronize(s));
   const uint64_t tc = ctx->d.traj_cap;
   uint64_t n = rs.traj_n < tc ? rs.traj_n : tc;
+  if (!out) {  // query the number available
+    if (n_out) *n_out = n;
+    return SAE_OK;
+  }
   if (n > cap) n = cap;
   if (n_out) *n_out = n;
-  if (!out || n == 0) return SAE_OK;
+  if (n == 0) return SAE_OK;
   std::vector<sae_traj> all(tc);
   CK(cudaMemcpyAsync(all.data(), ctx->d.traj + (uint64_t)replica * tc, tc * sizeof(sae_traj),
                      cudaMemcpyDeviceToHost, s));
