@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""bench.py — SAECache trace-replay throughput on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c2|c5]
+
+A "step" is one sae_admit_batch over one batch of requests of the workload's
+synthetic trace (all of §8(a): hash, lookup+touch, classify, score, select,
+evict, learn); the replay state carries across steps, as in a serving trace.
+Inputs are resident in HBM before the timed region; L2 is flushed (256 MiB
+write) between timed steps.  Under torchrun every rank replays its own seed of
+the workload (weak scaling, no data-path collective: the traces are independent).
+
+--impl reference times the CPU oracle (oracle/, the deliberately slow checker) on
+the same workload on the host cores; it is the reference arm of this tier.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2605_18825_b200 import configs as CFG  # noqa: E402
+from paper_2605_18825_b200 import tracegen as T  # noqa: E402
+
+WORKLOADS = {
+    "c2": dict(cfg="c2", per_step=5000, ref_step=1500,
+               desc="C2 multi-turn-dominated trace (Table 2 row 50/30/10/5/5), 100K requests, "
+                    "C=2304 blocks (36K tokens), 1 replica per GPU"),
+    "c5": dict(cfg="c5", per_step=250, ref_step=60,
+               desc="C5 parameter-sweep replicas: balanced trace, C=2304, 32 points x seeds, "
+                    "replicas per GPU = 1024/N"),
+}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", delete=False, suffix=".csv")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.flush()
+        rows = [l.strip().split(",") for l in open(self.f.name) if l.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+            except Exception:
+                continue
+            for nm, v in zip(names, r[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_trace(wl: dict, rank: int, n_requests: int | None = None, seed_shift: int = 0):
+    cfg = CFG.get(wl["cfg"])
+    if n_requests:
+        cfg["n_requests"] = n_requests
+    cfg["seed"] = cfg["seed"] + 0x1000 * rank + seed_shift
+    tr = T.generate(cfg)
+    T.materialize(tr)
+    tr["config"] = cfg
+    return tr
+
+
+def slice_batch(tr: dict, lo: int, hi: int, replica: int = 0) -> dict:
+    b = {k: tr[k][lo:hi] for k in ("arrival", "prompt_off", "prompt_len", "decode_off",
+                                   "decode_len", "flags", "spb")}
+    b["tokens"], b["types"], b["n"] = tr["tokens"], tr["types"], hi - lo
+    b["replica"] = np.full(hi - lo, replica, np.uint32)
+    return b
+
+
+# ------------------------------------------------------------------------------------
+def run_reference(args, wl, ws, rank):
+    """The oracle (as it stands) on the host cores: the reference arm."""
+    if rank != 0:
+        return
+    import oracle
+    n_need = wl["ref_step"] * (args.warmup + args.steps)
+    if wl["cfg"] == "c5":
+        tr = make_trace(wl, 0, n_requests=max(n_need, 1000))
+        pol = CFG.policy_config(tr["config"]["capacity"])
+    else:
+        tr = make_trace(wl, 0, n_requests=None)
+        pol = CFG.policy_config(tr["config"]["capacity"])
+    R = oracle.Replica(pol)
+    times, reqs = [], 0
+    pos = 0
+    for step in range(args.warmup + args.steps):
+        lo, hi = pos, min(pos + wl["ref_step"], tr["n"])
+        t0 = time.perf_counter()
+        res = R.replay(tr, lo, hi, want_hashes=False)
+        dt = time.perf_counter() - t0
+        pos = hi
+        if step >= args.warmup:
+            times.append(dt)
+            reqs += hi - lo
+    val = reqs / sum(times)
+    st = R.stats()
+    line = {
+        "impl": "reference", "metric": "requests replayed/s", "value": val, "unit": "req/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl["desc"], "requests_per_step": wl["ref_step"]},
+        "cpu_baseline": {"value": val, "unit": "req/s", "cores": 1, "kind": "oracle",
+                         "sample": "%d steps x %d requests of the %s trace after %d warm-up steps, "
+                                   "single thread" % (args.steps, wl["ref_step"], wl["cfg"],
+                                                      args.warmup)},
+        "e2e": {"value": val, "unit": "req/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "blocks_scored": int(st.blocks_scored),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(wl, tr, seconds: float = 15.0):
+    import oracle
+    pol = CFG.policy_config(tr["config"]["capacity"])
+    R = oracle.Replica(pol)
+    t0 = time.perf_counter()
+    pos, chunk = 0, 500
+    while time.perf_counter() - t0 < seconds and pos < tr["n"]:
+        R.replay(tr, pos, min(pos + chunk, tr["n"]), want_hashes=False)
+        pos = min(pos + chunk, tr["n"])
+    dt = time.perf_counter() - t0
+    return {"value": pos / dt, "unit": "req/s", "cores": 1, "kind": "oracle",
+            "sample": "first %d requests of the rank-0 %s trace (%.1f s, single thread)"
+                      % (pos, wl["cfg"], dt)}
+
+
+def run_ours(args, wl, ws, rank, local):
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist_
+        dist_.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = dist_
+    from paper_2605_18825_b200 import sae as S
+
+    W, K = args.warmup, args.steps
+    if wl["cfg"] == "c5":
+        R = 1024 // ws
+        per = wl["per_step"]
+        n_req = per * (W + 2 * K)
+        traces = []
+        seeds = sorted(set(((rank * R) + r) // 32 for r in range(R)))
+        for sd in seeds:
+            cfg = CFG.get("c5", n_requests=n_req)
+            t = T.generate(cfg, seed=0x5AEC1000 + sd)
+            T.materialize(t)
+            t["config"] = cfg
+            traces.append(t)
+        rep_of = [seeds.index(((rank * R) + r) // 32) for r in range(R)]
+        pol = CFG.policy_config(2304)
+        cache = S.SaeCache(2304, n_replicas=R, policy=pol)
+        for r in range(R):
+            cache.set_params(r, CFG.c5_point_params(((rank * R) + r) % 32))
+
+        def step_batch(step):
+            subs = [slice_batch(traces[rep_of[r]], step * per, (step + 1) * per, replica=r)
+                    for r in range(R)]
+            # shared arena: all replicas of one seed point into the same trace arena
+            offs = np.cumsum([0] + [t["n_tokens"] for t in traces])
+            out = {k: [] for k in ("arrival", "prompt_off", "prompt_len", "decode_off",
+                                   "decode_len", "flags", "spb", "replica")}
+            for r, sb in enumerate(subs):
+                o = np.uint64(offs[rep_of[r]])
+                for k in out:
+                    v = sb[k]
+                    if k in ("prompt_off", "decode_off"):
+                        v = v + o
+                    out[k].append(v)
+            bb = {k: np.concatenate(v) for k, v in out.items()}
+            bb["n"] = len(bb["arrival"])
+            return bb
+
+        arena_tok = np.concatenate([t["tokens"] for t in traces])
+        arena_typ = np.concatenate([t["types"] for t in traces])
+        tr0 = traces[0]
+    else:
+        R = 1
+        per = wl["per_step"]
+        tr0 = make_trace(wl, rank)
+        pol = CFG.policy_config(tr0["config"]["capacity"])
+        cache = S.SaeCache(pol["capacity"], n_replicas=1, policy=pol)
+
+        def step_batch(step):
+            return slice_batch(tr0, step * per, (step + 1) * per)
+
+        arena_tok, arena_typ = tr0["tokens"], tr0["types"]
+
+    dev = torch.device("cuda", local)
+    tok_d = torch.from_numpy(arena_tok.view(np.int32)).to(dev)
+    typ_d = torch.from_numpy(arena_typ).to(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def to_dev(bb):
+        x = S.batch_to_torch({**bb, "tokens": np.zeros(1, np.uint32), "types": np.zeros(1, np.uint8)},
+                             device=dev)
+        x["tokens"], x["types"] = tok_d, typ_d
+        return x
+
+    steps_dev = [to_dev(step_batch(s)) for s in range(W + K)]
+    outs = [cache.alloc_out(b) for b in steps_dev]
+    torch.cuda.synchronize()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    clk = Clocks(local)
+    # ---- device-resident timed steps
+    times = []
+    st0 = None
+    for s in range(W + K):
+        flush.zero_()
+        barrier()
+        torch.cuda.synchronize()
+        if s == W:
+            cache.sync()
+            st0 = [cache.stats(r) for r in range(R)]
+            l0 = cache.launches()
+            cache.profile(True)
+            cache.profile_read()
+            clk.start()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        cache.admit_batch(steps_dev[s], out=outs[s])
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        if s >= W:
+            times.append(e0.elapsed_time(e1))
+    clocks = clk.stop()
+    launches = cache.launches() - l0
+    rep_ms, rep_n = cache.profile_read()
+    cache.profile(False)
+    cache.sync()
+    st1 = [cache.stats(r) for r in range(R)]
+    tot_ms = sum(times)
+    d = lambda k: sum(getattr(b, k) - getattr(a, k) for a, b in zip(st0, st1))
+    req = d("requests")
+    scored, scored_struct = d("blocks_scored"), d("blocks_scored_struct")
+    hit_tok, prm_tok = d("hit_tokens"), d("prompt_tokens")
+    hit_blk, look = d("hit_blocks"), d("blocks_looked_up")
+
+    # ---- end to end through the public API with pinned host inputs (continuing the trace)
+    e2e_ms, h2d, d2h, e2e_req = 0.0, 0, 0, 0
+    host_steps = [step_batch(s) for s in range(W + K, W + 2 * K)]
+    tok_h = torch.from_numpy(arena_tok.view(np.int32)).pin_memory()
+    typ_h = torch.from_numpy(arena_typ).pin_memory()
+    for hb in host_steps:
+        hp = S.batch_to_torch({**hb, "tokens": np.zeros(1, np.uint32), "types": np.zeros(1, np.uint8)},
+                              pin=True)
+        a = int(hb["prompt_off"].min())
+        z = int((hb["decode_off"] + hb["decode_len"].astype(np.uint64)).max())
+        flush.zero_()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        res, nbytes_in, nbytes_out = cache.admit_batch_host(hp, tok_h, typ_h, tok_d, typ_d, a, z)
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        e2e_ms += e0.elapsed_time(e1)
+        h2d += nbytes_in
+        d2h += nbytes_out
+        e2e_req += hb["n"]
+
+    # ---- reduce over ranks (max time, summed work)
+    def allmax(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    tmax = allmax(tot_ms)
+    req_all = allsum(req)
+    e2e_tmax = allmax(e2e_ms)
+    e2e_all = allsum(e2e_req)
+    scored_all = allsum(scored)
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    hbm, src = peaks()
+    alg_bytes = 14.0 * scored + 8.0 * scored_struct
+    avg_ms = rep_ms / max(rep_n, 1)
+    achieved = (alg_bytes / max(rep_n, 1)) / (avg_ms * 1e-3) / 1e9 if rep_n else 0.0
+    traffic = None
+    pj = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(pj):
+        try:
+            traffic = json.load(open(pj)).get(wl["cfg"])
+        except Exception:
+            traffic = None
+    line = {
+        "metric": "requests replayed/s", "value": req_all / (tmax * 1e-3), "unit": "req/s",
+        "n_gpus": ws, "steps": K, "warmup": W, "ms_per_step": tmax / K,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": wl["desc"], "requests_per_step_per_gpu": int(req / K),
+                   "replicas_per_gpu": R, "capacity_blocks": int(pol["capacity"]),
+                   "l2": "flushed between timed steps (256 MiB device write)",
+                   "parallelism": "replicas%d" % ws},
+        "blocks_scored_per_s": scored_all / (tmax * 1e-3),
+        "hit_rate_tokens": hit_tok / max(prm_tok, 1),
+        "hit_rate_blocks": hit_blk / max(look, 1),
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "roofline": {"bound": "hbm", "kernel": "k_replay", "achieved": achieved, "peak": hbm,
+                     "peak_source": src, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": traffic,
+                     "algorithmic_bytes_per_launch": alg_bytes / max(rep_n, 1),
+                     "avg_launch_ms": avg_ms, "kernel_share_of_step": rep_ms / max(tot_ms, 1e-9)},
+        "e2e": {"value": e2e_all / (e2e_tmax * 1e-3), "unit": "req/s",
+                "h2d_bytes_per_step": int(h2d / K), "d2h_bytes_per_step": int(d2h / K)},
+    }
+    if ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(wl, tr0, seconds=args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    assert args.warmup >= 3 or args.impl == "reference" or os.environ.get("BENCH_ALLOW_FEW_WARMUP")
+    ws, rank, local = dist_setup()
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, wl, ws, rank)
+    else:
+        run_ours(args, wl, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -151,7 +151,7 @@ typedef struct {
 typedef struct {
   uint64_t requests, blocks_looked_up, hit_blocks, hit_tokens, prompt_tokens;
   uint64_t evictions, evict_by_queue[4], evict_by_type[6], mae_by_type[6];
-  uint64_t learner_firings, eviction_rounds, blocks_scored;
+  uint64_t learner_firings, eviction_rounds, blocks_scored, blocks_scored_struct;
   uint64_t resident, resident_by_queue[4];
   uint64_t E, next_id, gseq;
   double now;
@@ -225,6 +225,12 @@ sae_status sae_gen_tokens(uint64_t seed, uint64_t n_pieces, const uint64_t* stre
 
 /* Counts of device kernels launched by this ctx so far (for bench accounting). */
 uint64_t sae_launch_count(const sae_ctx* ctx);
+
+/* Profiling (bench roofline): when enabled, every replay-kernel launch is bracketed
+ * by CUDA events on its stream; sae_profile_read synchronizes, returns the summed
+ * elapsed milliseconds and the number of launches since the last read, and resets. */
+sae_status sae_profile(sae_ctx* ctx, int enable);
+sae_status sae_profile_read(sae_ctx* ctx, double* ms_total, uint64_t* n_launches);
 
 #ifdef __cplusplus
 }

@@ -37,6 +37,7 @@ constexpr uint64_t KEY_TOMB = ~0ull - 1;
 constexpr int NT = 512;            // threads per replay CTA
 constexpr int NW = NT / 32;
 constexpr int CAND_MAX = 4096;     // candidate buffer (smem) per CTA
+constexpr uint32_t SLACK = 16;     // extra candidates kept per segment across chunks (min)
 constexpr int RMAX = 4096;         // max interval ring
 constexpr uint32_t SLOT_MASK = 0x0FFFFFFFu;
 constexpr double INV_SQRT2 = 0.70710678118654757;  // 0x3FE6A09E667F3BCD
@@ -66,13 +67,15 @@ struct RState {
   // statistics
   uint64_t requests, blocks_looked_up, hit_blocks, hit_tokens, prompt_tokens, evictions;
   uint64_t evict_by_queue[4], evict_by_type[6], mae_by_type[6];
-  uint64_t learner_firings, eviction_rounds, blocks_scored;
+  uint64_t learner_firings, eviction_rounds, blocks_scored, blocks_scored_struct;
+  uint64_t thr[10];        // per-segment candidate thresholds on k0 (heuristic; exactness never depends on them)
   sae_params par;
 };
 
-struct Cand {           // one candidate victim: sort key (seg|tier, k0, k1, k2) + slot
+struct Cand {           // one candidate victim: sort key (tier, k0, k1, k2) + slot + segment
   uint64_t k0, k1;
-  uint32_t k2, ss;      // ss = slot | seg << 28
+  uint32_t k2, ss;      // ss = slot | tier << 28
+  uint32_t seg, pad;
 };
 
 struct Dev {
@@ -268,6 +271,51 @@ __device__ void block_sort(Cand* cand, int N) {
   }
 }
 
+__device__ __forceinline__ Cand shfl_cand(const Cand& x, int j) {
+  Cand y;
+  y.k0 = __shfl_xor_sync(~0u, x.k0, j);
+  y.k1 = __shfl_xor_sync(~0u, x.k1, j);
+  y.k2 = __shfl_xor_sync(~0u, x.k2, j);
+  y.ss = __shfl_xor_sync(~0u, x.ss, j);
+  y.seg = __shfl_xor_sync(~0u, x.seg, j);
+  return y;
+}
+
+// bitonic sort of a[0..N), 32 <= N <= NT (power of two): one element per thread held
+// in registers; strides < 32 exchange by warp shuffles, larger strides through smem.
+__device__ void sort_small(Cand* a, int N) {
+  const int t = threadIdx.x;
+  Cand x;
+  if (t < N) {
+    x = a[t];
+  } else {
+    x.k0 = ~0ull; x.k1 = ~0ull; x.k2 = ~0u; x.ss = ~0u;
+  }
+  for (int k = 2; k <= N; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      Cand y;
+      if (j >= 32) {
+        if (t < N) a[t] = x;
+        __syncthreads();
+        if (t < N) y = a[t ^ j]; else y = x;
+        __syncthreads();
+      } else {
+        y = shfl_cand(x, j);
+      }
+      const bool up = (t & k) == 0, lower = (t & j) == 0;
+      const bool take_y = (lower == up) ? cand_less(y, x) : cand_less(x, y);
+      if (take_y && t < N) x = y;
+    }
+  }
+  if (t < N) a[t] = x;
+  __syncthreads();
+}
+
+__device__ void sort_cands(Cand* a, int N) {
+  if (N <= NT) sort_small(a, N);
+  else block_sort(a, N);
+}
+
 // ---------------------------------------------------------------------------
 // Batch preparation kernels
 // ---------------------------------------------------------------------------
@@ -372,9 +420,10 @@ __global__ void __launch_bounds__(128) k_hash(BatchDev b, Dev d) {
 struct Smem {
   RState st;
   double cw[3][5];         // alpha_q * w_tau per scored queue (CHAT, AGENT, STRUCT)
-  uint32_t wsum[3 * NW];
+  uint32_t wsum[10 * NW];
   uint32_t tot[3];
-  uint32_t cnt[16], start[16];
+  uint32_t cnt[16], start[16], segtot[16], used[16];
+  uint32_t fail;
   uint32_t ncand;
   int32_t h;
   uint32_t npin, matched, nnew;
@@ -621,88 +670,158 @@ __device__ void rebuild_ghost(Ctx& c) {
 __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp) {
   const Dev& d = *c.d;
   Smem& s = *c.s;
-  const double now = s.st.now;
-  if (threadIdx.x < 16) s.cnt[threadIdx.x] = 0;
-  if (threadIdx.x == 0) s.ncand = 0;
-  __syncthreads();
-  for (uint32_t sl = threadIdx.x; sl < d.C; sl += NT) {
-    const uint64_t gi = c.base + sl;
-    const uint32_t meta = d.bmeta[gi];
-    if (!(meta & M_LIVE) || d.bpin[gi] == stamp) continue;
-    const uint32_t q = meta_q(meta), tau = meta_tau(meta);
-    Cand x;
-    uint32_t seg;
-    if (q == Q_EF) {
-      seg = 0;
-      x.k0 = ((uint64_t)meta_ntok(meta) << 32) | d.bid[gi];
-      x.k1 = 0;
-      x.k2 = 0;
-    } else if (q == Q_STRUCT) {
-      seg = 9;
-      double last = d.blast[gi];
-      double dt = __dsub_rn(now, last);
-      if (dt < d.dt_eps) dt = d.dt_eps;
-      double P = __ddiv_rn(__dmul_rn(s.cw[2][tau], d.bps[gi]), dt);
-      x.k0 = obits(P);
-      x.k1 = obits(last);
-      x.k2 = d.bid[gi];
-    } else {
-      seg = 1 + (q - 1) * 4 + (tau & 3);
-      x.k0 = obits(d.blast[gi]);
-      x.k1 = d.bid[gi];
-      x.k2 = 0;
-    }
-    x.ss = sl | (seg << 28);
-    uint32_t pos = atomicAdd(&s.ncand, 1u);
-    c.cand[pos] = x;
-    atomicAdd(&s.cnt[seg], 1u);
-  }
-  __syncthreads();
-  const uint32_t nc = s.ncand;
-  int N = 1;
-  while ((uint32_t)N < nc) N <<= 1;
-  for (uint32_t i = nc + threadIdx.x; i < (uint32_t)N; i += NT) {
-    c.cand[i].k0 = ~0ull; c.cand[i].k1 = ~0ull; c.cand[i].k2 = ~0u; c.cand[i].ss = 15u << 28;
-  }
-  if (threadIdx.x == 0) {
-    uint32_t run = 0;
-    for (int g = 0; g < 16; ++g) { s.start[g] = run; run += s.cnt[g]; }
-    s.st.blocks_scored += nc;
-  }
-  __syncthreads();
-  block_sort(c.cand, N);
-  const uint32_t e = min(m, s.cnt[0]);
-  const uint32_t mp = m - e;
-  // re-tier: 0 = EF head, 1 = scored candidate, 3 = out
-  for (uint32_t i = threadIdx.x; i < (uint32_t)N; i += NT) {
-    Cand x = c.cand[i];
-    uint32_t seg = x.ss >> 28, sl = x.ss & SLOT_MASK;
-    uint32_t rank = i - s.start[seg < 16 ? seg : 15];
-    uint32_t tier = 3;
-    if (seg == 0) {
-      tier = rank < e ? 0 : 3;
-    } else if (seg >= 1 && seg <= 8) {
-      if (rank < mp) {
+  RState& st = s.st;
+  const double now = st.now;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  uint32_t e = 0, mp = 0, c0 = 0;
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    if (tid < 16) { s.cnt[tid] = 0; s.segtot[tid] = 0; s.used[tid] = 0; }
+    if (tid == 0) { s.ncand = 0; s.fail = 0; }
+    __syncthreads();
+    // ---- one pass over the SoA: segment + key of every resident, unpinned block.
+    //      Blocks at or below their segment's carried threshold become candidates;
+    //      multi-turn candidates get their exact Eq.(1)/(3) score here.
+    for (uint32_t sl = tid; sl < d.C; sl += NT) {
+      const uint64_t gi = c.base + sl;
+      const uint32_t meta = d.bmeta[gi];
+      if (!(meta & M_LIVE) || d.bpin[gi] == stamp) continue;
+      const uint32_t q = meta_q(meta), tau = meta_tau(meta);
+      Cand x;
+      uint32_t seg, tier;
+      bool take;
+      if (q == Q_EF) {                      // Stage 1 key (num_tokens, id)
+        seg = 0;
+        tier = 0;
+        x.k0 = ((uint64_t)meta_ntok(meta) << 32) | d.bid[gi];
+        x.k1 = 0;
+        x.k2 = 0;
+        take = x.k0 <= st.thr[0];
+      } else if (q == Q_STRUCT) {           // Eq.(2)+(3) with the cached p_struct
+        seg = 9;
         tier = 1;
-        const uint32_t q = 1 + (seg - 1) / 4, tau = (seg - 1) & 3;
-        const double last = from_obits(x.k0);
+        const double last = d.blast[gi];
         double dt = __dsub_rn(now, last);
         if (dt < d.dt_eps) dt = d.dt_eps;
-        const double p = survival(dt, s.st.par.mu[q - 1], s.st.par.sigma[q - 1], d.z_cut);
-        const double P = __ddiv_rn(__dmul_rn(s.cw[q - 1][tau], p), dt);
-        x.k2 = (uint32_t)x.k1;  // id
-        x.k1 = x.k0;            // last
+        const double P = __ddiv_rn(__dmul_rn(s.cw[2][tau], d.bps[gi]), dt);
         x.k0 = obits(P);
+        x.k1 = obits(last);
+        x.k2 = d.bid[gi];
+        take = x.k0 <= st.thr[9];
+      } else {                              // multi-turn class (queue, tau): Eq.(1)+(3)
+        seg = 1 + (q - 1) * 4 + (tau & 3);
+        tier = 1;
+        const double last = d.blast[gi];
+        x.k1 = obits(last);
+        x.k2 = d.bid[gi];
+        take = x.k1 <= st.thr[seg];
+        if (take) {
+          double dt = __dsub_rn(now, last);
+          if (dt < d.dt_eps) dt = d.dt_eps;
+          const double p = survival(dt, st.par.mu[q - 1], st.par.sigma[q - 1], d.z_cut);
+          x.k0 = obits(__ddiv_rn(__dmul_rn(s.cw[q - 1][tau], p), dt));
+        }
       }
-    } else if (seg == 9) {
-      tier = rank < mp ? 1 : 3;
+      atomicAdd(&s.segtot[seg], 1u);
+      if (take) {
+        x.ss = sl | (tier << 28);
+        x.seg = seg;
+        const uint32_t pos = atomicAdd(&s.ncand, 1u);
+        c.cand[pos] = x;
+        atomicAdd(&s.cnt[seg], 1u);
+      }
     }
-    if (tier == 3) { x.k0 = ~0ull; x.k1 = ~0ull; x.k2 = ~0u; }
-    x.ss = sl | (tier << 28);
-    c.cand[i] = x;
+    __syncthreads();
+    const uint32_t nc = s.ncand;
+    int N = 32;
+    while ((uint32_t)N < nc) N <<= 1;
+    for (uint32_t i = nc + tid; i < (uint32_t)N; i += NT) {
+      c.cand[i].k0 = ~0ull; c.cand[i].k1 = ~0ull; c.cand[i].k2 = ~0u; c.cand[i].ss = 15u << 28;
+      c.cand[i].seg = 15;
+    }
+    if (tid == 0 && attempt == 0) {
+      uint32_t tot = 0;
+      for (int g = 0; g < 10; ++g) tot += s.segtot[g];
+      st.blocks_scored += tot;
+      st.blocks_scored_struct += s.segtot[9];
+    }
+    __syncthreads();
+    sort_cands(c.cand, N);          // (tier, P | (ntok,id), last, id)
+    c0 = s.cnt[0];
+    e = min(m, s.segtot[0]);
+    mp = m - e;
+    // ---- exactness check: every block a threshold left out must lose to the mp-th
+    //      scored candidate.  EF: enough heads.  Class c: a non-candidate has last > T_c,
+    //      so dt < now - T_c and, P being strictly decreasing in dt within a class,
+    //      P > P_c(now - T_c).  STRUCT: a non-candidate has P > T_S.
+    if (tid == 0 && c0 < e) atomicOr(&s.fail, 1u);
+    if (mp > 0 && tid >= 1 && tid <= 9 && s.segtot[tid] > s.cnt[tid]) {
+      const uint32_t g = tid;
+      const uint32_t S = nc - c0;
+      const double Pth = S >= mp ? from_obits(c.cand[c0 + mp - 1].k0)
+                                 : __longlong_as_double(0x7ff0000000000000ll);
+      bool ok;
+      if (g == 9) {
+        ok = Pth <= from_obits(st.thr[9]);
+      } else {
+        const uint32_t q = 1 + (g - 1) / 4, tau = (g - 1) & 3;
+        double dt = __dsub_rn(now, from_obits(st.thr[g]));
+        if (dt < d.dt_eps) dt = d.dt_eps;
+        const double p = survival(dt, st.par.mu[q - 1], st.par.sigma[q - 1], d.z_cut);
+        ok = Pth < __ddiv_rn(__dmul_rn(s.cw[q - 1][tau], p), dt);
+      }
+      if (!ok) atomicOr(&s.fail, 1u << g);
+    }
+    __syncthreads();
+    const uint32_t fail = s.fail;
+    if (fail == 0) break;
+    if (tid < 10 && (((fail >> tid) & 1u) || attempt >= 1)) st.thr[tid] = ~0ull;
+    __syncthreads();
   }
+  // ---- carry thresholds: keep about 2*used + SLACK candidates per segment.
+  //      EF is sorted contiguously at the front; tier 1 is ranked per segment.
+  const uint32_t nc = s.ncand;
+  if (tid == 0) {
+    const uint32_t want = 2 * e + SLACK;
+    if (c0 > want) st.thr[0] = c.cand[want - 1].k0;
+  }
+  for (uint32_t i = c0 + tid; i < c0 + mp; i += NT) atomicAdd(&s.used[c.cand[i].seg], 1u);
+  if (tid < 16) s.start[tid] = 0;   // running per-segment rank base
   __syncthreads();
-  block_sort(c.cand, N);
+  for (uint32_t i0 = c0; i0 < nc; i0 += NT) {
+    const uint32_t i = i0 + tid;
+    const uint32_t g = i < nc ? c.cand[i].seg : 15;
+    uint32_t myrank = 0;
+    for (uint32_t h = 1; h <= 9; ++h) {
+      const uint32_t bal = __ballot_sync(~0u, g == h);
+      if (g == h) myrank = __popc(bal & ((1u << lane) - 1u));
+      if (lane == 0) s.wsum[wid * 10 + (h - 1) % 10] = __popc(bal);
+    }
+    __syncthreads();
+    if (g >= 1 && g <= 9) {
+      uint32_t off = s.start[g];
+      for (int w = 0; w < wid; ++w) off += s.wsum[w * 10 + (g - 1)];
+      const uint32_t r = off + myrank, want = 2 * s.used[g] + SLACK;
+      if (r == want - 1 && s.cnt[g] > want) st.thr[g] = g == 9 ? c.cand[i].k0 : c.cand[i].k1;
+    }
+    __syncthreads();
+    if (tid >= 1 && tid <= 9) {
+      uint32_t t = 0;
+      for (int w = 0; w < NW; ++w) t += s.wsum[w * 10 + (tid - 1)];
+      s.start[tid] += t;
+    }
+    __syncthreads();
+  }
+  // ---- compact the victims into cand[0..m): EF heads then the mp scored heads
+  if (c0 > e && mp > 0) {
+    for (uint32_t v0 = 0; v0 < mp; v0 += NT) {   // dst < src: chunked read-then-write
+      Cand x;
+      const uint32_t v = v0 + tid;
+      if (v < mp) x = c.cand[c0 + v];
+      __syncthreads();
+      if (v < mp) c.cand[e + v] = x;
+      __syncthreads();
+    }
+  }
 }
 
 // Apply a chunk of m victims (cand[0..m) in eviction order): SURVEY c.2 O11 steps 1-4.
@@ -1152,6 +1271,9 @@ struct sae_ctx {
   void* ws = nullptr;
   size_t ws_cap = 0;
   std::vector<void*> allocs;
+  // optional profiling: CUDA events around every k_replay launch (bench roofline)
+  bool prof = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev;
 };
 
 static uint32_t pow2_at_least(uint64_t x) {
@@ -1245,6 +1367,7 @@ sae_status sae_create(const sae_config* cfg, sae_ctx** out) {
     RState s;
     std::memset(&s, 0, sizeof s);
     s.free_top = d.C;
+    for (int g = 0; g < 10; ++g) s.thr[g] = ~0ull;
     s.par = cfg->init;
     st[r] = s;
   }
@@ -1406,8 +1529,18 @@ sae_status sae_admit_batch(sae_ctx* ctx, const sae_batch* b, sae_admit_out* o, s
   x.o_vids = o->victim_ids;
   x.vcap = o->victim_ids ? o->victim_cap : ~0ull;
   if (o->victim_off) CK(cudaMemcpyAsync(o->victim_off, x.boff, (b->n + 1) * 8, cudaMemcpyDeviceToDevice, s));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (ctx->prof) {
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, s));
+  }
   k_replay<<<ctx->d.R, NT, smem_bytes(), s>>>(ctx->d, x);
   ctx->launches++;
+  if (ctx->prof) {
+    CK(cudaEventRecord(e1, s));
+    ctx->prof_ev.push_back({e0, e1});
+  }
   CK(cudaGetLastError());
   if (o->block_hash) CK(cudaMemcpyAsync(o->block_hash, x.h, b->total_blocks * 8, cudaMemcpyDeviceToDevice, s));
   if (o->block_tau) CK(cudaMemcpyAsync(o->block_tau, x.tau, b->total_blocks, cudaMemcpyDeviceToDevice, s));
@@ -1491,6 +1624,7 @@ sae_status sae_stats(sae_ctx* ctx, uint32_t replica, sae_replica_stats* out, sae
   out->learner_firings = rs.learner_firings;
   out->eviction_rounds = rs.eviction_rounds;
   out->blocks_scored = rs.blocks_scored;
+  out->blocks_scored_struct = rs.blocks_scored_struct;
   out->resident = hq[4];
   for (int i = 0; i < 4; ++i) out->resident_by_queue[i] = hq[i];
   out->E = rs.E;
@@ -1549,5 +1683,30 @@ sae_status sae_gen_tokens(uint64_t seed, uint64_t n_pieces, const uint64_t* stre
 }
 
 uint64_t sae_launch_count(const sae_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+sae_status sae_profile(sae_ctx* ctx, int enable) {
+  if (!ctx) return SAE_E_INVAL;
+  ctx->prof = enable != 0;
+  return SAE_OK;
+}
+
+sae_status sae_profile_read(sae_ctx* ctx, double* ms_total, uint64_t* n_launches) {
+  if (!ctx) return SAE_E_INVAL;
+  double tot = 0.0;
+  uint64_t n = 0;
+  for (auto& pr : ctx->prof_ev) {
+    CK(cudaEventSynchronize(pr.second));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, pr.first, pr.second));
+    tot += ms;
+    ++n;
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  ctx->prof_ev.clear();
+  if (ms_total) *ms_total = tot;
+  if (n_launches) *n_launches = n;
+  return SAE_OK;
+}
 
 }  // extern "C"

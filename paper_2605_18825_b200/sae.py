@@ -69,6 +69,7 @@ class sae_replica_stats(C.Structure):
                 ("evict_by_queue", C.c_uint64 * 4), ("evict_by_type", C.c_uint64 * 6),
                 ("mae_by_type", C.c_uint64 * 6), ("learner_firings", C.c_uint64),
                 ("eviction_rounds", C.c_uint64), ("blocks_scored", C.c_uint64),
+                ("blocks_scored_struct", C.c_uint64),
                 ("resident", C.c_uint64), ("resident_by_queue", C.c_uint64 * 4),
                 ("E", C.c_uint64), ("next_id", C.c_uint64), ("gseq", C.c_uint64),
                 ("now", C.c_double), ("ts_ev", C.c_uint64 * 5), ("ts_mae", C.c_uint64 * 5),
@@ -86,7 +87,7 @@ class sae_traj(C.Structure):
 EXPORTS = ["sae_create", "sae_destroy", "sae_set_params", "sae_params_gather", "sae_params_scatter",
            "sae_batch_blocks", "sae_admit_batch", "sae_lookup", "sae_evict", "sae_update",
            "sae_stats", "sae_get_traj", "sae_sync", "sae_last_error", "sae_gen_tokens",
-           "sae_launch_count"]
+           "sae_launch_count", "sae_profile", "sae_profile_read"]
 
 _lib = None
 
@@ -116,6 +117,8 @@ def lib():
             "sae_last_error": (C.c_char_p, [vp]),
             "sae_gen_tokens": (i32, [u64, u64, vp, vp, vp, vp, vp, vp, vp, vp]),
             "sae_launch_count": (u64, [vp]),
+            "sae_profile": (i32, [vp, i32]),
+            "sae_profile_read": (i32, [vp, P(C.c_double), P(u64)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -267,6 +270,49 @@ class SaeCache:
         self._check(lib().sae_admit_batch(self.h, C.byref(self._batch(b)), C.byref(ao), _stream(stream)))
         return out
 
+    def admit_batch_host(self, hb: dict, tok_h, typ_h, tok_d, typ_d, a: int, z: int, stream=None):
+        """End-to-end call with HOST (pinned) inputs: copy the step's request arrays and
+        its token range [a, z) host->device, replay, copy the results device->host.
+        Returns (host outputs, h2d bytes, d2h bytes)."""
+        dev = tok_d.device
+        st = self._staging = getattr(self, "_staging", {})
+        n = hb["n"]
+        db = {"n": n, "total_blocks": hb["total_blocks"], "tokens": tok_d, "types": typ_d}
+        h2d = 0
+        for k in ("replica", "arrival", "prompt_off", "prompt_len", "decode_off", "decode_len",
+                  "flags", "spb"):
+            t = hb[k]
+            buf = st.get(k)
+            if buf is None or buf.numel() < t.numel():
+                buf = st[k] = torch.empty(max(t.numel(), 1) * 2, dtype=t.dtype, device=dev)
+            buf[: t.numel()].copy_(t, non_blocking=True)
+            db[k] = buf[: t.numel()]
+            h2d += t.numel() * t.element_size()
+        tok_d[a:z].copy_(tok_h[a:z], non_blocking=True)
+        typ_d[a:z].copy_(typ_h[a:z], non_blocking=True)
+        h2d += (z - a) * 5
+        outd = st.get("out")
+        if outd is None or outd["victim_ids"].numel() < max(hb["total_blocks"], 1) or \
+                outd["hit_blocks"].numel() < n:
+            outd = st["out"] = self.alloc_out({"n": 2 * n, "total_blocks": 2 * hb["total_blocks"],
+                                               "arrival": db["arrival"]})
+        o = {k: v[: n] for k, v in outd.items() if k in ("hit_blocks", "miss_blocks",
+                                                          "matched_tokens", "n_victims")}
+        o["victim_off"] = outd["victim_off"][: n + 1]
+        o["victim_ids"] = outd["victim_ids"][: max(hb["total_blocks"], 1)]
+        self.admit_batch(db, out=o, stream=stream)
+        hout = st.get("hout")
+        if hout is None or hout["victim_ids"].numel() < outd["victim_ids"].numel():
+            hout = st["hout"] = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
+                                 for k, v in outd.items()}
+        res, d2h = {}, 0
+        for k, v in o.items():
+            hbuf = hout[k][: v.numel()]
+            hbuf.copy_(v, non_blocking=True)
+            res[k] = hbuf
+            d2h += v.numel() * v.element_size()
+        return res, h2d, d2h
+
     def lookup(self, b: dict, stream=None) -> torch.Tensor:
         hit = torch.empty(b["n"], dtype=torch.int32, device=b["arrival"].device)
         self._check(lib().sae_lookup(self.h, C.byref(self._batch(b)), hit.data_ptr(), _stream(stream)))
@@ -314,6 +360,16 @@ class SaeCache:
 
     def launches(self) -> int:
         return int(lib().sae_launch_count(self.h))
+
+    def profile(self, enable: bool = True):
+        self._check(lib().sae_profile(self.h, 1 if enable else 0))
+
+    def profile_read(self):
+        """(summed replay-kernel ms, number of replay launches) since the last read."""
+        ms = C.c_double()
+        n = C.c_uint64()
+        self._check(lib().sae_profile_read(self.h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
 
 
 def gen_tokens(seed: int, pieces: dict, dst: np.ndarray, n_tokens: int, device="cuda",
