@@ -160,6 +160,9 @@ typedef struct {
   uint64_t pb_hit[16], pb_acc[16];                   /* positional bins */
   uint64_t iv_len[2];                                /* reuse_intervals sizes */
   uint64_t traj_count;
+  /* select diagnostics: scan passes actually run (>= chunks; extra passes are threshold
+   * fallbacks), candidates sorted, passes with > 512 candidates, fallbacks per segment */
+  uint64_t select_passes, select_cands, select_big, select_fail_seg[10];
   sae_params params;
 } sae_replica_stats;
 

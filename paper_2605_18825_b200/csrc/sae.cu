@@ -37,7 +37,7 @@ constexpr uint64_t KEY_TOMB = ~0ull - 1;
 constexpr int NT = 512;            // threads per replay CTA
 constexpr int NW = NT / 32;
 constexpr int CAND_MAX = 4096;     // candidate buffer (smem) per CTA
-constexpr uint32_t SLACK = 16;     // extra candidates kept per segment across chunks (min)
+constexpr uint32_t SLACK = 32;     // extra candidates kept per segment across chunks (min)
 constexpr int RMAX = 4096;         // max interval ring
 constexpr uint32_t SLOT_MASK = 0x0FFFFFFFu;
 constexpr double INV_SQRT2 = 0.70710678118654757;  // 0x3FE6A09E667F3BCD
@@ -68,6 +68,7 @@ struct RState {
   uint64_t requests, blocks_looked_up, hit_blocks, hit_tokens, prompt_tokens, evictions;
   uint64_t evict_by_queue[4], evict_by_type[6], mae_by_type[6];
   uint64_t learner_firings, eviction_rounds, blocks_scored, blocks_scored_struct;
+  uint64_t select_passes, select_cands, select_big, select_fail_seg[10];
   uint64_t thr[10];        // per-segment candidate thresholds on k0 (heuristic; exactness never depends on them)
   sae_params par;
 };
@@ -281,38 +282,68 @@ __device__ __forceinline__ Cand shfl_cand(const Cand& x, int j) {
   return y;
 }
 
-// bitonic sort of a[0..N), 32 <= N <= NT (power of two): one element per thread held
-// in registers; strides < 32 exchange by warp shuffles, larger strides through smem.
-__device__ void sort_small(Cand* a, int N) {
+// Bitonic sort of a[0..N) (N a power of two, 32 <= N <= E*NT) with E elements per
+// thread held in registers: element e of thread t is index e*NT + t.  Strides >= NT
+// stay inside a thread, strides < 32 use warp shuffles, the rest go through smem.
+template <int E>
+__device__ void sort_reg(Cand* a, int N) {
   const int t = threadIdx.x;
-  Cand x;
-  if (t < N) {
-    x = a[t];
-  } else {
-    x.k0 = ~0ull; x.k1 = ~0ull; x.k2 = ~0u; x.ss = ~0u;
+  Cand x[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = e * NT + t;
+    if (i < N) {
+      x[e] = a[i];
+    } else {
+      x[e].k0 = ~0ull; x[e].k1 = ~0ull; x[e].k2 = ~0u; x[e].ss = ~0u; x[e].seg = 15;
+    }
   }
   for (int k = 2; k <= N; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
-      Cand y;
+      if (j >= NT) {
+        const int pe = j / NT;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          if ((e & pe) == 0 && (e | pe) < E) {
+            const int i = e * NT + t;
+            const bool up = (i & k) == 0;
+            Cand& lo = x[e];
+            Cand& hi = x[e | pe];
+            if (cand_less(hi, lo) == up) { Cand tmp = lo; lo = hi; hi = tmp; }
+          }
+        }
+        continue;
+      }
+      Cand y[E];
       if (j >= 32) {
-        if (t < N) a[t] = x;
+#pragma unroll
+        for (int e = 0; e < E; ++e) if (e * NT + t < N) a[e * NT + t] = x[e];
         __syncthreads();
-        if (t < N) y = a[t ^ j]; else y = x;
+#pragma unroll
+        for (int e = 0; e < E; ++e) y[e] = (e * NT + t < N) ? a[(e * NT + t) ^ j] : x[e];
         __syncthreads();
       } else {
-        y = shfl_cand(x, j);
+#pragma unroll
+        for (int e = 0; e < E; ++e) y[e] = shfl_cand(x[e], j);
       }
-      const bool up = (t & k) == 0, lower = (t & j) == 0;
-      const bool take_y = (lower == up) ? cand_less(y, x) : cand_less(x, y);
-      if (take_y && t < N) x = y;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = e * NT + t;
+        const bool up = (i & k) == 0, lower = (i & j) == 0;
+        const bool take_y = (lower == up) ? cand_less(y[e], x[e]) : cand_less(x[e], y[e]);
+        if (take_y && i < N) x[e] = y[e];
+      }
     }
   }
-  if (t < N) a[t] = x;
+#pragma unroll
+  for (int e = 0; e < E; ++e) if (e * NT + t < N) a[e * NT + t] = x[e];
   __syncthreads();
 }
 
 __device__ void sort_cands(Cand* a, int N) {
-  if (N <= NT) sort_small(a, N);
+  if (N <= NT) sort_reg<1>(a, N);
+  else if (N <= 2 * NT) sort_reg<2>(a, N);
+  else if (N <= 4 * NT) sort_reg<4>(a, N);
   else block_sort(a, N);
 }
 
@@ -738,6 +769,11 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp) {
       c.cand[i].k0 = ~0ull; c.cand[i].k1 = ~0ull; c.cand[i].k2 = ~0u; c.cand[i].ss = 15u << 28;
       c.cand[i].seg = 15;
     }
+    if (tid == 0) {
+      st.select_passes++;
+      st.select_cands += nc;
+      if (nc > (uint32_t)NT) st.select_big++;
+    }
     if (tid == 0 && attempt == 0) {
       uint32_t tot = 0;
       for (int g = 0; g < 10; ++g) tot += s.segtot[g];
@@ -774,14 +810,15 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp) {
     __syncthreads();
     const uint32_t fail = s.fail;
     if (fail == 0) break;
+    if (tid < 10 && ((fail >> tid) & 1u)) st.select_fail_seg[tid]++;
     if (tid < 10 && (((fail >> tid) & 1u) || attempt >= 1)) st.thr[tid] = ~0ull;
     __syncthreads();
   }
-  // ---- carry thresholds: keep about 2*used + SLACK candidates per segment.
+  // ---- carry thresholds: keep about 3*used + SLACK candidates per segment.
   //      EF is sorted contiguously at the front; tier 1 is ranked per segment.
   const uint32_t nc = s.ncand;
   if (tid == 0) {
-    const uint32_t want = 2 * e + SLACK;
+    const uint32_t want = 3 * e + SLACK;
     if (c0 > want) st.thr[0] = c.cand[want - 1].k0;
   }
   for (uint32_t i = c0 + tid; i < c0 + mp; i += NT) atomicAdd(&s.used[c.cand[i].seg], 1u);
@@ -800,7 +837,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp) {
     if (g >= 1 && g <= 9) {
       uint32_t off = s.start[g];
       for (int w = 0; w < wid; ++w) off += s.wsum[w * 10 + (g - 1)];
-      const uint32_t r = off + myrank, want = 2 * s.used[g] + SLACK;
+      const uint32_t r = off + myrank, want = 3 * s.used[g] + SLACK;
       if (r == want - 1 && s.cnt[g] > want) st.thr[g] = g == 9 ? c.cand[i].k0 : c.cand[i].k1;
     }
     __syncthreads();
@@ -1625,6 +1662,10 @@ sae_status sae_stats(sae_ctx* ctx, uint32_t replica, sae_replica_stats* out, sae
   out->eviction_rounds = rs.eviction_rounds;
   out->blocks_scored = rs.blocks_scored;
   out->blocks_scored_struct = rs.blocks_scored_struct;
+  out->select_passes = rs.select_passes;
+  out->select_cands = rs.select_cands;
+  out->select_big = rs.select_big;
+  for (int g = 0; g < 10; ++g) out->select_fail_seg[g] = rs.select_fail_seg[g];
   out->resident = hq[4];
   for (int i = 0; i < 4; ++i) out->resident_by_queue[i] = hq[i];
   out->E = rs.E;

@@ -75,7 +75,10 @@ class sae_replica_stats(C.Structure):
                 ("now", C.c_double), ("ts_ev", C.c_uint64 * 5), ("ts_mae", C.c_uint64 * 5),
                 ("ts_hit", C.c_uint64 * 5), ("ts_acc", C.c_uint64 * 5), ("qh", C.c_uint64 * 3),
                 ("qe", C.c_uint64 * 3), ("pb_hit", C.c_uint64 * 16), ("pb_acc", C.c_uint64 * 16),
-                ("iv_len", C.c_uint64 * 2), ("traj_count", C.c_uint64), ("params", sae_params)]
+                ("iv_len", C.c_uint64 * 2), ("traj_count", C.c_uint64),
+                ("select_passes", C.c_uint64), ("select_cands", C.c_uint64),
+                ("select_big", C.c_uint64), ("select_fail_seg", C.c_uint64 * 10),
+                ("params", sae_params)]
 
 
 class sae_traj(C.Structure):

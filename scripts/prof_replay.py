@@ -15,3 +15,6 @@ for lo, hi in ((0, n_warm), (n_warm, n_warm + n_prof)):
     cache.admit_batch(b)
     torch.cuda.synchronize()
 print("done", cache.stats(0).requests)
+st = cache.stats(0)
+print("chunks~", st.learner_firings, "passes", st.select_passes, "cands/pass", st.select_cands / max(st.select_passes, 1),
+      "big", st.select_big, "fails", list(st.select_fail_seg), "evictions", st.evictions, "rounds", st.eviction_rounds)
