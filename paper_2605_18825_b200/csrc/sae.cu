@@ -21,6 +21,7 @@
 //   k_gen_tokens (K7)     synthetic token materialisation (input generator)
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -38,6 +39,8 @@ constexpr int NT = 512;            // threads per replay CTA
 constexpr int NW = NT / 32;
 constexpr int CAND_MAX = 4096;     // candidate buffer (smem) per CTA
 constexpr uint32_t SLACK = 32;     // extra candidates kept per segment across chunks (min)
+constexpr int NSEG = 13;           // EF, 8 multi-turn classes (queue, tau), 4 STRUCT classes (tau)
+constexpr uint32_t MSUB = 192;     // victims selected per scan pass (keys are frozen within a chunk)
 constexpr int RMAX = 4096;         // max interval ring
 constexpr uint32_t SLOT_MASK = 0x0FFFFFFFu;
 constexpr double INV_SQRT2 = 0.70710678118654757;  // 0x3FE6A09E667F3BCD
@@ -69,7 +72,7 @@ struct RState {
   uint64_t evict_by_queue[4], evict_by_type[6], mae_by_type[6];
   uint64_t learner_firings, eviction_rounds, blocks_scored, blocks_scored_struct;
   uint64_t select_passes, select_cands, select_big, select_fail_seg[10];
-  uint64_t thr[10];        // per-segment candidate thresholds on k0 (heuristic; exactness never depends on them)
+  uint64_t thr[16];        // per-segment candidate thresholds on k0 (heuristic; exactness never depends on them)
   sae_params par;
 };
 
@@ -79,8 +82,29 @@ struct Cand {           // one candidate victim: sort key (tier, k0, k1, k2) + s
   uint32_t seg, pad;
 };
 
+// Control block of a multi-CTA replica group (global memory, one per replica).  The
+// leader CTA publishes a command + its parameters; all CTAs of the group execute their
+// partition of it between two group barriers.
+enum { CMD_SCAN = 1, CMD_HIST, CMD_COMPACT, CMD_REFRESH, CMD_CLEAR_T, CMD_FILL_T, CMD_CLEAR_G,
+       CMD_FILL_G, CMD_COUNTQ, CMD_EXIT };
+struct GroupCtl {
+  unsigned bar_count, bar_gen, cmd, stamp;
+  unsigned ncand, nsel, shift, active;
+  unsigned segtot[16], cnt[16], selcnt[16];
+  unsigned tblcnt, gtblcnt, cntq[4];
+  unsigned long long thr[16], pfx[16], pmask[16];
+  double now, gamma, dt_eps, z_cut;
+  double cw[3][5], mu[2], sigma[2];
+  unsigned hist[NSEG * 256];
+};
+
 struct Dev {
   uint32_t R, C, tmask, G, gmask, K, iv_ring, iv_keep, iv_min, nbins, B, traj_cap;
+  uint32_t GP;          // CTAs per replica (group size)
+  uint32_t cand_smem;   // 1: candidates live in the leader's smem (C <= CAND_MAX, GP == 1)
+  Cand* gcand;          // [R*C] global candidate buffer (large pools)
+  Cand* gsel;           // [R*CAND_MAX] compacted candidates after narrowing
+  GroupCtl* ctl;        // [R]
   uint64_t hash_seed;
   double dt_eps, z_cut;
   RState* st;
@@ -451,23 +475,23 @@ __global__ void __launch_bounds__(128) k_hash(BatchDev b, Dev d) {
 struct Smem {
   RState st;
   double cw[3][5];         // alpha_q * w_tau per scored queue (CHAT, AGENT, STRUCT)
-  uint32_t wsum[10 * NW];
+  uint32_t wsum[16 * NW];
   uint32_t tot[3];
   uint32_t cnt[16], start[16], segtot[16], used[16];
-  uint32_t fail;
-  uint32_t ncand;
+  uint32_t fail, ncand;
   int32_t h;
-  uint32_t npin, matched, nnew;
+  uint32_t npin, matched;
   uint64_t k, admit;
-  uint32_t flag;
-  double red[NW];
+  uint64_t pfx[16], pmask[16];
+  uint32_t below[16], target[16];
 };
 
-struct Ctx {               // per-CTA view of one replica
+struct Ctx {               // per-CTA view of one replica (group)
   const Dev* d;
   Smem* s;
   Cand* cand;
-  uint32_t r;
+  GroupCtl* ctl;
+  uint32_t r, rank, GP;
   uint64_t base;           // r * C
 };
 
@@ -478,15 +502,312 @@ __device__ void recompute_cw(Smem& s) {
   }
 }
 
+__device__ __forceinline__ uint32_t seg_of(uint32_t q, uint32_t tau) {
+  return q == Q_EF ? 0u : (q == Q_STRUCT ? 9u + (tau & 3u) : 1u + (q - 1u) * 4u + (tau & 3u));
+}
+// the key a segment's threshold applies to: (last) for multi-turn classes, k0 otherwise
+__device__ __forceinline__ uint64_t seg_key(const Cand& x) {
+  return (x.seg >= 1 && x.seg <= 8) ? x.k1 : x.k0;
+}
+__device__ __forceinline__ void part_range(uint64_t n, uint32_t rank, uint32_t GP, uint64_t& lo,
+                                           uint64_t& hi) {
+  lo = n * rank / GP;
+  hi = n * (rank + 1) / GP;
+}
+
+// ---------------------------------------------------------------------------
+// Group barrier over the GP CTAs of one replica (co-resident by cooperative launch).
+// ---------------------------------------------------------------------------
+__device__ void group_bar(Ctx& c) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    GroupCtl* g = c.ctl;
+    volatile unsigned* genp = &g->bar_gen;
+    const unsigned gen = *genp;
+    __threadfence();
+    if (atomicAdd(&g->bar_count, 1u) == c.GP - 1) {
+      atomicExch(&g->bar_count, 0u);
+      __threadfence();
+      atomicAdd(&g->bar_gen, 1u);
+    } else {
+      while (*genp == gen) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Parameters of a scan, from the leader's smem (leader) or the control block (workers).
+struct ScanP {
+  double now, dt_eps, z_cut;
+  uint32_t stamp;
+  const unsigned long long* thr;
+  const double* cw;        // [3][5]
+  const double* mu;
+  const double* sg;
+};
+
+// One pass over slots [lo, hi) of the replica's SoA: segment + key of every resident,
+// unpinned block (a4); those at or below the segment's threshold become candidates.
+// Counts go to smem (segtot, cnt); candidates to smem (cand_smem) or the global buffer.
+__device__ void scan_range(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P) {
+  const Dev& d = *c.d;
+  Smem& s = *c.s;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const bool gm = !d.cand_smem;
+  Cand* gdst = gm ? d.gcand + c.base : nullptr;
+  for (uint64_t i0 = lo; i0 < hi; i0 += NT) {
+    const uint64_t sl = i0 + tid;
+    bool take = false;
+    Cand x;
+    if (sl < hi) {
+      const uint64_t gi = c.base + sl;
+      const uint32_t meta = __ldcg(d.bmeta + gi);
+      if ((meta & M_LIVE) && __ldcg(d.bpin + gi) != P.stamp) {
+        const uint32_t q = meta_q(meta), tau = meta_tau(meta);
+        const uint32_t seg = seg_of(q, tau);
+        const uint32_t id = __ldcg(d.bid + gi);
+        if (q == Q_EF) {                      // Stage 1 key (num_tokens, id)
+          x.k0 = ((uint64_t)meta_ntok(meta) << 32) | id;
+          x.k1 = 0;
+          x.k2 = 0;
+          take = x.k0 <= P.thr[seg];
+        } else if (q == Q_STRUCT) {           // Eq.(2)+(3) with the cached p_struct
+          const double last = __ldcg(d.blast + gi);
+          double dt = __dsub_rn(P.now, last);
+          if (dt < P.dt_eps) dt = P.dt_eps;
+          const double Pv = __ddiv_rn(__dmul_rn(P.cw[10 + tau], __ldcg(d.bps + gi)), dt);
+          x.k0 = obits(Pv);
+          x.k1 = obits(last);
+          x.k2 = id;
+          take = x.k0 <= P.thr[seg];
+        } else {                              // multi-turn class (queue, tau): Eq.(1)+(3)
+          const double last = __ldcg(d.blast + gi);
+          x.k1 = obits(last);
+          x.k2 = id;
+          take = x.k1 <= P.thr[seg];
+          if (take) {
+            double dt = __dsub_rn(P.now, last);
+            if (dt < P.dt_eps) dt = P.dt_eps;
+            const double p = survival(dt, P.mu[q - 1], P.sg[q - 1], P.z_cut);
+            x.k0 = obits(__ddiv_rn(__dmul_rn(P.cw[(q - 1) * 5 + tau], p), dt));
+          }
+        }
+        x.ss = (uint32_t)sl | ((q == Q_EF ? 0u : 1u) << 28);
+        x.seg = seg;
+        atomicAdd(&s.segtot[seg], 1u);
+        if (take) atomicAdd(&s.cnt[seg], 1u);
+      }
+    }
+    if (gm) {
+      const uint32_t bal = __ballot_sync(~0u, take);
+      if (bal) {
+        uint32_t basep = 0;
+        if (lane == 0) basep = atomicAdd(&c.ctl->ncand, (unsigned)__popc(bal));
+        basep = __shfl_sync(~0u, basep, 0);
+        if (take) gdst[basep + __popc(bal & ((1u << lane) - 1u))] = x;
+      }
+    } else if (take) {
+      c.cand[atomicAdd(&s.ncand, 1u)] = x;
+    }
+  }
+}
+
+// stride-halving tree sum over y[0..P) in smem (SURVEY c.3 TREE)
+__device__ double tree_sum(double* y, int P);
+
+// Execute this CTA's share of a group command (all CTAs of the group, or the only CTA).
+__device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
+  const Dev& d = *c.d;
+  Smem& s = *c.s;
+  GroupCtl* g = c.ctl;
+  const int tid = threadIdx.x;
+  uint64_t lo, hi;
+  switch (cmd) {
+    case CMD_SCAN: {
+      if (tid < 16) { s.segtot[tid] = 0; s.cnt[tid] = 0; }
+      if (tid == 0) s.ncand = 0;
+      __syncthreads();
+      ScanP P;
+      if (leader) {   // the leader scans with its own smem copies
+        P.now = s.st.now;
+        P.thr = (const unsigned long long*)s.st.thr; P.cw = &s.cw[0][0];
+        P.mu = s.st.par.mu; P.sg = s.st.par.sigma;
+      } else {        // published by the leader before the command
+        P.now = __ldcg(&g->now);
+        P.thr = g->thr; P.cw = &g->cw[0][0]; P.mu = g->mu; P.sg = g->sigma;
+      }
+      P.stamp = __ldcg(&g->stamp);
+      P.dt_eps = d.dt_eps;
+      P.z_cut = d.z_cut;
+      part_range(d.C, c.rank, c.GP, lo, hi);
+      scan_range(c, lo, hi, P);
+      __syncthreads();
+      if (!d.cand_smem && tid < NSEG) {
+        if (s.segtot[tid]) atomicAdd(&g->segtot[tid], s.segtot[tid]);
+        if (s.cnt[tid]) atomicAdd(&g->cnt[tid], s.cnt[tid]);
+      }
+      break;
+    }
+    case CMD_HIST: {   // radix histograms of the active segments' keys (global candidates)
+      unsigned* h = reinterpret_cast<unsigned*>(c.cand);
+      for (int i = tid; i < NSEG * 256; i += NT) h[i] = 0;
+      __syncthreads();
+      const unsigned shift = __ldcg(&g->shift), active = __ldcg(&g->active);
+      part_range(__ldcg(&g->ncand), c.rank, c.GP, lo, hi);
+      const Cand* src = d.gcand + c.base;
+      for (uint64_t i = lo + tid; i < hi; i += NT) {
+        const uint32_t seg = __ldcg(&src[i].seg);
+        if (!((active >> seg) & 1u)) continue;
+        const uint64_t key = seg >= 1 && seg <= 8 ? __ldcg(&src[i].k1) : __ldcg(&src[i].k0);
+        if ((key & __ldcg(&g->pmask[seg])) != __ldcg(&g->pfx[seg])) continue;
+        atomicAdd(&h[seg * 256 + ((key >> shift) & 255u)], 1u);
+      }
+      __syncthreads();
+      for (int i = tid; i < NSEG * 256; i += NT)
+        if (h[i]) atomicAdd(&g->hist[i], h[i]);
+      __syncthreads();
+      break;
+    }
+    case CMD_COMPACT: {  // keep candidates at or below the (new) thresholds
+      part_range(__ldcg(&g->ncand), c.rank, c.GP, lo, hi);
+      const Cand* src = d.gcand + c.base;
+      Cand* dst = d.gsel + (uint64_t)c.r * CAND_MAX;
+      const int lane = tid & 31;
+      for (uint64_t i0 = lo; i0 < hi; i0 += NT) {
+        const uint64_t i = i0 + tid;
+        bool take = false;
+        Cand x;
+        if (i < hi) {
+          x.k0 = __ldcg(&src[i].k0); x.k1 = __ldcg(&src[i].k1);
+          x.k2 = __ldcg(&src[i].k2); x.ss = __ldcg(&src[i].ss); x.seg = __ldcg(&src[i].seg);
+          take = seg_key(x) <= __ldcg(&g->thr[x.seg]);
+        }
+        const uint32_t bal = __ballot_sync(~0u, take);
+        if (bal) {
+          uint32_t basep = 0;
+          if (lane == 0) basep = atomicAdd(&g->nsel, (unsigned)__popc(bal));
+          basep = __shfl_sync(~0u, basep, 0);
+          const uint32_t pos = basep + __popc(bal & ((1u << lane) - 1u));
+          if (take) {
+            atomicAdd(&g->selcnt[x.seg], 1u);
+            if (pos < (uint32_t)CAND_MAX) dst[pos] = x;
+          }
+        }
+      }
+      break;
+    }
+    case CMD_REFRESH: {  // gamma changed: recompute the cached structural priorities
+      const double gam = leader ? s.st.par.gamma : __ldcg(&g->gamma);
+      part_range(d.C, c.rank, c.GP, lo, hi);
+      for (uint64_t sl = lo + tid; sl < hi; sl += NT) {
+        const uint64_t gi = c.base + sl;
+        const uint32_t m = __ldcg(d.bmeta + gi);
+        if ((m & M_LIVE) && meta_q(m) == Q_STRUCT)
+          d.bps[gi] = p_struct(__ldcg(d.bob + gi), __ldcg(d.bomax + gi), gam);
+      }
+      break;
+    }
+    case CMD_CLEAR_T: {
+      const uint64_t tb = (uint64_t)d.tmask + 1;
+      part_range(tb, c.rank, c.GP, lo, hi);
+      uint64_t* keys = d.tkey + (uint64_t)c.r * tb;
+      for (uint64_t i = lo + tid; i < hi; i += NT) keys[i] = KEY_EMPTY;
+      break;
+    }
+    case CMD_FILL_T: {
+      const uint64_t tb = (uint64_t)d.tmask + 1;
+      part_range(d.C, c.rank, c.GP, lo, hi);
+      uint64_t* keys = d.tkey + (uint64_t)c.r * tb;
+      uint32_t* vals = d.tval + (uint64_t)c.r * tb;
+      for (uint64_t sl = lo + tid; sl < hi; sl += NT) {
+        const uint64_t gi = c.base + sl;
+        if (__ldcg(d.bmeta + gi) & M_LIVE)
+          tbl_insert(keys, vals, d.tmask, __ldcg(d.bhash + gi), (uint32_t)sl, &g->tblcnt);
+      }
+      break;
+    }
+    case CMD_CLEAR_G: {
+      const uint64_t gt = (uint64_t)d.gmask + 1;
+      part_range(gt, c.rank, c.GP, lo, hi);
+      uint64_t* keys = d.gkey + (uint64_t)c.r * gt;
+      for (uint64_t i = lo + tid; i < hi; i += NT) keys[i] = KEY_EMPTY;
+      break;
+    }
+    case CMD_FILL_G: {
+      const uint64_t gt = (uint64_t)d.gmask + 1, gb = (uint64_t)c.r * d.G;
+      part_range(d.G, c.rank, c.GP, lo, hi);
+      uint64_t* keys = d.gkey + (uint64_t)c.r * gt;
+      uint32_t* vals = d.gval + (uint64_t)c.r * gt;
+      for (uint64_t p = lo + tid; p < hi; p += NT)
+        if (__ldcg(d.glive + gb + p))
+          d.gtslot[gb + p] = tbl_insert(keys, vals, d.gmask, __ldcg(d.ghash + gb + p), (uint32_t)p, &g->gtblcnt);
+      break;
+    }
+    case CMD_COUNTQ: {
+      if (tid < 4) s.cnt[tid] = 0;
+      __syncthreads();
+      part_range(d.C, c.rank, c.GP, lo, hi);
+      for (uint64_t sl = lo + tid; sl < hi; sl += NT) {
+        const uint32_t m = __ldcg(d.bmeta + c.base + sl);
+        if (m & M_LIVE) atomicAdd(&s.cnt[meta_q(m)], 1u);
+      }
+      __syncthreads();
+      if (tid < 4 && s.cnt[tid]) atomicAdd(&g->cntq[tid], s.cnt[tid]);
+      break;
+    }
+    default:
+      break;
+  }
+  __syncthreads();
+}
+
+// Leader: run a command on the whole group (GP == 1: just run it over everything).
+__device__ void issue(Ctx& c, unsigned cmd) {
+  if (c.GP == 1) {
+    run_cmd(c, cmd, true);
+    return;
+  }
+  if (threadIdx.x == 0) c.ctl->cmd = cmd;
+  group_bar(c);                 // workers start
+  if (cmd == CMD_EXIT) return;
+  run_cmd(c, cmd, true);
+  group_bar(c);                 // everyone done
+}
+
+__device__ void worker_loop(Ctx& c) {
+  while (true) {
+    group_bar(c);
+    const unsigned cmd = __ldcg(&c.ctl->cmd);
+    if (cmd == CMD_EXIT) return;
+    run_cmd(c, cmd, false);
+    group_bar(c);
+  }
+}
+
 // Recompute the cached structural priority of every live STRUCT block (gamma changed).
 __device__ void refresh_pstruct(Ctx& c) {
-  const Dev& d = *c.d;
-  const double gam = c.s->st.par.gamma;
-  for (uint32_t sl = threadIdx.x; sl < d.C; sl += NT) {
-    uint64_t gi = c.base + sl;
-    uint32_t m = d.bmeta[gi];
-    if ((m & M_LIVE) && meta_q(m) == Q_STRUCT) d.bps[gi] = p_struct(d.bob[gi], d.bomax[gi], gam);
-  }
+  if (threadIdx.x == 0) c.ctl->gamma = c.s->st.par.gamma;
+  __syncthreads();
+  issue(c, CMD_REFRESH);
+}
+
+// Rebuild the resident table (tombstone cleanup) from the live SoA.
+__device__ void rebuild_table(Ctx& c) {
+  if (threadIdx.x == 0) c.ctl->tblcnt = 0;
+  __syncthreads();
+  issue(c, CMD_CLEAR_T);
+  issue(c, CMD_FILL_T);
+  if (threadIdx.x == 0) c.s->st.tbl_used = __ldcg(&c.ctl->tblcnt);
+  __syncthreads();
+}
+__device__ void rebuild_ghost(Ctx& c) {
+  if (threadIdx.x == 0) c.ctl->gtblcnt = 0;
+  __syncthreads();
+  issue(c, CMD_CLEAR_G);
+  issue(c, CMD_FILL_G);
+  if (threadIdx.x == 0) c.s->st.gtbl_used = __ldcg(&c.ctl->gtblcnt);
+  __syncthreads();
 }
 
 // stride-halving tree sum over y[0..P) in smem (SURVEY c.3 TREE)
@@ -537,12 +858,10 @@ __device__ void learn(Ctx& c) {
   // L2 QueueWeights (Alg. P:575-597 or relative rule P:814-817)
   if (f & SAE_L_QUEUES) {
     if (f & SAE_L_QUEUE_RELATIVE) {
-      if (threadIdx.x < 3) s.cnt[threadIdx.x] = 0;
+      if (threadIdx.x < 4) c.ctl->cntq[threadIdx.x] = 0;
       __syncthreads();
-      for (uint32_t sl = threadIdx.x; sl < d.C; sl += NT) {
-        uint32_t m = d.bmeta[c.base + sl];
-        if ((m & M_LIVE) && meta_q(m) != Q_EF) atomicAdd(&s.cnt[meta_q(m) - 1], 1u);
-      }
+      issue(c, CMD_COUNTQ);
+      if (threadIdx.x < 3) s.cnt[threadIdx.x] = __ldcg(&c.ctl->cntq[threadIdx.x + 1]);
       __syncthreads();
       if (threadIdx.x == 0) {
         double Eq[3];
@@ -638,8 +957,18 @@ __device__ void learn(Ctx& c) {
     }
   }
   __syncthreads();
+  double cw_old[4];
+  for (int t = 0; t < 4; ++t) cw_old[t] = s.cw[2][t];
   if (p.gamma != gamma_old) refresh_pstruct(c);
   recompute_cw(s);
+  __syncthreads();
+  // STRUCT-class thresholds follow a pure rescaling of alpha*w (heuristic only; the
+  // exactness check in select_chunk never depends on them)
+  if (threadIdx.x < 4 && p.gamma == gamma_old && st.thr[9 + threadIdx.x] != ~0ull &&
+      s.cw[2][threadIdx.x] != cw_old[threadIdx.x] && cw_old[threadIdx.x] > 0.0) {
+    const double T = from_obits(st.thr[9 + threadIdx.x]);
+    st.thr[9 + threadIdx.x] = obits(T * (s.cw[2][threadIdx.x] / cw_old[threadIdx.x]) * (1.0 + 0x1p-40));
+  }
   if (threadIdx.x == 0) {
     st.learner_firings++;
     if (d.traj_cap > 0) {
@@ -657,111 +986,60 @@ __device__ void learn(Ctx& c) {
   __syncthreads();
 }
 
-// Rebuild the resident table (tombstone cleanup) from the live SoA.
-__device__ void rebuild_table(Ctx& c) {
-  const Dev& d = *c.d;
-  const uint64_t tb = (uint64_t)d.tmask + 1;
-  uint64_t* keys = d.tkey + (uint64_t)c.r * tb;
-  uint32_t* vals = d.tval + (uint64_t)c.r * tb;
-  for (uint64_t i = threadIdx.x; i < tb; i += NT) keys[i] = KEY_EMPTY;
-  if (threadIdx.x == 0) c.s->st.tbl_used = 0;
-  __syncthreads();
-  for (uint32_t sl = threadIdx.x; sl < d.C; sl += NT) {
-    uint64_t gi = c.base + sl;
-    if (d.bmeta[gi] & M_LIVE) tbl_insert(keys, vals, d.tmask, d.bhash[gi], sl, &c.s->st.tbl_used);
-  }
-  __syncthreads();
-}
-__device__ void rebuild_ghost(Ctx& c) {
-  const Dev& d = *c.d;
-  const uint64_t gt = (uint64_t)d.gmask + 1;
-  uint64_t* keys = d.gkey + (uint64_t)c.r * gt;
-  uint32_t* vals = d.gval + (uint64_t)c.r * gt;
-  for (uint64_t i = threadIdx.x; i < gt; i += NT) keys[i] = KEY_EMPTY;
-  if (threadIdx.x == 0) c.s->st.gtbl_used = 0;
-  __syncthreads();
-  const uint64_t gb = (uint64_t)c.r * d.G;
-  for (uint32_t p = threadIdx.x; p < d.G; p += NT) {
-    if (d.glive[gb + p]) d.gtslot[gb + p] = tbl_insert(keys, vals, d.gmask, d.ghash[gb + p], p, &c.s->st.gtbl_used);
-  }
-  __syncthreads();
-}
+// ---------------------------------------------------------------------------
+// Fused score + select (a4 + a5) for one chunk of m <= MSUB victims (no learner firing
+// inside).  Exact: key = (tier, primary, last, id) per SURVEY c.2 O11.  One pass over
+// the SoA (split over the group's CTAs) computes every resident, unpinned block's
+// segment (EF / 8 multi-turn classes (queue, tau) / 4 STRUCT classes (tau)) and key:
+// EF (ntok, id); multi-turn (last, id) -- P is strictly decreasing in dt within a class
+// (§8(a) a4), so only class heads need Eq.(1); STRUCT (P, last, id) with the cached
+// p_struct.  Blocks at or below their segment's carried threshold are candidates; the
+// candidates are sorted by (tier, key), an exactness check proves no excluded block can
+// be a victim (else the segment is rescanned), thresholds are re-carried.
+// Output: the victims' slots in eviction order in cand[0..m).
+// ---------------------------------------------------------------------------
+__device__ void narrow(Ctx& c, uint32_t e, uint32_t mp);
 
-// ---------------------------------------------------------------------------
-// Fused score + select (a4 + a5) for one chunk of m victims (no learner firing
-// inside).  Exact: key = (tier, primary, last, id) per SURVEY c.2 O11.  Per
-// resident, unpinned block one pass computes its segment (EF / 8 multi-turn
-// classes (queue, tau) / STRUCT) and key: EF (ntok, id); multi-turn class
-// (last, id) (P strictly decreasing in dt within a class, §8(a) a4); STRUCT
-// (P, last, id) with the cached p_struct.  Candidates are sorted; EF victims come
-// first (Stage 1); the class heads get their exact Eq.(3) P and the
-// scored union is merged by (P, last, id) (Stage 2).
-// Output: victims' slots in eviction order in cand[0..m).
-// ---------------------------------------------------------------------------
 __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp) {
   const Dev& d = *c.d;
   Smem& s = *c.s;
   RState& st = s.st;
+  GroupCtl* g = c.ctl;
   const double now = st.now;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const bool gm = !d.cand_smem;
   uint32_t e = 0, mp = 0, c0 = 0;
   for (int attempt = 0; attempt < 3; ++attempt) {
-    if (tid < 16) { s.cnt[tid] = 0; s.segtot[tid] = 0; s.used[tid] = 0; }
-    if (tid == 0) { s.ncand = 0; s.fail = 0; }
-    __syncthreads();
-    // ---- one pass over the SoA: segment + key of every resident, unpinned block.
-    //      Blocks at or below their segment's carried threshold become candidates;
-    //      multi-turn candidates get their exact Eq.(1)/(3) score here.
-    for (uint32_t sl = tid; sl < d.C; sl += NT) {
-      const uint64_t gi = c.base + sl;
-      const uint32_t meta = d.bmeta[gi];
-      if (!(meta & M_LIVE) || d.bpin[gi] == stamp) continue;
-      const uint32_t q = meta_q(meta), tau = meta_tau(meta);
-      Cand x;
-      uint32_t seg, tier;
-      bool take;
-      if (q == Q_EF) {                      // Stage 1 key (num_tokens, id)
-        seg = 0;
-        tier = 0;
-        x.k0 = ((uint64_t)meta_ntok(meta) << 32) | d.bid[gi];
-        x.k1 = 0;
-        x.k2 = 0;
-        take = x.k0 <= st.thr[0];
-      } else if (q == Q_STRUCT) {           // Eq.(2)+(3) with the cached p_struct
-        seg = 9;
-        tier = 1;
-        const double last = d.blast[gi];
-        double dt = __dsub_rn(now, last);
-        if (dt < d.dt_eps) dt = d.dt_eps;
-        const double P = __ddiv_rn(__dmul_rn(s.cw[2][tau], d.bps[gi]), dt);
-        x.k0 = obits(P);
-        x.k1 = obits(last);
-        x.k2 = d.bid[gi];
-        take = x.k0 <= st.thr[9];
-      } else {                              // multi-turn class (queue, tau): Eq.(1)+(3)
-        seg = 1 + (q - 1) * 4 + (tau & 3);
-        tier = 1;
-        const double last = d.blast[gi];
-        x.k1 = obits(last);
-        x.k2 = d.bid[gi];
-        take = x.k1 <= st.thr[seg];
-        if (take) {
-          double dt = __dsub_rn(now, last);
-          if (dt < d.dt_eps) dt = d.dt_eps;
-          const double p = survival(dt, st.par.mu[q - 1], st.par.sigma[q - 1], d.z_cut);
-          x.k0 = obits(__ddiv_rn(__dmul_rn(s.cw[q - 1][tau], p), dt));
-        }
-      }
-      atomicAdd(&s.segtot[seg], 1u);
-      if (take) {
-        x.ss = sl | (tier << 28);
-        x.seg = seg;
-        const uint32_t pos = atomicAdd(&s.ncand, 1u);
-        c.cand[pos] = x;
-        atomicAdd(&s.cnt[seg], 1u);
+    if (tid < 16) { s.used[tid] = 0; }
+    if (tid == 0) {
+      s.fail = 0;
+      g->stamp = stamp;
+      if (gm) {
+        g->ncand = 0;
+        g->now = now;
+        for (int i = 0; i < 16; ++i) { g->segtot[i] = 0; g->cnt[i] = 0; g->thr[i] = st.thr[i]; }
+        for (int q = 0; q < 3; ++q) for (int t = 0; t < 5; ++t) g->cw[q][t] = s.cw[q][t];
+        for (int i = 0; i < 2; ++i) { g->mu[i] = st.par.mu[i]; g->sigma[i] = st.par.sigma[i]; }
       }
     }
     __syncthreads();
+    issue(c, CMD_SCAN);
+    if (gm) {            // gather the group's counts; bring the candidates into smem
+      if (tid < 16) { s.segtot[tid] = __ldcg(&g->segtot[tid]); s.cnt[tid] = __ldcg(&g->cnt[tid]); }
+      if (tid == 0) s.ncand = __ldcg(&g->ncand);
+      __syncthreads();
+      const uint32_t e0 = min(m, s.segtot[0]);
+      const bool narrowed = s.ncand > (uint32_t)CAND_MAX;
+      if (narrowed) narrow(c, e0, m - e0);
+      const Cand* src = narrowed ? d.gsel + (uint64_t)c.r * CAND_MAX : d.gcand + c.base;
+      for (uint32_t i = tid; i < s.ncand; i += NT) {
+        Cand x;
+        x.k0 = __ldcg(&src[i].k0); x.k1 = __ldcg(&src[i].k1); x.k2 = __ldcg(&src[i].k2);
+        x.ss = __ldcg(&src[i].ss); x.seg = __ldcg(&src[i].seg);
+        c.cand[i] = x;
+      }
+      __syncthreads();
+    }
     const uint32_t nc = s.ncand;
     int N = 32;
     while ((uint32_t)N < nc) N <<= 1;
@@ -773,12 +1051,12 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp) {
       st.select_passes++;
       st.select_cands += nc;
       if (nc > (uint32_t)NT) st.select_big++;
-    }
-    if (tid == 0 && attempt == 0) {
-      uint32_t tot = 0;
-      for (int g = 0; g < 10; ++g) tot += s.segtot[g];
-      st.blocks_scored += tot;
-      st.blocks_scored_struct += s.segtot[9];
+      if (attempt == 0) {
+        uint32_t tot = 0;
+        for (int k = 0; k < NSEG; ++k) tot += s.segtot[k];
+        st.blocks_scored += tot;
+        for (int k = 9; k < NSEG; ++k) st.blocks_scored_struct += s.segtot[k];
+      }
     }
     __syncthreads();
     sort_cands(c.cand, N);          // (tier, P | (ntok,id), last, id)
@@ -788,30 +1066,30 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp) {
     // ---- exactness check: every block a threshold left out must lose to the mp-th
     //      scored candidate.  EF: enough heads.  Class c: a non-candidate has last > T_c,
     //      so dt < now - T_c and, P being strictly decreasing in dt within a class,
-    //      P > P_c(now - T_c).  STRUCT: a non-candidate has P > T_S.
+    //      P > P_c(now - T_c).  STRUCT class: a non-candidate has P > T_S.
     if (tid == 0 && c0 < e) atomicOr(&s.fail, 1u);
-    if (mp > 0 && tid >= 1 && tid <= 9 && s.segtot[tid] > s.cnt[tid]) {
-      const uint32_t g = tid;
+    if (mp > 0 && tid >= 1 && tid < NSEG && s.segtot[tid] > s.cnt[tid]) {
+      const uint32_t gsg = tid;
       const uint32_t S = nc - c0;
       const double Pth = S >= mp ? from_obits(c.cand[c0 + mp - 1].k0)
                                  : __longlong_as_double(0x7ff0000000000000ll);
       bool ok;
-      if (g == 9) {
-        ok = Pth <= from_obits(st.thr[9]);
+      if (gsg >= 9) {
+        ok = Pth <= from_obits(st.thr[gsg]);
       } else {
-        const uint32_t q = 1 + (g - 1) / 4, tau = (g - 1) & 3;
-        double dt = __dsub_rn(now, from_obits(st.thr[g]));
+        const uint32_t q = 1 + (gsg - 1) / 4, tau = (gsg - 1) & 3;
+        double dt = __dsub_rn(now, from_obits(st.thr[gsg]));
         if (dt < d.dt_eps) dt = d.dt_eps;
         const double p = survival(dt, st.par.mu[q - 1], st.par.sigma[q - 1], d.z_cut);
         ok = Pth < __ddiv_rn(__dmul_rn(s.cw[q - 1][tau], p), dt);
       }
-      if (!ok) atomicOr(&s.fail, 1u << g);
+      if (!ok) atomicOr(&s.fail, 1u << gsg);
     }
     __syncthreads();
     const uint32_t fail = s.fail;
     if (fail == 0) break;
     if (tid < 10 && ((fail >> tid) & 1u)) st.select_fail_seg[tid]++;
-    if (tid < 10 && (((fail >> tid) & 1u) || attempt >= 1)) st.thr[tid] = ~0ull;
+    if (tid < NSEG && (((fail >> tid) & 1u) || attempt >= 1)) st.thr[tid] = ~0ull;
     __syncthreads();
   }
   // ---- carry thresholds: keep about 3*used + SLACK candidates per segment.
@@ -826,24 +1104,24 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp) {
   __syncthreads();
   for (uint32_t i0 = c0; i0 < nc; i0 += NT) {
     const uint32_t i = i0 + tid;
-    const uint32_t g = i < nc ? c.cand[i].seg : 15;
+    const uint32_t gsg = i < nc ? c.cand[i].seg : 15;
     uint32_t myrank = 0;
-    for (uint32_t h = 1; h <= 9; ++h) {
-      const uint32_t bal = __ballot_sync(~0u, g == h);
-      if (g == h) myrank = __popc(bal & ((1u << lane) - 1u));
-      if (lane == 0) s.wsum[wid * 10 + (h - 1) % 10] = __popc(bal);
+    for (uint32_t h = 1; h < (uint32_t)NSEG; ++h) {
+      const uint32_t bal = __ballot_sync(~0u, gsg == h);
+      if (gsg == h) myrank = __popc(bal & ((1u << lane) - 1u));
+      if (lane == 0) s.wsum[wid * 16 + h] = __popc(bal);
     }
     __syncthreads();
-    if (g >= 1 && g <= 9) {
-      uint32_t off = s.start[g];
-      for (int w = 0; w < wid; ++w) off += s.wsum[w * 10 + (g - 1)];
-      const uint32_t r = off + myrank, want = 3 * s.used[g] + SLACK;
-      if (r == want - 1 && s.cnt[g] > want) st.thr[g] = g == 9 ? c.cand[i].k0 : c.cand[i].k1;
+    if (gsg >= 1 && gsg < (uint32_t)NSEG) {
+      uint32_t off = s.start[gsg];
+      for (int w = 0; w < wid; ++w) off += s.wsum[w * 16 + gsg];
+      const uint32_t r = off + myrank, want = 3 * s.used[gsg] + SLACK;
+      if (r == want - 1 && s.cnt[gsg] > want) st.thr[gsg] = gsg >= 9 ? c.cand[i].k0 : c.cand[i].k1;
     }
     __syncthreads();
-    if (tid >= 1 && tid <= 9) {
+    if (tid >= 1 && tid < NSEG) {
       uint32_t t = 0;
-      for (int w = 0; w < NW; ++w) t += s.wsum[w * 10 + (tid - 1)];
+      for (int w = 0; w < NW; ++w) t += s.wsum[w * 16 + tid];
       s.start[tid] += t;
     }
     __syncthreads();
@@ -859,6 +1137,82 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp) {
       __syncthreads();
     }
   }
+}
+
+// Too many candidates for the leader's smem: choose, per over-full segment, the exact key
+// of rank target_s by a group-parallel MSB radix select over the candidate buffer, then
+// compact the candidates at or below the new thresholds.  The new thresholds are exact
+// bounds (every dropped candidate has a larger key), so the exactness check still holds.
+__device__ void narrow(Ctx& c, uint32_t e, uint32_t mp) {
+  Smem& s = *c.s;
+  RState& st = s.st;
+  GroupCtl* g = c.ctl;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid < NSEG) {
+    const uint32_t need = tid == 0 ? e : mp;
+    s.target[tid] = need + 2 * SLACK;
+    s.pfx[tid] = 0;
+    s.pmask[tid] = 0;
+    s.below[tid] = 0;
+  }
+  __syncthreads();
+  uint32_t active = 0;
+  for (int k = 0; k < NSEG; ++k) if (s.cnt[k] > s.target[k]) active |= 1u << k;
+  for (int shift = 56; shift >= 0 && active; shift -= 8) {
+    if (tid == 0) {
+      g->shift = (unsigned)shift;
+      g->active = active;
+      for (int k = 0; k < NSEG; ++k) { g->pfx[k] = s.pfx[k]; g->pmask[k] = s.pmask[k]; }
+    }
+    for (int i = tid; i < NSEG * 256; i += NT) g->hist[i] = 0;
+    __syncthreads();
+    issue(c, CMD_HIST);
+    // one warp per active segment: find the digit holding rank target
+    if (wid < NSEG && ((active >> wid) & 1u)) {
+      const int k = wid;
+      uint32_t v[8], loc = 0;
+      for (int j = 0; j < 8; ++j) { v[j] = __ldcg(&g->hist[k * 256 + lane * 8 + j]); loc += v[j]; }
+      uint32_t inc = loc;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(~0u, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const uint32_t need = s.target[k] - s.below[k];     // >= 1
+      const uint32_t excl = inc - loc;
+      const bool mine = excl < need && inc >= need;
+      const uint32_t bal = __ballot_sync(~0u, mine);
+      const int src = __ffs(bal) - 1;
+      if (lane == src) {
+        uint32_t run = excl;
+        int b = 0;
+        for (int j = 0; j < 8; ++j) {
+          if (run + v[j] >= need) { b = lane * 8 + j; break; }
+          run += v[j];
+        }
+        s.below[k] += run;
+        s.pfx[k] |= (uint64_t)b << shift;
+        s.pmask[k] |= 0xFFull << shift;
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    for (int k = 0; k < NSEG; ++k) if ((active >> k) & 1u) st.thr[k] = s.pfx[k];
+    for (int k = 0; k < 16; ++k) { g->thr[k] = st.thr[k]; g->selcnt[k] = 0; }
+    g->nsel = 0;
+  }
+  __syncthreads();
+  issue(c, CMD_COMPACT);
+  if (tid < 16) s.cnt[tid] = __ldcg(&g->selcnt[tid]);
+  if (tid == 0) {
+    s.ncand = __ldcg(&g->nsel);
+    if (s.ncand > (uint32_t)CAND_MAX) {     // pathological key ties: cannot hold them all
+      st.err = (uint32_t)(-SAE_E_OVERFLOW);
+      raise_err(*c.d, SAE_E_OVERFLOW);
+      s.ncand = CAND_MAX;
+    }
+  }
+  __syncthreads();
 }
 
 // Apply a chunk of m victims (cand[0..m) in eviction order): SURVEY c.2 O11 steps 1-4.
@@ -919,14 +1273,15 @@ __device__ void apply_chunk(Ctx& c, uint32_t m, uint32_t* vids_out) {
   }
 }
 
-// Evict k victims with pin stamp (k <= unpinned residents), chunked at K crossings (A14).
+// Evict k victims with pin stamp (k <= unpinned residents), chunked at K crossings (A14)
+// and in passes of at most MSUB victims (keys are frozen between firings).
 __device__ void evict_k(Ctx& c, uint64_t k, uint32_t stamp, uint32_t* vids_out) {
   const Dev& d = *c.d;
   Smem& s = *c.s;
   uint64_t done = 0;
   while (done < k) {
     const uint64_t to_cross = d.K - (s.st.E % d.K);
-    const uint32_t m = (uint32_t)min(k - done, to_cross);
+    const uint32_t m = (uint32_t)min(min(k - done, to_cross), (uint64_t)MSUB);
     select_chunk(c, m, stamp);
     apply_chunk(c, m, vids_out ? vids_out + done : nullptr);
     done += m;
@@ -939,7 +1294,7 @@ __device__ void load_state(Ctx& c) {
   const Dev& d = *c.d;
   const uint32_t* src = reinterpret_cast<const uint32_t*>(d.st + c.r);
   uint32_t* dst = reinterpret_cast<uint32_t*>(&c.s->st);
-  for (int i = threadIdx.x; i < (int)(sizeof(RState) / 4); i += NT) dst[i] = src[i];
+  for (int i = threadIdx.x; i < (int)(sizeof(RState) / 4); i += NT) dst[i] = __ldcg(src + i);
   __syncthreads();
   recompute_cw(*c.s);
   __syncthreads();
@@ -1136,36 +1491,51 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
 
 extern __shared__ __align__(16) unsigned char g_smem[];
 
-__device__ Ctx make_ctx(const Dev& d, uint32_t r) {
+__device__ Ctx make_ctx(const Dev& d, uint32_t r, uint32_t rank) {
   Ctx c;
   c.d = &d;
   c.s = reinterpret_cast<Smem*>(g_smem);
   c.cand = reinterpret_cast<Cand*>(g_smem + ((sizeof(Smem) + 15) / 16) * 16);
+  c.ctl = d.ctl + r;
   c.r = r;
+  c.rank = rank;
+  c.GP = d.GP;
   c.base = (uint64_t)r * d.C;
   return c;
 }
 
-// Persistent replay: CTA r owns replica r and replays its run of the batch.
+// Persistent replay: the group of GP CTAs (blockIdx / GP) owns replica r; its leader
+// (rank 0) replays the replica's run of the batch in order, the others execute the
+// leader's group commands (scan / histogram / compact / refresh / rebuild).
 __global__ void __launch_bounds__(NT, 1) k_replay(Dev d, BatchDev b) {
-  const uint32_t r = blockIdx.x;
+  const uint32_t r = blockIdx.x / d.GP, rank = blockIdx.x % d.GP;
   if (r >= d.R) return;
-  Ctx c = make_ctx(d, r);
-  const uint32_t lo = b.run_start[r];
-  if (lo == 0xFFFFFFFFu) return;
-  const uint32_t hi = b.run_end[r];
-  load_state(c);
-  if (c.s->st.err == 0) {
-    for (uint32_t i = lo; i < hi; ++i)
-      if (!admit_one(c, b, i)) break;
+  Ctx c = make_ctx(d, r, rank);
+  if (rank != 0) {
+    worker_loop(c);
+    return;
   }
-  store_state(c);
+  const uint32_t lo = b.run_start[r];
+  if (lo != 0xFFFFFFFFu) {
+    const uint32_t hi = b.run_end[r];
+    load_state(c);
+    if (c.s->st.err == 0) {
+      for (uint32_t i = lo; i < hi; ++i)
+        if (!admit_one(c, b, i)) break;
+    }
+    store_state(c);
+  }
+  if (c.GP > 1) issue(c, CMD_EXIT);
 }
 
 // sae_evict: Alg.1 Evict x k with an empty pin set.
 __global__ void __launch_bounds__(NT, 1) k_evict(Dev d, uint32_t r, uint32_t k, double now,
                                                  uint32_t* vids, uint32_t* n_out) {
-  Ctx c = make_ctx(d, r);
+  Ctx c = make_ctx(d, r, blockIdx.x);
+  if (blockIdx.x != 0) {
+    worker_loop(c);
+    return;
+  }
   load_state(c);
   RState& st = c.s->st;
   if (st.err == 0) {
@@ -1187,15 +1557,21 @@ __global__ void __launch_bounds__(NT, 1) k_evict(Dev d, uint32_t r, uint32_t k, 
     }
   }
   store_state(c);
+  if (c.GP > 1) issue(c, CMD_EXIT);
 }
 
 __global__ void __launch_bounds__(NT, 1) k_update(Dev d, uint32_t r0, uint32_t r1) {
-  const uint32_t r = r0 + blockIdx.x;
+  const uint32_t r = r0 + blockIdx.x / d.GP, rank = blockIdx.x % d.GP;
   if (r >= r1) return;
-  Ctx c = make_ctx(d, r);
+  Ctx c = make_ctx(d, r, rank);
+  if (rank != 0) {
+    worker_loop(c);
+    return;
+  }
   load_state(c);
   learn(c);
   store_state(c);
+  if (c.GP > 1) issue(c, CMD_EXIT);
 }
 
 // read-only probe, one warp per request
@@ -1309,6 +1685,7 @@ struct sae_ctx {
   size_t ws_cap = 0;
   std::vector<void*> allocs;
   // optional profiling: CUDA events around every k_replay launch (bench roofline)
+  uint64_t coresident = 0;
   bool prof = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev;
 };
@@ -1339,6 +1716,13 @@ static size_t smem_bytes() {
   return ((sizeof(Smem) + 15) / 16) * 16 + sizeof(Cand) * CAND_MAX;
 }
 
+static cudaError_t launch_group(const void* fn, uint32_t grid, bool coop, cudaStream_t s, Dev& d,
+                                BatchDev* x) {
+  void* args[] = {(void*)&d, (void*)x};
+  if (coop) return cudaLaunchCooperativeKernel(fn, grid, NT, args, smem_bytes(), s);
+  return cudaLaunchKernel(fn, grid, NT, args, smem_bytes(), s);
+}
+
 extern "C" {
 
 sae_status sae_create(const sae_config* cfg, sae_ctx** out) {
@@ -1352,7 +1736,6 @@ sae_status sae_create(const sae_config* cfg, sae_ctx** out) {
     return SAE_E_INVAL;
   for (int q = 0; q < 2; ++q)
     if (!(cfg->init.sigma[q] > 0.0)) return SAE_E_INVAL;
-  if (cfg->capacity_blocks > (uint32_t)CAND_MAX) return SAE_E_INVAL;  // v1: pool fits one CTA
   ctx = new sae_ctx();
   ctx->cfg = *cfg;
   ctx->device = cfg->device;
@@ -1398,13 +1781,38 @@ sae_status sae_create(const sae_config* cfg, sae_ctx** out) {
   CK(dalloc(ctx, &d.iv, R * 2 * RMAX));
   CK(dalloc(ctx, &d.traj, R * (uint64_t)(d.traj_cap ? d.traj_cap : 1)));
   CK(dalloc(ctx, &d.err, 1));
+  // group size: one CTA per replica while the pool fits the leader's candidate buffer;
+  // otherwise a co-resident group (cooperative launch) that splits every scan pass
+  int nsm = 0, occ = 0;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg->device));
+  CK(cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes()));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_replay, NT, smem_bytes()));
+  const uint64_t coresident = (uint64_t)nsm * (uint64_t)(occ > 0 ? occ : 1);
+  uint64_t gp = cfg->ctas_per_replica;
+  if (gp == 0) {
+    if (d.C <= (uint32_t)CAND_MAX) gp = 1;
+    else gp = std::min<uint64_t>(std::max<uint64_t>(1, d.C / 8192), coresident / R);
+  }
+  if (gp == 0 || (gp > 1 && gp * R > coresident)) {
+    ctx->last_error = "ctas_per_replica x n_replicas exceeds the co-resident CTA capacity";
+    return SAE_E_INVAL;
+  }
+  d.GP = (uint32_t)gp;
+  d.cand_smem = (d.C <= (uint32_t)CAND_MAX && d.GP == 1) ? 1u : 0u;
+  ctx->coresident = coresident;
+  CK(dalloc(ctx, &d.ctl, R));
+  CK(cudaMemset(d.ctl, 0, R * sizeof(GroupCtl)));
+  if (!d.cand_smem) {
+    CK(dalloc(ctx, &d.gcand, RC));
+    CK(dalloc(ctx, &d.gsel, R * (uint64_t)CAND_MAX));
+  }
   // initial scalar state
   std::vector<RState> st(R);
   for (uint64_t r = 0; r < R; ++r) {
     RState s;
     std::memset(&s, 0, sizeof s);
     s.free_top = d.C;
-    for (int g = 0; g < 10; ++g) s.thr[g] = ~0ull;
+    for (int g = 0; g < 16; ++g) s.thr[g] = ~0ull;
     s.par = cfg->init;
     st[r] = s;
   }
@@ -1572,7 +1980,7 @@ sae_status sae_admit_batch(sae_ctx* ctx, const sae_batch* b, sae_admit_out* o, s
     CK(cudaEventCreate(&e1));
     CK(cudaEventRecord(e0, s));
   }
-  k_replay<<<ctx->d.R, NT, smem_bytes(), s>>>(ctx->d, x);
+  CK(launch_group((const void*)k_replay, ctx->d.R * ctx->d.GP, ctx->d.GP > 1, s, ctx->d, &x));
   ctx->launches++;
   if (ctx->prof) {
     CK(cudaEventRecord(e1, s));
@@ -1600,7 +2008,11 @@ sae_status sae_lookup(sae_ctx* ctx, const sae_batch* b, uint32_t* hit, sae_strea
 sae_status sae_evict(sae_ctx* ctx, uint32_t replica, uint32_t k, double now, uint32_t* vids,
                      uint32_t* n_out, sae_stream st) {
   if (!ctx || replica >= ctx->d.R || (k > 0 && !vids)) return SAE_E_INVAL;
-  k_evict<<<1, NT, smem_bytes(), (cudaStream_t)st>>>(ctx->d, replica, k, now, vids, n_out);
+  void* args[] = {(void*)&ctx->d, (void*)&replica, (void*)&k, (void*)&now, (void*)&vids, (void*)&n_out};
+  if (ctx->d.GP > 1)
+    CK(cudaLaunchCooperativeKernel((const void*)k_evict, ctx->d.GP, NT, args, smem_bytes(), (cudaStream_t)st));
+  else
+    CK(cudaLaunchKernel((const void*)k_evict, 1, NT, args, smem_bytes(), (cudaStream_t)st));
   ctx->launches++;
   CK(cudaGetLastError());
   return SAE_OK;
@@ -1611,8 +2023,17 @@ sae_status sae_update(sae_ctx* ctx, uint32_t replica, sae_stream st) {
   uint32_t r0 = replica, r1 = replica + 1;
   if (replica == 0xFFFFFFFFu) { r0 = 0; r1 = ctx->d.R; }
   else if (replica >= ctx->d.R) return SAE_E_INVAL;
-  k_update<<<r1 - r0, NT, smem_bytes(), (cudaStream_t)st>>>(ctx->d, r0, r1);
-  ctx->launches++;
+  // groups must be co-resident: update at most coresident/GP replicas per launch
+  const uint32_t per = ctx->d.GP > 1 ? (uint32_t)std::max<uint64_t>(1, ctx->coresident / ctx->d.GP) : (r1 - r0);
+  for (uint32_t a = r0; a < r1; a += per) {
+    uint32_t b = std::min(r1, a + per);
+    void* args[] = {(void*)&ctx->d, (void*)&a, (void*)&b};
+    if (ctx->d.GP > 1)
+      CK(cudaLaunchCooperativeKernel((const void*)k_update, (b - a) * ctx->d.GP, NT, args, smem_bytes(), (cudaStream_t)st));
+    else
+      CK(cudaLaunchKernel((const void*)k_update, b - a, NT, args, smem_bytes(), (cudaStream_t)st));
+    ctx->launches++;
+  }
   CK(cudaGetLastError());
   return SAE_OK;
 }

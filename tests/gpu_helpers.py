@@ -15,7 +15,7 @@ def u32(t):
     return t.cpu().numpy().view(np.uint32)
 
 
-def gpu_replay(tr, pol, n_replicas=1, traj=1 << 16, lo=0, hi=None, cache=None):
+def gpu_replay(tr, pol, n_replicas=1, traj=1 << 16, lo=0, hi=None, cache=None, ctas=0):
     """Replay requests [lo, hi) of a single-replica trace on the GPU (replica 0)."""
     hi = tr["n"] if hi is None else hi
     sub = {k: tr[k][lo:hi] for k in ("arrival", "prompt_off", "prompt_len", "decode_off",
@@ -23,7 +23,7 @@ def gpu_replay(tr, pol, n_replicas=1, traj=1 << 16, lo=0, hi=None, cache=None):
     sub["tokens"], sub["types"], sub["n"] = tr["tokens"], tr["types"], hi - lo
     sub["replica"] = np.zeros(hi - lo, np.uint32)
     cache = cache or S.SaeCache(pol["capacity"], n_replicas=n_replicas, policy=pol,
-                                traj_capacity=traj)
+                                traj_capacity=traj, ctas_per_replica=ctas)
     b = S.batch_to_torch(sub)
     out = cache.admit_batch(b, want_hashes=True)
     torch.cuda.synchronize()
@@ -66,8 +66,8 @@ def assert_stats_equal(g, o):
                                                             list(getattr(o, k)))
 
 
-def compare_replay(tr, pol, lo=0, hi=None, check_hashes=True):
-    cache, b, out = gpu_replay(tr, pol, lo=lo, hi=hi)
+def compare_replay(tr, pol, lo=0, hi=None, check_hashes=True, ctas=0):
+    cache, b, out = gpu_replay(tr, pol, lo=lo, hi=hi, ctas=ctas)
     R = oracle.Replica(pol)
     ref = R.replay(tr, lo, hi)
     n = (tr["n"] if hi is None else hi) - lo
