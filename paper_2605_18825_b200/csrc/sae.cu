@@ -40,13 +40,14 @@ constexpr int NW = NT / 32;
 constexpr int CAND_MAX = 4096;     // candidate buffer (smem) per CTA
 constexpr uint32_t SLACK = 32;     // extra candidates kept per segment across chunks (min)
 constexpr int NSEG = 13;           // EF, 8 multi-turn classes (queue, tau), 4 STRUCT classes (tau)
-constexpr uint32_t MSUB = 192;     // victims selected per scan pass (keys are frozen within a chunk)
+constexpr uint32_t MSUB = 96;      // victims selected per scan pass (keys are frozen within a chunk)
+constexpr uint32_t VCAP = 256;      // victim staging buffer (m smallest + key ties); power of two >= 2*MSUB
 constexpr int RMAX = 4096;         // max interval ring
 constexpr uint32_t SLOT_MASK = 0x0FFFFFFFu;
 constexpr double INV_SQRT2 = 0.70710678118654757;  // 0x3FE6A09E667F3BCD
 
 enum { Q_EF = 0, Q_CHAT = 1, Q_AGENT = 2, Q_STRUCT = 3 };
-enum { M_LIVE = 1u << 10 };
+enum { M_LIVE = 1u << 10, M_PIN = 1u << 11 };
 
 __host__ __device__ inline uint32_t meta_pack(uint32_t q, uint32_t tau, uint32_t ntok) {
   return q | (tau << 2) | (ntok << 5) | M_LIVE;
@@ -72,6 +73,7 @@ struct RState {
   uint64_t evict_by_queue[4], evict_by_type[6], mae_by_type[6];
   uint64_t learner_firings, eviction_rounds, blocks_scored, blocks_scored_struct;
   uint64_t select_passes, select_cands, select_big, select_fail_seg[10];
+  uint64_t tph[8];          // leader phase timers (ns): probe, scan, narrow, select, apply, learn, insert, rebuild
   uint64_t thr[16];        // per-segment candidate thresholds on k0 (heuristic; exactness never depends on them)
   sae_params par;
 };
@@ -161,6 +163,12 @@ struct BatchDev {
   uint32_t* o_vids;
   uint64_t vcap;
 };
+
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ inline void raise_err(const Dev& d, int status) {
   atomicCAS(d.err, 0u, (uint32_t)(-status));
@@ -484,12 +492,15 @@ struct Smem {
   uint64_t k, admit;
   uint64_t pfx[16], pmask[16];
   uint32_t below[16], target[16];
+  uint32_t nv;
+  uint32_t rhist[NSEG * 256];   // radix-select histograms (one 256-bin digit per segment)
 };
 
 struct Ctx {               // per-CTA view of one replica (group)
   const Dev* d;
   Smem* s;
   Cand* cand;
+  Cand* vbuf;              // [VCAP] victims staging
   GroupCtl* ctl;
   uint32_t r, rank, GP;
   uint64_t base;           // r * C
@@ -549,67 +560,135 @@ struct ScanP {
 
 // One pass over slots [lo, hi) of the replica's SoA: segment + key of every resident,
 // unpinned block (a4); those at or below the segment's threshold become candidates.
-// Counts go to smem (segtot, cnt); candidates to smem (cand_smem) or the global buffer.
+// Each thread handles 4 consecutive slots per step with 128-bit cache-global loads
+// (meta, id, last; p_struct only for STRUCT blocks); per-segment counts accumulate in
+// registers (16-bit fields) and are reduced once per pass.  Counts go to smem
+// (segtot, cnt); candidates to smem (cand_smem) or the group's global buffer.
+__device__ __forceinline__ void pk_add(uint64_t (&pk)[4], uint32_t seg) {
+  const uint64_t inc = 1ull << ((seg & 3u) * 16u);
+  switch (seg >> 2) {
+    case 0: pk[0] += inc; break;
+    case 1: pk[1] += inc; break;
+    case 2: pk[2] += inc; break;
+    default: pk[3] += inc; break;
+  }
+}
+
+__device__ __forceinline__ bool score_one(const Dev& d, const ScanP& P, uint32_t meta, uint32_t id,
+                                          double last, uint64_t gi, uint32_t sl, Cand& x,
+                                          uint32_t& seg) {
+  const uint32_t q = meta_q(meta), tau = meta_tau(meta);
+  seg = seg_of(q, tau);
+  bool take;
+  if (q == Q_EF) {                      // Stage 1 key (num_tokens, id)
+    x.k0 = ((uint64_t)meta_ntok(meta) << 32) | id;
+    x.k1 = 0;
+    x.k2 = 0;
+    take = x.k0 <= P.thr[seg];
+  } else if (q == Q_STRUCT) {           // Eq.(2)+(3) with the cached p_struct
+    double dt = __dsub_rn(P.now, last);
+    if (dt < P.dt_eps) dt = P.dt_eps;
+    const double Pv = __ddiv_rn(__dmul_rn(P.cw[10 + tau], __ldcg(d.bps + gi)), dt);
+    x.k0 = obits(Pv);
+    x.k1 = obits(last);
+    x.k2 = id;
+    take = x.k0 <= P.thr[seg];
+  } else {                              // multi-turn class (queue, tau): Eq.(1)+(3) for heads
+    x.k1 = obits(last);
+    x.k2 = id;
+    take = x.k1 <= P.thr[seg];
+    if (take) {
+      double dt = __dsub_rn(P.now, last);
+      if (dt < P.dt_eps) dt = P.dt_eps;
+      const double p = survival(dt, P.mu[q - 1], P.sg[q - 1], P.z_cut);
+      x.k0 = obits(__ddiv_rn(__dmul_rn(P.cw[(q - 1) * 5 + tau], p), dt));
+    }
+  }
+  x.ss = sl | ((q == Q_EF ? 0u : 1u) << 28);
+  x.seg = seg;
+  return take;
+}
+
 __device__ void scan_range(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P) {
   const Dev& d = *c.d;
   Smem& s = *c.s;
   const int tid = threadIdx.x, lane = tid & 31;
   const bool gm = !d.cand_smem;
   Cand* gdst = gm ? d.gcand + c.base : nullptr;
-  for (uint64_t i0 = lo; i0 < hi; i0 += NT) {
-    const uint64_t sl = i0 + tid;
-    bool take = false;
-    Cand x;
-    if (sl < hi) {
-      const uint64_t gi = c.base + sl;
-      const uint32_t meta = __ldcg(d.bmeta + gi);
-      if ((meta & M_LIVE) && __ldcg(d.bpin + gi) != P.stamp) {
-        const uint32_t q = meta_q(meta), tau = meta_tau(meta);
-        const uint32_t seg = seg_of(q, tau);
-        const uint32_t id = __ldcg(d.bid + gi);
-        if (q == Q_EF) {                      // Stage 1 key (num_tokens, id)
-          x.k0 = ((uint64_t)meta_ntok(meta) << 32) | id;
-          x.k1 = 0;
-          x.k2 = 0;
-          take = x.k0 <= P.thr[seg];
-        } else if (q == Q_STRUCT) {           // Eq.(2)+(3) with the cached p_struct
-          const double last = __ldcg(d.blast + gi);
-          double dt = __dsub_rn(P.now, last);
-          if (dt < P.dt_eps) dt = P.dt_eps;
-          const double Pv = __ddiv_rn(__dmul_rn(P.cw[10 + tau], __ldcg(d.bps + gi)), dt);
-          x.k0 = obits(Pv);
-          x.k1 = obits(last);
-          x.k2 = id;
-          take = x.k0 <= P.thr[seg];
-        } else {                              // multi-turn class (queue, tau): Eq.(1)+(3)
-          const double last = __ldcg(d.blast + gi);
-          x.k1 = obits(last);
-          x.k2 = id;
-          take = x.k1 <= P.thr[seg];
-          if (take) {
-            double dt = __dsub_rn(P.now, last);
-            if (dt < P.dt_eps) dt = P.dt_eps;
-            const double p = survival(dt, P.mu[q - 1], P.sg[q - 1], P.z_cut);
-            x.k0 = obits(__ddiv_rn(__dmul_rn(P.cw[(q - 1) * 5 + tau], p), dt));
-          }
+  uint64_t tot[4] = {0, 0, 0, 0}, cnt[4] = {0, 0, 0, 0};
+  const bool vec = ((c.base + lo) & 3u) == 0;
+  // software pipeline: the next step's 4 slots are loaded before this step is scored
+  uint32_t mt[4], idv[4];
+  double lt[4];
+  auto load = [&](uint64_t s0, uint32_t (&m)[4], uint32_t (&iv)[4], double (&l)[4]) {
+    if (vec && s0 + 3 < hi) {
+      const uint4 m4 = __ldcg(reinterpret_cast<const uint4*>(d.bmeta + c.base + s0));
+      const uint4 i4 = __ldcg(reinterpret_cast<const uint4*>(d.bid + c.base + s0));
+      const double2 l0 = __ldcg(reinterpret_cast<const double2*>(d.blast + c.base + s0));
+      const double2 l1 = __ldcg(reinterpret_cast<const double2*>(d.blast + c.base + s0 + 2));
+      m[0] = m4.x; m[1] = m4.y; m[2] = m4.z; m[3] = m4.w;
+      iv[0] = i4.x; iv[1] = i4.y; iv[2] = i4.z; iv[3] = i4.w;
+      l[0] = l0.x; l[1] = l0.y; l[2] = l1.x; l[3] = l1.y;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const bool ok = s0 + u < hi;
+        m[u] = ok ? __ldcg(d.bmeta + c.base + s0 + u) : 0u;
+        iv[u] = ok ? __ldcg(d.bid + c.base + s0 + u) : 0u;
+        l[u] = ok ? __ldcg(d.blast + c.base + s0 + u) : 0.0;
+      }
+    }
+  };
+  uint64_t s0 = lo + 4ull * tid;
+  if (s0 < hi) load(s0, mt, idv, lt);
+  else { mt[0] = mt[1] = mt[2] = mt[3] = 0; }
+  for (uint64_t i0 = lo; i0 < hi; i0 += 4 * NT) {
+    const uint64_t sn = s0 + 4ull * NT;
+    uint32_t mn[4] = {0, 0, 0, 0}, in_[4] = {0, 0, 0, 0};
+    double ln_[4] = {0.0, 0.0, 0.0, 0.0};
+    if (sn < hi) load(sn, mn, in_, ln_);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      bool take = false;
+      Cand x;
+      const uint32_t meta = s0 < hi ? mt[u] : 0u;
+      if ((meta & (M_LIVE | M_PIN)) == M_LIVE) {
+        uint32_t seg;
+        take = score_one(d, P, meta, idv[u], lt[u], c.base + s0 + u, (uint32_t)(s0 + u), x, seg);
+        pk_add(tot, seg);
+        if (take) pk_add(cnt, seg);
+      }
+      if (gm) {
+        const uint32_t bal = __ballot_sync(~0u, take);
+        if (bal) {
+          uint32_t basep = 0;
+          if (lane == 0) basep = atomicAdd(&c.ctl->ncand, (unsigned)__popc(bal));
+          basep = __shfl_sync(~0u, basep, 0);
+          if (take) gdst[basep + __popc(bal & ((1u << lane) - 1u))] = x;
         }
-        x.ss = (uint32_t)sl | ((q == Q_EF ? 0u : 1u) << 28);
-        x.seg = seg;
-        atomicAdd(&s.segtot[seg], 1u);
-        if (take) atomicAdd(&s.cnt[seg], 1u);
+      } else if (take) {
+        c.cand[atomicAdd(&s.ncand, 1u)] = x;
       }
     }
-    if (gm) {
-      const uint32_t bal = __ballot_sync(~0u, take);
-      if (bal) {
-        uint32_t basep = 0;
-        if (lane == 0) basep = atomicAdd(&c.ctl->ncand, (unsigned)__popc(bal));
-        basep = __shfl_sync(~0u, basep, 0);
-        if (take) gdst[basep + __popc(bal & ((1u << lane) - 1u))] = x;
-      }
-    } else if (take) {
-      c.cand[atomicAdd(&s.ncand, 1u)] = x;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { mt[u] = mn[u]; idv[u] = in_[u]; lt[u] = ln_[u]; }
+    s0 = sn;
+  }
+  // reduce the packed per-thread counts: warp shuffles, then one smem atomic per warp
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    for (int o = 16; o > 0; o >>= 1) {
+      tot[w] += __shfl_xor_sync(~0u, tot[w], o);
+      cnt[w] += __shfl_xor_sync(~0u, cnt[w], o);
     }
+  }
+  if (lane < NSEG) {
+    const int w = lane >> 2, f = (lane & 3) * 16;
+    uint64_t tv = w == 0 ? tot[0] : w == 1 ? tot[1] : w == 2 ? tot[2] : tot[3];
+    uint64_t cv = w == 0 ? cnt[0] : w == 1 ? cnt[1] : w == 2 ? cnt[2] : cnt[3];
+    const uint32_t t16 = (uint32_t)((tv >> f) & 0xFFFFu), c16 = (uint32_t)((cv >> f) & 0xFFFFu);
+    if (t16) atomicAdd(&s.segtot[lane], t16);
+    if (c16) atomicAdd(&s.cnt[lane], c16);
   }
 }
 
@@ -1000,7 +1079,60 @@ __device__ void learn(Ctx& c) {
 // ---------------------------------------------------------------------------
 __device__ void narrow(Ctx& c, uint32_t e, uint32_t mp);
 
-__device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp) {
+// Block-wide MSB radix select over a[0..n): for every class g in `active` find the key of
+// rank s.target[g] (1-based) -> s.pfx[g], and the number of smaller keys -> s.below[g].
+// Global mode: one class (0), key k0.  Per-segment mode: class = segment, key = seg_key.
+__device__ void radix_select(const Cand* a, uint32_t n, bool per_seg, uint32_t active, Smem& s) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid < 16) { s.pfx[tid] = 0; s.pmask[tid] = 0; s.below[tid] = 0; }
+  __syncthreads();
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = tid; i < NSEG * 256; i += NT) s.rhist[i] = 0;
+    __syncthreads();
+    for (uint32_t i0 = 0; i0 < n; i0 += NT) {
+      const uint32_t i = i0 + tid;
+      uint32_t bin = 0xFFFFFFFFu;
+      if (i < n) {
+        const Cand& x = a[i];
+        const uint32_t g = per_seg ? x.seg : 0u;
+        if (g < 16 && ((active >> g) & 1u)) {
+          const uint64_t key = per_seg ? seg_key(x) : x.k0;
+          if ((key & s.pmask[g]) == s.pfx[g]) bin = g * 256u + (uint32_t)((key >> shift) & 255u);
+        }
+      }
+      const uint32_t peers = __match_any_sync(~0u, bin);
+      if (bin != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&s.rhist[bin], (uint32_t)__popc(peers));
+    }
+    __syncthreads();
+    if (wid < NSEG && ((active >> wid) & 1u)) {
+      const int g = wid;
+      uint32_t v[8], loc = 0;
+      for (int j = 0; j < 8; ++j) { v[j] = s.rhist[g * 256 + lane * 8 + j]; loc += v[j]; }
+      uint32_t inc = loc;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(~0u, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const uint32_t need = s.target[g] - s.below[g];
+      const uint32_t excl = inc - loc;
+      const uint32_t bal = __ballot_sync(~0u, excl < need && inc >= need);
+      if (lane == __ffs(bal) - 1) {
+        uint32_t run = excl;
+        int bsel = 0;
+        for (int j = 0; j < 8; ++j) {
+          if (run + v[j] >= need) { bsel = lane * 8 + j; break; }
+          run += v[j];
+        }
+        s.below[g] += run;
+        s.pfx[g] |= (uint64_t)bsel << shift;
+        s.pmask[g] |= 0xFFull << shift;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass) {
   const Dev& d = *c.d;
   Smem& s = *c.s;
   RState& st = s.st;
@@ -1023,7 +1155,9 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp) {
       }
     }
     __syncthreads();
+    uint64_t t0 = gtimer();
     issue(c, CMD_SCAN);
+    if (tid == 0) { const uint64_t t1 = gtimer(); st.tph[1] += t1 - t0; t0 = t1; }
     if (gm) {            // gather the group's counts; bring the candidates into smem
       if (tid < 16) { s.segtot[tid] = __ldcg(&g->segtot[tid]); s.cnt[tid] = __ldcg(&g->cnt[tid]); }
       if (tid == 0) s.ncand = __ldcg(&g->ncand);
@@ -1031,6 +1165,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp) {
       const uint32_t e0 = min(m, s.segtot[0]);
       const bool narrowed = s.ncand > (uint32_t)CAND_MAX;
       if (narrowed) narrow(c, e0, m - e0);
+      if (tid == 0 && narrowed) { const uint64_t t1 = gtimer(); st.tph[2] += t1 - t0; t0 = t1; }
       const Cand* src = narrowed ? d.gsel + (uint64_t)c.r * CAND_MAX : d.gcand + c.base;
       for (uint32_t i = tid; i < s.ncand; i += NT) {
         Cand x;
@@ -1041,17 +1176,11 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp) {
       __syncthreads();
     }
     const uint32_t nc = s.ncand;
-    int N = 32;
-    while ((uint32_t)N < nc) N <<= 1;
-    for (uint32_t i = nc + tid; i < (uint32_t)N; i += NT) {
-      c.cand[i].k0 = ~0ull; c.cand[i].k1 = ~0ull; c.cand[i].k2 = ~0u; c.cand[i].ss = 15u << 28;
-      c.cand[i].seg = 15;
-    }
     if (tid == 0) {
       st.select_passes++;
       st.select_cands += nc;
       if (nc > (uint32_t)NT) st.select_big++;
-      if (attempt == 0) {
+      if (attempt == 0 && count_pass) {   // one required pass per chunk (extra passes are overhead)
         uint32_t tot = 0;
         for (int k = 0; k < NSEG; ++k) tot += s.segtot[k];
         st.blocks_scored += tot;
@@ -1059,10 +1188,18 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp) {
       }
     }
     __syncthreads();
-    sort_cands(c.cand, N);          // (tier, P | (ntok,id), last, id)
+    // The victims are the m smallest candidates by (k0, k1, k2): EF keys (ntok, id) are
+    // < 2^63 <= obits(P), so Stage 1 precedes Stage 2 by construction.
     c0 = s.cnt[0];
     e = min(m, s.segtot[0]);
     mp = m - e;
+    uint64_t Kth = ~0ull;
+    if (nc >= m) {
+      if (tid == 0) s.target[0] = m;
+      __syncthreads();
+      radix_select(c.cand, nc, false, 1u, s);
+      Kth = s.pfx[0];
+    }
     // ---- exactness check: every block a threshold left out must lose to the mp-th
     //      scored candidate.  EF: enough heads.  Class c: a non-candidate has last > T_c,
     //      so dt < now - T_c and, P being strictly decreasing in dt within a class,
@@ -1070,9 +1207,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp) {
     if (tid == 0 && c0 < e) atomicOr(&s.fail, 1u);
     if (mp > 0 && tid >= 1 && tid < NSEG && s.segtot[tid] > s.cnt[tid]) {
       const uint32_t gsg = tid;
-      const uint32_t S = nc - c0;
-      const double Pth = S >= mp ? from_obits(c.cand[c0 + mp - 1].k0)
-                                 : __longlong_as_double(0x7ff0000000000000ll);
+      const double Pth = nc >= m ? from_obits(Kth) : __longlong_as_double(0x7ff0000000000000ll);
       bool ok;
       if (gsg >= 9) {
         ok = Pth <= from_obits(st.thr[gsg]);
@@ -1087,56 +1222,68 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp) {
     }
     __syncthreads();
     const uint32_t fail = s.fail;
+    if (tid == 0) st.tph[3] += gtimer() - t0;
     if (fail == 0) break;
     if (tid < 10 && ((fail >> tid) & 1u)) st.select_fail_seg[tid]++;
     if (tid < NSEG && (((fail >> tid) & 1u) || attempt >= 1)) st.thr[tid] = ~0ull;
     __syncthreads();
   }
-  // ---- carry thresholds: keep about 3*used + SLACK candidates per segment.
-  //      EF is sorted contiguously at the front; tier 1 is ranked per segment.
   const uint32_t nc = s.ncand;
-  if (tid == 0) {
-    const uint32_t want = 3 * e + SLACK;
-    if (c0 > want) st.thr[0] = c.cand[want - 1].k0;
-  }
-  for (uint32_t i = c0 + tid; i < c0 + mp; i += NT) atomicAdd(&s.used[c.cand[i].seg], 1u);
-  if (tid < 16) s.start[tid] = 0;   // running per-segment rank base
+  uint64_t Kth = nc >= m ? s.pfx[0] : ~0ull;
+  // ---- stage the victims: every candidate with k0 <= Kth (the m smallest plus key ties)
+  if (tid == 0) s.nv = 0;
   __syncthreads();
-  for (uint32_t i0 = c0; i0 < nc; i0 += NT) {
+  for (uint32_t i0 = 0; i0 < nc; i0 += NT) {
     const uint32_t i = i0 + tid;
-    const uint32_t gsg = i < nc ? c.cand[i].seg : 15;
-    uint32_t myrank = 0;
-    for (uint32_t h = 1; h < (uint32_t)NSEG; ++h) {
-      const uint32_t bal = __ballot_sync(~0u, gsg == h);
-      if (gsg == h) myrank = __popc(bal & ((1u << lane) - 1u));
-      if (lane == 0) s.wsum[wid * 16 + h] = __popc(bal);
+    const bool take = i < nc && c.cand[i].k0 <= Kth;
+    const uint32_t bal = __ballot_sync(~0u, take);
+    uint32_t basep = 0;
+    if (lane == 0 && bal) basep = atomicAdd(&s.nv, (uint32_t)__popc(bal));
+    basep = __shfl_sync(~0u, basep, 0);
+    const uint32_t pos = basep + __popc(bal & ((1u << lane) - 1u));
+    if (take && pos < VCAP) c.vbuf[pos] = c.cand[i];
+  }
+  __syncthreads();
+  uint32_t nv = s.nv;
+  if (nv > VCAP) {               // pathological key ties: fall back to a full sort
+    int N = 32;
+    while ((uint32_t)N < nc) N <<= 1;
+    for (uint32_t i = nc + tid; i < (uint32_t)N; i += NT) {
+      c.cand[i].k0 = ~0ull; c.cand[i].k1 = ~0ull; c.cand[i].k2 = ~0u; c.cand[i].ss = 15u << 28;
+      c.cand[i].seg = 15;
     }
     __syncthreads();
-    if (gsg >= 1 && gsg < (uint32_t)NSEG) {
-      uint32_t off = s.start[gsg];
-      for (int w = 0; w < wid; ++w) off += s.wsum[w * 16 + gsg];
-      const uint32_t r = off + myrank, want = 3 * s.used[gsg] + SLACK;
-      if (r == want - 1 && s.cnt[gsg] > want) st.thr[gsg] = gsg >= 9 ? c.cand[i].k0 : c.cand[i].k1;
+    sort_cands(c.cand, N);
+    for (uint32_t v = tid; v < m; v += NT) c.vbuf[v] = c.cand[v];
+    nv = m;
+    __syncthreads();
+  } else {
+    int N = 32;
+    while ((uint32_t)N < nv) N <<= 1;
+    for (uint32_t i = nv + tid; i < (uint32_t)N; i += NT) {
+      c.vbuf[i].k0 = ~0ull; c.vbuf[i].k1 = ~0ull; c.vbuf[i].k2 = ~0u; c.vbuf[i].ss = 15u << 28;
+      c.vbuf[i].seg = 15;
     }
     __syncthreads();
-    if (tid >= 1 && tid < NSEG) {
-      uint32_t t = 0;
-      for (int w = 0; w < NW; ++w) t += s.wsum[w * 16 + tid];
-      s.start[tid] += t;
-    }
+    sort_cands(c.vbuf, N);       // small: the m victims in (k0, last, id) order
+  }
+  // ---- carry thresholds: trim segments holding far more candidates than they use
+  for (uint32_t v = tid; v < m; v += NT) atomicAdd(&s.used[c.vbuf[v].seg], 1u);
+  __syncthreads();
+  uint32_t shrink = 0;
+  for (int g = 0; g < NSEG; ++g) {
+    const uint32_t want = 3 * s.used[g] + SLACK;
+    if (s.cnt[g] > 8 * want) shrink |= 1u << g;
+  }
+  if (shrink && nv <= VCAP) {
+    if (tid < NSEG) s.target[tid] = 4 * (3 * s.used[tid] + SLACK);
+    __syncthreads();
+    radix_select(c.cand, nc, true, shrink, s);
+    if (tid < NSEG && ((shrink >> tid) & 1u)) st.thr[tid] = s.pfx[tid];
     __syncthreads();
   }
-  // ---- compact the victims into cand[0..m): EF heads then the mp scored heads
-  if (c0 > e && mp > 0) {
-    for (uint32_t v0 = 0; v0 < mp; v0 += NT) {   // dst < src: chunked read-then-write
-      Cand x;
-      const uint32_t v = v0 + tid;
-      if (v < mp) x = c.cand[c0 + v];
-      __syncthreads();
-      if (v < mp) c.cand[e + v] = x;
-      __syncthreads();
-    }
-  }
+  for (uint32_t v = tid; v < m; v += NT) c.cand[v] = c.vbuf[v];
+  __syncthreads();
 }
 
 // Too many candidates for the leader's smem: choose, per over-full segment, the exact key
@@ -1150,7 +1297,7 @@ __device__ void narrow(Ctx& c, uint32_t e, uint32_t mp) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid < NSEG) {
     const uint32_t need = tid == 0 ? e : mp;
-    s.target[tid] = need + 2 * SLACK;
+    s.target[tid] = 3 * (need + SLACK);   // refill a reserve for several chunks
     s.pfx[tid] = 0;
     s.pmask[tid] = 0;
     s.below[tid] = 0;
@@ -1278,14 +1425,21 @@ __device__ void apply_chunk(Ctx& c, uint32_t m, uint32_t* vids_out) {
 __device__ void evict_k(Ctx& c, uint64_t k, uint32_t stamp, uint32_t* vids_out) {
   const Dev& d = *c.d;
   Smem& s = *c.s;
-  uint64_t done = 0;
+  uint64_t done = 0, chunk_end = 0;
   while (done < k) {
     const uint64_t to_cross = d.K - (s.st.E % d.K);
+    const bool first = done >= chunk_end;          // first sub-pass of a chunk between firings
+    if (first) chunk_end = done + min(k - done, to_cross);
     const uint32_t m = (uint32_t)min(min(k - done, to_cross), (uint64_t)MSUB);
-    select_chunk(c, m, stamp);
+    select_chunk(c, m, stamp, first);
+    uint64_t t0 = gtimer();
     apply_chunk(c, m, vids_out ? vids_out + done : nullptr);
+    if (threadIdx.x == 0) { const uint64_t t1 = gtimer(); s.st.tph[4] += t1 - t0; t0 = t1; }
     done += m;
-    if (s.st.E % d.K == 0) learn(c);
+    if (s.st.E % d.K == 0) {
+      learn(c);
+      if (threadIdx.x == 0) s.st.tph[5] += gtimer() - t0;
+    }
   }
   if (s.st.gtbl_used > ((d.gmask + 1) / 4) * 3) rebuild_ghost(c);
 }
@@ -1347,6 +1501,7 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
   }
   __syncthreads();
   const uint32_t stamp = (uint32_t)st.round;
+  uint64_t tA = gtimer();
   // ---- O4/O5 classify + probe (Alg.1 Classify P:550-564; strict prefix P:158)
   for (uint32_t j = threadIdx.x; j < n; j += NT) {
     const uint64_t H = b.h[bo + j];
@@ -1374,7 +1529,6 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
       if (q == Q_STRUCT) atomicAdd((unsigned long long*)&st.pb_acc[bin], 1ull);
       if (sl >= 0) {
         const uint64_t gi = c.base + (uint32_t)sl;
-        d.bpin[gi] = stamp;
         const uint32_t meta = d.bmeta[gi];
         if (j < h) {  // O7 hit (A9: credited to the old queue before re-routing)
           double dt = __dsub_rn(now, d.blast[gi]);
@@ -1394,7 +1548,7 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
         }
         // O7/O8 touch: last = now, hint overwritten (A9, A10)
         d.blast[gi] = now;
-        d.bmeta[gi] = meta_pack(q, tau, meta_ntok(meta));
+        d.bmeta[gi] = meta_pack(q, tau, meta_ntok(meta)) | M_PIN;   // pinned for this round (A11)
         d.bob[gi] = j;
         d.bomax[gi] = omax;
         if (q == Q_STRUCT) d.bps[gi] = p_struct(j, omax, st.par.gamma);
@@ -1442,8 +1596,15 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
   __syncthreads();
   if (st.err) return false;
   const uint64_t k = s.k, admit = s.admit;
+  if (threadIdx.x == 0) st.tph[0] += gtimer() - tA;
   // ---- O11 evictions (Alg.1 Evict x k, chunked at K crossings)
   if (k > 0) evict_k(c, k, stamp, b.o_vids ? b.o_vids + b.boff[i] : nullptr);
+  tA = gtimer();
+  // ---- unpin this request's resident blocks
+  for (uint32_t j = threadIdx.x; j < n; j += NT) {
+    const int32_t sl = b.slot[bo + j];
+    if (sl >= 0) d.bmeta[c.base + (uint32_t)sl] &= ~M_PIN;
+  }
   // ---- O12 insert New (Alg.1 Add: q.insert(b))
   if (threadIdx.x == 0 && st.next_id + admit > 0xFFFFFFFFull) {
     st.err = (uint32_t)(-SAE_E_OVERFLOW);
@@ -1485,7 +1646,11 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
     st.prompt_tokens += L;
   }
   __syncthreads();
-  if (st.tbl_used > (d.tmask + 1) / 4 * 3) rebuild_table(c);
+  if (threadIdx.x == 0) { const uint64_t t1 = gtimer(); st.tph[6] += t1 - tA; tA = t1; }
+  if (st.tbl_used > (d.tmask + 1) / 4 * 3) {
+    rebuild_table(c);
+    if (threadIdx.x == 0) st.tph[7] += gtimer() - tA;
+  }
   return true;
 }
 
@@ -1496,6 +1661,7 @@ __device__ Ctx make_ctx(const Dev& d, uint32_t r, uint32_t rank) {
   c.d = &d;
   c.s = reinterpret_cast<Smem*>(g_smem);
   c.cand = reinterpret_cast<Cand*>(g_smem + ((sizeof(Smem) + 15) / 16) * 16);
+  c.vbuf = c.cand + CAND_MAX;
   c.ctl = d.ctl + r;
   c.r = r;
   c.rank = rank;
@@ -1713,7 +1879,7 @@ static cudaError_t dalloc(sae_ctx* ctx, T** p, uint64_t n) {
 }
 
 static size_t smem_bytes() {
-  return ((sizeof(Smem) + 15) / 16) * 16 + sizeof(Cand) * CAND_MAX;
+  return ((sizeof(Smem) + 15) / 16) * 16 + sizeof(Cand) * (CAND_MAX + VCAP);
 }
 
 static cudaError_t launch_group(const void* fn, uint32_t grid, bool coop, cudaStream_t s, Dev& d,
@@ -2087,6 +2253,7 @@ sae_status sae_stats(sae_ctx* ctx, uint32_t replica, sae_replica_stats* out, sae
   out->select_cands = rs.select_cands;
   out->select_big = rs.select_big;
   for (int g = 0; g < 10; ++g) out->select_fail_seg[g] = rs.select_fail_seg[g];
+  for (int g = 0; g < 8; ++g) out->phase_ns[g] = rs.tph[g];
   out->resident = hq[4];
   for (int i = 0; i < 4; ++i) out->resident_by_queue[i] = hq[i];
   out->E = rs.E;

@@ -18,3 +18,4 @@ print("done", cache.stats(0).requests)
 st = cache.stats(0)
 print("chunks~", st.learner_firings, "passes", st.select_passes, "cands/pass", st.select_cands / max(st.select_passes, 1),
       "big", st.select_big, "fails", list(st.select_fail_seg), "evictions", st.evictions, "rounds", st.eviction_rounds)
+print("phase ms", [round(x / 1e6, 1) for x in st.phase_ns])
