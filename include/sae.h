@@ -164,8 +164,9 @@ typedef struct {
    * fallbacks), candidates sorted, passes with > 512 candidates, fallbacks per segment */
   uint64_t select_passes, select_cands, select_big, select_fail_seg[10];
   /* device time (ns, globaltimer) spent by the replica leader per phase: probe+touch,
-   * scan passes, narrowing, sort+check, apply, learn, insert+outputs, table rebuild */
-  uint64_t phase_ns[8];
+   * scan passes, narrowing, sort+check, apply, learn, insert+outputs, table rebuild, and for
+   * multi-CTA groups: command start barrier, leader's own partition, end barrier, spare */
+  uint64_t phase_ns[12];
   sae_params params;
 } sae_replica_stats;
 

@@ -73,7 +73,8 @@ struct RState {
   uint64_t evict_by_queue[4], evict_by_type[6], mae_by_type[6];
   uint64_t learner_firings, eviction_rounds, blocks_scored, blocks_scored_struct;
   uint64_t select_passes, select_cands, select_big, select_fail_seg[10];
-  uint64_t tph[8];          // leader phase timers (ns): probe, scan, narrow, select, apply, learn, insert, rebuild
+  uint64_t tph[12];         // leader phase timers (ns): probe, scan, narrow, select, apply, learn, insert, rebuild,
+                            // + issue(): start barrier, own partition, end barrier, (spare)
   uint64_t thr[16];        // per-segment candidate thresholds on k0 (heuristic; exactness never depends on them)
   sae_params par;
 };
@@ -89,21 +90,30 @@ struct Cand {           // one candidate victim: sort key (tier, k0, k1, k2) + s
 // partition of it between two group barriers.
 enum { CMD_SCAN = 1, CMD_HIST, CMD_COMPACT, CMD_REFRESH, CMD_CLEAR_T, CMD_FILL_T, CMD_CLEAR_G,
        CMD_FILL_G, CMD_COUNTQ, CMD_EXIT };
-struct GroupCtl {
-  unsigned bar_count, bar_gen, cmd, stamp;
-  unsigned ncand, nsel, shift, active;
-  unsigned segtot[16], cnt[16], selcnt[16];
-  unsigned tblcnt, gtblcnt, cntq[4];
+struct GroupCtl {          // hot words on separate 128-byte lines (polled / atomically updated)
+  alignas(128) unsigned bar_count;
+  alignas(128) unsigned bar_gen;
+  alignas(128) unsigned ncand;
+  alignas(128) unsigned nsel;
+  alignas(128) unsigned tblcnt;
+  alignas(128) unsigned gtblcnt;
+  alignas(128) unsigned segtot[16];
+  alignas(128) unsigned cnt[16];
+  alignas(128) unsigned selcnt[16];
+  alignas(128) unsigned cntq[4];
+  unsigned long long wscan_ns;        // worker 1's accumulated scan time (diagnostic)
+  alignas(128) unsigned cmd, stamp, shift, active;   // read-only while a command runs
   unsigned long long thr[16], pfx[16], pmask[16];
   double now, gamma, dt_eps, z_cut;
   double cw[3][5], mu[2], sigma[2];
-  unsigned hist[NSEG * 256];
+  alignas(128) unsigned hist[NSEG * 256];
 };
 
 struct Dev {
   uint32_t R, C, tmask, G, gmask, K, iv_ring, iv_keep, iv_min, nbins, B, traj_cap;
   uint32_t GP;          // CTAs per replica (group size)
   uint32_t cand_smem;   // 1: candidates live in the leader's smem (C <= CAND_MAX, GP == 1)
+  uint32_t bulk_ok;     // 1: replica bases are 16-byte aligned (C % 4 == 0): bulk-copy scan
   Cand* gcand;          // [R*C] global candidate buffer (large pools)
   Cand* gsel;           // [R*CAND_MAX] compacted candidates after narrowing
   GroupCtl* ctl;        // [R]
@@ -494,6 +504,9 @@ struct Smem {
   uint32_t below[16], target[16];
   uint32_t nv;
   uint32_t rhist[NSEG * 256];   // radix-select histograms (one 256-bin digit per segment)
+  __align__(8) uint64_t mbar[4];  // bulk-copy stage barriers (worker scan pipeline)
+  uint64_t wthr[16], wpfx[16], wpmask[16];   // worker copies of the leader's command parameters
+  double wcw[15], wmu[2], wsg[2];
 };
 
 struct Ctx {               // per-CTA view of one replica (group)
@@ -541,7 +554,7 @@ __device__ void group_bar(Ctx& c) {
       __threadfence();
       atomicAdd(&g->bar_gen, 1u);
     } else {
-      while (*genp == gen) __nanosleep(32);
+      while (*genp == gen) __nanosleep(64);
     }
     __threadfence();
   }
@@ -692,6 +705,166 @@ __device__ void scan_range(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P) {
   }
 }
 
+// ---- bulk asynchronous copies (cp.async.bulk, completion on an mbarrier) -------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Worker scan over [lo, hi) (lo a multiple of 4, replica base 16-byte aligned): the SoA
+// columns (meta u32, id u32, last f64, p_struct f64) are streamed tile by tile into
+// shared memory by bulk asynchronous copies, BSTAGES tiles in flight, and scored from
+// shared memory.  Same outputs as scan_range.
+constexpr int BTILE = 1024, BSTAGES = 4;
+constexpr uint32_t BTILE_BYTES = BTILE * (4 + 4 + 8 + 8);
+__device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P) {
+  const Dev& d = *c.d;
+  Smem& s = *c.s;
+  const int tid = threadIdx.x, lane = tid & 31;
+  Cand* gdst = d.gcand + c.base;
+  unsigned char* buf = reinterpret_cast<unsigned char*>(c.cand);
+  uint64_t tot[4] = {0, 0, 0, 0}, cnt[4] = {0, 0, 0, 0};
+  const uint64_t ntiles = (hi - lo + BTILE - 1) / BTILE;
+  auto stage_ptrs = [&](int st, uint32_t*& m, uint32_t*& iv, double*& l, double*& ps) {
+    unsigned char* b = buf + (size_t)st * BTILE_BYTES;
+    m = reinterpret_cast<uint32_t*>(b);
+    iv = reinterpret_cast<uint32_t*>(b + BTILE * 4);
+    l = reinterpret_cast<double*>(b + BTILE * 8);
+    ps = reinterpret_cast<double*>(b + BTILE * 16);
+  };
+  auto issue_tile = [&](uint64_t t) {
+    const int st = (int)(t % BSTAGES);
+    const uint64_t t0 = lo + t * BTILE;
+    const uint32_t n = (uint32_t)min((uint64_t)BTILE, hi - t0);
+    const uint32_t n4 = (n + 3) & ~3u;                 // 16-byte multiple (SoA is padded)
+    uint32_t *m, *iv;
+    double *l, *ps;
+    stage_ptrs(st, m, iv, l, ps);
+    mbar_expect_tx(&s.mbar[st], n4 * 24u);
+    bulk_g2s(m, d.bmeta + c.base + t0, n4 * 4u, &s.mbar[st]);
+    bulk_g2s(iv, d.bid + c.base + t0, n4 * 4u, &s.mbar[st]);
+    bulk_g2s(l, d.blast + c.base + t0, n4 * 8u, &s.mbar[st]);
+    bulk_g2s(ps, d.bps + c.base + t0, n4 * 8u, &s.mbar[st]);
+  };
+  if (tid == 0) {
+    for (int st = 0; st < BSTAGES; ++st) mbar_init(&s.mbar[st], 1);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (uint64_t t = 0; t < ntiles && t < (uint64_t)BSTAGES; ++t) issue_tile(t);
+  }
+  __syncthreads();
+  // thresholds as doubles (multi-turn: last; STRUCT: P) for the division-free prefilter
+  double* thrD = reinterpret_cast<double*>(&s.wpfx[0]);   // 16 doubles of scratch
+  if (tid < NSEG) {
+    const uint64_t T = P.thr[tid];
+    thrD[tid] = (T == ~0ull || tid == 0) ? __longlong_as_double(0x7ff0000000000000ll) : from_obits(T);
+  }
+  __syncthreads();
+  const double inflate = 1.0 + 0x1p-40;
+  for (uint64_t t = 0; t < ntiles; ++t) {
+    const int st = (int)(t % BSTAGES);
+    mbar_wait(&s.mbar[st], (uint32_t)((t / BSTAGES) & 1));
+    uint32_t *m, *iv;
+    double *l, *ps;
+    stage_ptrs(st, m, iv, l, ps);
+    const uint64_t t0 = lo + t * BTILE;
+    const uint32_t n = (uint32_t)min((uint64_t)BTILE, hi - t0);
+#pragma unroll
+    for (int u = 0; u < BTILE / NT; ++u) {
+      const uint32_t k = (uint32_t)(u * NT + tid);
+      bool take = false;
+      const uint32_t meta = k < n ? m[k] : 0u;
+      uint32_t q = 0, tau = 0, seg = 0;
+      if ((meta & (M_LIVE | M_PIN)) == M_LIVE) {
+        q = meta_q(meta);
+        tau = meta_tau(meta);
+        seg = seg_of(q, tau);
+        pk_add(tot, seg);
+        if (q == Q_EF) {
+          take = ((((uint64_t)meta_ntok(meta)) << 32) | iv[k]) <= P.thr[0];
+        } else if (q == Q_STRUCT) {
+          // prefilter (a superset of P <= T): cw*ps <= T*dt*(1+2^-40); exact P below
+          double dt = __dsub_rn(P.now, l[k]);
+          if (dt < P.dt_eps) dt = P.dt_eps;
+          take = __dmul_rn(P.cw[10 + tau], ps[k]) <= __dmul_rn(__dmul_rn(thrD[seg], dt), inflate);
+        } else {
+          take = l[k] <= thrD[seg];
+        }
+      }
+      Cand x;
+      if (take) {                         // exact keys for the (few) candidates
+        const uint32_t id = iv[k];
+        const double last = l[k];
+        x.ss = (uint32_t)(t0 + k) | ((q == Q_EF ? 0u : 1u) << 28);
+        x.seg = seg;
+        if (q == Q_EF) {
+          x.k0 = ((uint64_t)meta_ntok(meta) << 32) | id;
+          x.k1 = 0;
+          x.k2 = 0;
+        } else {
+          double dt = __dsub_rn(P.now, last);
+          if (dt < P.dt_eps) dt = P.dt_eps;
+          x.k1 = obits(last);
+          x.k2 = id;
+          if (q == Q_STRUCT) {
+            x.k0 = obits(__ddiv_rn(__dmul_rn(P.cw[10 + tau], ps[k]), dt));
+            take = x.k0 <= P.thr[seg];
+          } else {
+            const double pv = survival(dt, P.mu[q - 1], P.sg[q - 1], P.z_cut);
+            x.k0 = obits(__ddiv_rn(__dmul_rn(P.cw[(q - 1) * 5 + tau], pv), dt));
+          }
+        }
+        if (take) pk_add(cnt, seg);
+      }
+      const uint32_t bal = __ballot_sync(~0u, take);
+      if (bal) {
+        uint32_t basep = 0;
+        if (lane == 0) basep = atomicAdd(&c.ctl->ncand, (unsigned)__popc(bal));
+        basep = __shfl_sync(~0u, basep, 0);
+        if (take) gdst[basep + __popc(bal & ((1u << lane) - 1u))] = x;
+      }
+    }
+    __syncthreads();                       // stage st fully consumed
+    if (tid == 0 && t + BSTAGES < ntiles) issue_tile(t + BSTAGES);
+  }
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    for (int o = 16; o > 0; o >>= 1) {
+      tot[w] += __shfl_xor_sync(~0u, tot[w], o);
+      cnt[w] += __shfl_xor_sync(~0u, cnt[w], o);
+    }
+  }
+  if (lane < NSEG) {
+    const int w = lane >> 2, f = (lane & 3) * 16;
+    uint64_t tv = w == 0 ? tot[0] : w == 1 ? tot[1] : w == 2 ? tot[2] : tot[3];
+    uint64_t cv = w == 0 ? cnt[0] : w == 1 ? cnt[1] : w == 2 ? cnt[2] : cnt[3];
+    const uint32_t t16 = (uint32_t)((tv >> f) & 0xFFFFu), c16 = (uint32_t)((cv >> f) & 0xFFFFu);
+    if (t16) atomicAdd(&s.segtot[lane], t16);
+    if (c16) atomicAdd(&s.cnt[lane], c16);
+  }
+}
+
 // stride-halving tree sum over y[0..P) in smem (SURVEY c.3 TREE)
 __device__ double tree_sum(double* y, int P);
 
@@ -712,15 +885,33 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
         P.now = s.st.now;
         P.thr = (const unsigned long long*)s.st.thr; P.cw = &s.cw[0][0];
         P.mu = s.st.par.mu; P.sg = s.st.par.sigma;
-      } else {        // published by the leader before the command
+      } else {        // published by the leader before the command: stage into smem
+        if (tid < 16) s.wthr[tid] = __ldcg(&g->thr[tid]);
+        if (tid < 15) s.wcw[tid] = __ldcg(&g->cw[0][0] + tid);
+        if (tid < 2) { s.wmu[tid] = __ldcg(&g->mu[tid]); s.wsg[tid] = __ldcg(&g->sigma[tid]); }
+        __syncthreads();
         P.now = __ldcg(&g->now);
-        P.thr = g->thr; P.cw = &g->cw[0][0]; P.mu = g->mu; P.sg = g->sigma;
+        P.thr = (const unsigned long long*)s.wthr; P.cw = s.wcw; P.mu = s.wmu; P.sg = s.wsg;
       }
       P.stamp = __ldcg(&g->stamp);
       P.dt_eps = d.dt_eps;
       P.z_cut = d.z_cut;
-      part_range(d.C, c.rank, c.GP, lo, hi);
-      scan_range(c, lo, hi, P);
+      if (c.GP > 1) {
+        // the leader's smem holds the candidates: workers 1..GP-1 split the pool in
+        // 4-slot-aligned slices and stream it through shared memory
+        if (!leader) {
+          const uint64_t nw = c.GP - 1, w = c.rank - 1;
+          lo = ((uint64_t)d.C * w / nw) & ~3ull;
+          hi = w + 1 == nw ? d.C : (((uint64_t)d.C * (w + 1) / nw) & ~3ull);
+          const uint64_t tw0 = gtimer();
+          if (d.bulk_ok) scan_range_bulk(c, lo, hi, P);
+          else scan_range(c, lo, hi, P);
+          if (c.rank == 1 && tid == 0) g->wscan_ns += gtimer() - tw0;
+        }
+      } else {
+        part_range(d.C, c.rank, c.GP, lo, hi);
+        scan_range(c, lo, hi, P);
+      }
       __syncthreads();
       if (!d.cand_smem && tid < NSEG) {
         if (s.segtot[tid]) atomicAdd(&g->segtot[tid], s.segtot[tid]);
@@ -732,6 +923,8 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
       unsigned* h = reinterpret_cast<unsigned*>(c.cand);
       for (int i = tid; i < NSEG * 256; i += NT) h[i] = 0;
       __syncthreads();
+      if (tid < 16) { s.wpfx[tid] = __ldcg(&g->pfx[tid]); s.wpmask[tid] = __ldcg(&g->pmask[tid]); }
+      __syncthreads();
       const unsigned shift = __ldcg(&g->shift), active = __ldcg(&g->active);
       part_range(__ldcg(&g->ncand), c.rank, c.GP, lo, hi);
       const Cand* src = d.gcand + c.base;
@@ -739,7 +932,7 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
         const uint32_t seg = __ldcg(&src[i].seg);
         if (!((active >> seg) & 1u)) continue;
         const uint64_t key = seg >= 1 && seg <= 8 ? __ldcg(&src[i].k1) : __ldcg(&src[i].k0);
-        if ((key & __ldcg(&g->pmask[seg])) != __ldcg(&g->pfx[seg])) continue;
+        if ((key & s.wpmask[seg]) != s.wpfx[seg]) continue;
         atomicAdd(&h[seg * 256 + ((key >> shift) & 255u)], 1u);
       }
       __syncthreads();
@@ -749,6 +942,8 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
       break;
     }
     case CMD_COMPACT: {  // keep candidates at or below the (new) thresholds
+      if (tid < 16) s.wthr[tid] = __ldcg(&g->thr[tid]);
+      __syncthreads();
       part_range(__ldcg(&g->ncand), c.rank, c.GP, lo, hi);
       const Cand* src = d.gcand + c.base;
       Cand* dst = d.gsel + (uint64_t)c.r * CAND_MAX;
@@ -760,7 +955,7 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
         if (i < hi) {
           x.k0 = __ldcg(&src[i].k0); x.k1 = __ldcg(&src[i].k1);
           x.k2 = __ldcg(&src[i].k2); x.ss = __ldcg(&src[i].ss); x.seg = __ldcg(&src[i].seg);
-          take = seg_key(x) <= __ldcg(&g->thr[x.seg]);
+          take = seg_key(x) <= s.wthr[x.seg];
         }
         const uint32_t bal = __ballot_sync(~0u, take);
         if (bal) {
@@ -848,10 +1043,19 @@ __device__ void issue(Ctx& c, unsigned cmd) {
     return;
   }
   if (threadIdx.x == 0) c.ctl->cmd = cmd;
+  uint64_t t0 = gtimer();
   group_bar(c);                 // workers start
   if (cmd == CMD_EXIT) return;
+  uint64_t t1 = gtimer();
   run_cmd(c, cmd, true);
+  uint64_t t2 = gtimer();
   group_bar(c);                 // everyone done
+  if (threadIdx.x == 0) {
+    const uint64_t t3 = gtimer();
+    c.s->st.tph[8] += t1 - t0;
+    c.s->st.tph[9] += t2 - t1;
+    c.s->st.tph[10] += t3 - t2;
+  }
 }
 
 __device__ void worker_loop(Ctx& c) {
@@ -1104,8 +1308,8 @@ __device__ void radix_select(const Cand* a, uint32_t n, bool per_seg, uint32_t a
       if (bin != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&s.rhist[bin], (uint32_t)__popc(peers));
     }
     __syncthreads();
-    if (wid < NSEG && ((active >> wid) & 1u)) {
-      const int g = wid;
+    for (int g = wid; g < NSEG; g += NW) {
+      if (!((active >> g) & 1u)) continue;
       uint32_t v[8], loc = 0;
       for (int j = 0; j < 8; ++j) { v[j] = s.rhist[g * 256 + lane * 8 + j]; loc += v[j]; }
       uint32_t inc = loc;
@@ -1315,8 +1519,8 @@ __device__ void narrow(Ctx& c, uint32_t e, uint32_t mp) {
     __syncthreads();
     issue(c, CMD_HIST);
     // one warp per active segment: find the digit holding rank target
-    if (wid < NSEG && ((active >> wid) & 1u)) {
-      const int k = wid;
+    for (int k = wid; k < NSEG; k += NW) {
+      if (!((active >> k) & 1u)) continue;
       uint32_t v[8], loc = 0;
       for (int j = 0; j < 8; ++j) { v[j] = __ldcg(&g->hist[k * 256 + lane * 8 + j]); loc += v[j]; }
       uint32_t inc = loc;
@@ -1927,12 +2131,12 @@ sae_status sae_create(const sae_config* cfg, sae_ctx** out) {
   const uint64_t R = d.R, RC = R * d.C;
   CK(dalloc(ctx, &d.st, R));
   CK(dalloc(ctx, &d.bhash, RC));
-  CK(dalloc(ctx, &d.blast, RC));
-  CK(dalloc(ctx, &d.bid, RC));
-  CK(dalloc(ctx, &d.bmeta, RC));
+  CK(dalloc(ctx, &d.blast, RC + 4));   // +4: bulk-copy tail padding
+  CK(dalloc(ctx, &d.bid, RC + 4));   // +4: bulk-copy tail padding
+  CK(dalloc(ctx, &d.bmeta, RC + 4));   // +4: bulk-copy tail padding
   CK(dalloc(ctx, &d.bob, RC));
   CK(dalloc(ctx, &d.bomax, RC));
-  CK(dalloc(ctx, &d.bps, RC));
+  CK(dalloc(ctx, &d.bps, RC + 4));   // +4: bulk-copy tail padding
   CK(dalloc(ctx, &d.bacc, RC));
   CK(dalloc(ctx, &d.bpin, RC));
   CK(dalloc(ctx, &d.freestk, RC));
@@ -1965,6 +2169,7 @@ sae_status sae_create(const sae_config* cfg, sae_ctx** out) {
   }
   d.GP = (uint32_t)gp;
   d.cand_smem = (d.C <= (uint32_t)CAND_MAX && d.GP == 1) ? 1u : 0u;
+  d.bulk_ok = (d.C % 4 == 0) ? 1u : 0u;
   ctx->coresident = coresident;
   CK(dalloc(ctx, &d.ctl, R));
   CK(cudaMemset(d.ctl, 0, R * sizeof(GroupCtl)));
@@ -2253,7 +2458,12 @@ sae_status sae_stats(sae_ctx* ctx, uint32_t replica, sae_replica_stats* out, sae
   out->select_cands = rs.select_cands;
   out->select_big = rs.select_big;
   for (int g = 0; g < 10; ++g) out->select_fail_seg[g] = rs.select_fail_seg[g];
-  for (int g = 0; g < 8; ++g) out->phase_ns[g] = rs.tph[g];
+  for (int g = 0; g < 12; ++g) out->phase_ns[g] = rs.tph[g];
+  {
+    unsigned long long w = 0;
+    CK(cudaMemcpy(&w, &ctx->d.ctl[replica].wscan_ns, 8, cudaMemcpyDeviceToHost));
+    out->phase_ns[11] = w;
+  }
   out->resident = hq[4];
   for (int i = 0; i < 4; ++i) out->resident_by_queue[i] = hq[i];
   out->E = rs.E;

@@ -78,7 +78,7 @@ class sae_replica_stats(C.Structure):
                 ("iv_len", C.c_uint64 * 2), ("traj_count", C.c_uint64),
                 ("select_passes", C.c_uint64), ("select_cands", C.c_uint64),
                 ("select_big", C.c_uint64), ("select_fail_seg", C.c_uint64 * 10),
-                ("phase_ns", C.c_uint64 * 8),
+                ("phase_ns", C.c_uint64 * 12),
                 ("params", sae_params)]
 
 
