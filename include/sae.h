@@ -190,6 +190,12 @@ sae_status sae_set_params(sae_ctx* ctx, uint32_t replica, const sae_params* p, s
 sae_status sae_params_gather(sae_ctx* ctx, sae_params* dev_out, sae_stream s);
 /* Replace every replica's parameters from dev_in[n_replicas] (device), stream-ordered. */
 sae_status sae_params_scatter(sae_ctx* ctx, const sae_params* dev_in, sae_stream s);
+/* mean_w sync over the ALL-GATHERED parameters of n_total replicas laid out
+ * replica = point + n_points * seed: out[r] = all[r] with w replaced by the mean of w over
+ * the replicas of r's point, summed in seed order (identical at any GPU count).  Device
+ * pointers; n_total must be a multiple of n_points. */
+sae_status sae_params_point_mean(const sae_params* all_dev, uint32_t n_total, uint32_t n_points,
+                                 sae_params* out_dev, sae_stream s);
 
 /* Synchronously compute batch->total_blocks (reads prompt/decode lengths on the device). */
 sae_status sae_batch_blocks(sae_ctx* ctx, const sae_batch* batch, uint64_t* total_blocks, sae_stream s);

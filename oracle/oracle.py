@@ -307,3 +307,19 @@ class Replica:
         nv = int(voff[n])
         return ReplayResult(out4, vout[:nv].copy(), voff, None if hashes is None else hashes[:tot],
                             None if taus is None else taus[:tot], boff, self.traj(), self.stats())
+
+
+def point_mean_w(params: list, n_points: int) -> list:
+    """mean_w sync, plain: for point p and type t, s = 0.0; s = s + w[p +
+    n_points*i][t] for i in seed order; mean = s / S.  Returns new parameter dicts."""
+    S = len(params) // n_points
+    out = [dict(p, w=list(p["w"])) for p in params]
+    for p in range(n_points):
+        for t in range(5):
+            s = 0.0
+            for i in range(S):
+                s = s + params[p + n_points * i]["w"][t]
+            m = s / float(S)
+            for i in range(S):
+                out[p + n_points * i]["w"][t] = m
+    return out

@@ -2007,6 +2007,22 @@ __global__ void k_params_commit(Dev d, const sae_params* in, uint32_t r0, uint32
     if (r0 + i < d.R) d.st[r0 + i].par = in[i];
 }
 
+// mean_w sync: for parameter point p, w_mean[tau] = (sum over i = 0..S-1 in
+// index order of w[p + P*i][tau]) / S; every replica of point p gets w_mean.  Fixed
+// order => identical results at any GPU count (no fp64 all-reduce).
+__global__ void k_point_mean(const sae_params* all, uint32_t n_total, uint32_t n_points, sae_params* out) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_total) return;
+  const uint32_t p = r % n_points, S = n_total / n_points;
+  sae_params o = all[r];
+  for (int t = 0; t < 5; ++t) {
+    double acc = 0.0;
+    for (uint32_t i = 0; i < S; ++i) acc = __dadd_rn(acc, all[p + n_points * i].w[t]);
+    o.w[t] = __ddiv_rn(acc, (double)S);
+  }
+  out[r] = o;
+}
+
 __global__ void k_count_queues(Dev d, uint32_t r, unsigned long long* out5) {
   const uint64_t base = (uint64_t)r * d.C;
   for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < d.C; s += gridDim.x * blockDim.x) {
@@ -2522,6 +2538,15 @@ sae_status sae_gen_tokens(uint64_t seed, uint64_t n_pieces, const uint64_t* stre
 }
 
 uint64_t sae_launch_count(const sae_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+sae_status sae_params_point_mean(const sae_params* all_dev, uint32_t n_total, uint32_t n_points,
+                                 sae_params* out_dev, sae_stream st) {
+  sae_ctx* ctx = nullptr;
+  if (!all_dev || !out_dev || n_points == 0 || n_total % n_points != 0) return SAE_E_INVAL;
+  k_point_mean<<<(n_total + 255) / 256, 256, 0, (cudaStream_t)st>>>(all_dev, n_total, n_points, out_dev);
+  CK(cudaGetLastError());
+  return SAE_OK;
+}
 
 sae_status sae_profile(sae_ctx* ctx, int enable) {
   if (!ctx) return SAE_E_INVAL;

@@ -91,7 +91,7 @@ class sae_traj(C.Structure):
 EXPORTS = ["sae_create", "sae_destroy", "sae_set_params", "sae_params_gather", "sae_params_scatter",
            "sae_batch_blocks", "sae_admit_batch", "sae_lookup", "sae_evict", "sae_update",
            "sae_stats", "sae_get_traj", "sae_sync", "sae_last_error", "sae_gen_tokens",
-           "sae_launch_count", "sae_profile", "sae_profile_read"]
+           "sae_launch_count", "sae_profile", "sae_profile_read", "sae_params_point_mean"]
 
 _lib = None
 
@@ -122,6 +122,7 @@ def lib():
             "sae_gen_tokens": (i32, [u64, u64, vp, vp, vp, vp, vp, vp, vp, vp]),
             "sae_launch_count": (u64, [vp]),
             "sae_profile": (i32, [vp, i32]),
+            "sae_params_point_mean": (i32, [vp, u32, u32, vp, vp]),
             "sae_profile_read": (i32, [vp, P(C.c_double), P(u64)]),
         }
         for name, (res, args) in sig.items():
@@ -374,6 +375,16 @@ class SaeCache:
         n = C.c_uint64()
         self._check(lib().sae_profile_read(self.h, C.byref(ms), C.byref(n)))
         return ms.value, n.value
+
+
+def params_point_mean(all_params: torch.Tensor, n_points: int, stream=None) -> torch.Tensor:
+    """mean_w over seeds per parameter point (fixed order), on the device."""
+    out = torch.empty_like(all_params)
+    rc = lib().sae_params_point_mean(all_params.data_ptr(), all_params.shape[0], n_points,
+                                     out.data_ptr(), _stream(stream))
+    if rc != 0:
+        raise SaeError(rc, "sae_params_point_mean")
+    return out
 
 
 def gen_tokens(seed: int, pieces: dict, dst: np.ndarray, n_tokens: int, device="cuda",

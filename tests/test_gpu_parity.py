@@ -174,3 +174,55 @@ def test_gen_tokens_matches_numpy():
     tok, ty = S.gen_tokens(tr["tseed"], allp, dst, tr["n_tokens"])
     assert np.array_equal(u32(tok)[:tr["n_tokens"]], tr["tokens"])
     assert np.array_equal(ty.cpu().numpy()[:tr["n_tokens"]], tr["types"])
+
+
+def test_c5_mean_w_sync_matches_oracle():
+    """mean_w@E sync: after every epoch of E requests per replica the token
+    weights of each parameter point become the fixed-order mean over its seeds."""
+    from paper_2605_18825_b200 import replicas as RP
+    npts, nseeds, E, epochs = 32, 2, 150, 3
+    R = npts * nseeds
+    traces = []
+    for sd in range(nseeds):
+        t = T.generate(C.get("c5", n_requests=E * epochs), seed=0x5AEC1000 + sd)
+        T.materialize(t)
+        traces.append(t)
+    pol = C.policy_config(256, K=40)
+    cache = S.SaeCache(256, n_replicas=R, policy=pol, traj_capacity=1 << 12)
+    refs = []
+    for r in range(R):
+        sd, pt = RP.layout(r, npts)
+        cache.set_params(r, C.c5_point_params(pt))
+        p = dict(pol)
+        p["params"] = C.c5_point_params(pt)
+        refs.append(oracle.Replica(p))
+    offs = np.cumsum([0] + [t["n_tokens"] for t in traces])
+    tok = np.concatenate([t["tokens"] for t in traces])
+    typ = np.concatenate([t["types"] for t in traces])
+    for ep in range(epochs):
+        lo, hi = ep * E, (ep + 1) * E
+        cols = {k: [] for k in ("arrival", "prompt_off", "prompt_len", "decode_off", "decode_len",
+                                "flags", "spb", "replica")}
+        for r in range(R):
+            t = traces[RP.layout(r, npts)[0]]
+            for k in ("arrival", "prompt_len", "decode_len", "flags", "spb"):
+                cols[k].append(t[k][lo:hi])
+            o = np.uint64(offs[RP.layout(r, npts)[0]])
+            cols["prompt_off"].append(t["prompt_off"][lo:hi] + o)
+            cols["decode_off"].append(t["decode_off"][lo:hi] + o)
+            cols["replica"].append(np.full(hi - lo, r, np.uint32))
+        bb = {k: np.concatenate(v) for k, v in cols.items()}
+        bb["n"], bb["tokens"], bb["types"] = len(bb["arrival"]), tok, typ
+        out = cache.admit_batch(S.batch_to_torch(bb))
+        RP.sync_mean_w(cache, npts)
+        torch.cuda.synchronize()
+        o4, _ = unpack(out, bb["n"])
+        for r in range(R):
+            t = traces[RP.layout(r, npts)[0]]
+            res = refs[r].replay(t, lo, hi, want_hashes=False)
+            assert np.array_equal(o4[r * E:(r + 1) * E], res.out4), (ep, r)
+        newp = oracle.point_mean_w([x.params() for x in refs], npts)
+        for r in range(R):
+            refs[r].set_params(newp[r])
+    for r in range(R):
+        assert_params_equal(S.params_dict(cache.stats(r).params), refs[r].params())
