@@ -43,6 +43,10 @@ WORKLOADS = {
     "c2": dict(cfg="c2", per_step=5000, ref_step=1500,
                desc="C2 multi-turn-dominated trace (Table 2 row 50/30/10/5/5), 100K requests, "
                     "C=2304 blocks (36K tokens), 1 replica per GPU"),
+    "c4": dict(cfg="c4", per_step=2000, ref_step=2, prefill=100_000,
+               desc="C4 single-turn-dominated templated trace (Table 2 row 10/10/40/25/15), "
+                    "4M-block (64 Mi-token) pool, one 148-CTA cooperative replica group per GPU; "
+                    "pool pre-filled with the trace's first 100K requests (untimed)"),
     "c5": dict(cfg="c5", per_step=250, ref_step=60,
                desc="C5 parameter-sweep replicas: balanced trace, C=2304, 32 points x seeds, "
                     "replicas per GPU = 1024/N"),
@@ -133,21 +137,40 @@ def slice_batch(tr: dict, lo: int, hi: int, replica: int = 0) -> dict:
 
 
 # ------------------------------------------------------------------------------------
+def oracle_fill(R, tr, cap: int, limit: int) -> int:
+    """Replay requests while none can evict (resident + the chunk's blocks <= capacity), in
+    chunks; returns the index of the first request that may evict.  Keeps the oracle's
+    untimed pre-fill of the 4M-block pool to seconds."""
+    nb = (-(-tr["prompt_len"].astype(np.int64) // 16) - (-tr["decode_len"].astype(np.int64) // 16))
+    pos, chunk = 0, 4000
+    while pos < limit:
+        res = R.size()
+        hi = min(pos + chunk, limit)
+        if res + int(nb[pos:hi].sum()) <= cap:
+            R.replay(tr, pos, hi, want_hashes=False)
+            pos = hi
+        elif chunk > 1:
+            chunk //= 2
+        else:
+            break
+    return pos
+
+
 def run_reference(args, wl, ws, rank):
     """The oracle (as it stands) on the host cores: the reference arm."""
     if rank != 0:
         return
     import oracle
     n_need = wl["ref_step"] * (args.warmup + args.steps)
+    pre = wl.get("prefill", 0)
     if wl["cfg"] == "c5":
         tr = make_trace(wl, 0, n_requests=max(n_need, 1000))
-        pol = CFG.policy_config(tr["config"]["capacity"])
     else:
-        tr = make_trace(wl, 0, n_requests=None)
-        pol = CFG.policy_config(tr["config"]["capacity"])
+        tr = make_trace(wl, 0, n_requests=(pre + n_need) if pre else None)
+    pol = CFG.policy_config(tr["config"]["capacity"])
     R = oracle.Replica(pol)
+    pos = oracle_fill(R, tr, pol["capacity"], pre) if pre else 0   # untimed pre-fill
     times, reqs = [], 0
-    pos = 0
     for step in range(args.warmup + args.steps):
         lo, hi = pos, min(pos + wl["ref_step"], tr["n"])
         t0 = time.perf_counter()
@@ -179,6 +202,19 @@ def cpu_baseline(wl, tr, seconds: float = 15.0):
     """The oracle as it stands, single thread, on a bounded sample of the workload."""
     import oracle
     pol = CFG.policy_config(tr["config"]["capacity"])
+    pre = wl.get("prefill", 0)
+    if pre:   # C4: pre-fill the 4M-block pool up to its first eviction (untimed), then time rounds
+        R = oracle.Replica(pol)
+        pre = oracle_fill(R, tr, pol["capacity"], pre)
+        t0 = time.perf_counter()
+        pos = pre
+        while time.perf_counter() - t0 < seconds and pos < tr["n"]:
+            R.replay(tr, pos, pos + 1, want_hashes=False)
+            pos += 1
+        dt = time.perf_counter() - t0
+        return {"value": (pos - pre) / dt, "unit": "req/s", "cores": 1, "kind": "oracle",
+                "sample": "requests %d..%d of the rank-0 c4 trace (the first eviction rounds) after "
+                          "an untimed pre-fill of the 4M-block pool (%.1f s, single thread)" % (pre, pos, dt)}
     t0 = time.perf_counter()
     done, reps = 0, 0
     while time.perf_counter() - t0 < seconds:
@@ -255,12 +291,17 @@ def run_ours(args, wl, ws, rank, local):
     else:
         R = 1
         per = wl["per_step"]
-        tr0 = make_trace(wl, rank)
+        pre = wl.get("prefill", 0)
+        tr0 = make_trace(wl, rank, n_requests=(pre + per * (W + 2 * K)) if pre else None)
         pol = CFG.policy_config(tr0["config"]["capacity"])
         cache = S.SaeCache(pol["capacity"], n_replicas=1, policy=pol)
+        for lo in range(0, pre, 20000):   # untimed pre-fill of the pool
+            cache.admit_batch(S.batch_to_torch(slice_batch(tr0, lo, min(lo + 20000, pre)),
+                                               device=torch.device("cuda", local)))
+            torch.cuda.synchronize()
 
         def step_batch(step):
-            return slice_batch(tr0, step * per, (step + 1) * per)
+            return slice_batch(tr0, pre + step * per, pre + (step + 1) * per)
 
         arena_tok, arena_typ = tr0["tokens"], tr0["types"]
 
@@ -369,7 +410,21 @@ def run_ours(args, wl, ws, rank, local):
             dist.destroy_process_group()
         return
     hbm, src = peaks()
-    alg_bytes = 14.0 * scored + 8.0 * scored_struct
+    alg_bytes = 14.0 * scored + 4.0 * scored_struct
+    # device-timer view of the fused score/select scan (multi-CTA groups: worker 1's
+    # streamed slice; single-CTA replicas: the leader's scan phase), per pass
+    passes = d("select_passes")
+    ph1 = sum(b.phase_ns[1] - a.phase_ns[1] for a, b in zip(st0, st1)) / max(R, 1)
+    ph11 = st1[0].phase_ns[11] - st0[0].phase_ns[11]
+    scan_ns = ph11 if ph11 > 0 else ph1
+    phase_info = {"passes_per_request": passes / max(req, 1),
+                  "required_passes_per_request": (d("eviction_rounds") + d("learner_firings")) / max(req, 1),
+                  "scan_ns_per_pass": scan_ns / max(passes / max(R, 1), 1),
+                  "bytes_streamed_per_pass": (20.0 * pol["capacity"]) if ph11 > 0 else None,
+                  "phase_ms_per_step": [round((b - a) / 1e6 / K, 3) for a, b in
+                                        zip(st0[0].phase_ns, st1[0].phase_ns)]}
+    if ph11 > 0:
+        phase_info["streamed_GBps"] = phase_info["bytes_streamed_per_pass"] / phase_info["scan_ns_per_pass"]
     avg_ms = rep_ms / max(rep_n, 1)
     achieved = (alg_bytes / max(rep_n, 1)) / (avg_ms * 1e-3) / 1e9 if rep_n else 0.0
     traffic = None
@@ -394,6 +449,7 @@ def run_ours(args, wl, ws, rank, local):
         "hit_rate_blocks": hit_blk / max(look, 1),
         "gpu_launches": int(launches),
         "clocks": clocks,
+        "score_select_phase": phase_info,
         "roofline": {"bound": "hbm", "kernel": "k_replay", "achieved": achieved, "peak": hbm,
                      "peak_source": src, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic,

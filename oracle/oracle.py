@@ -96,6 +96,7 @@ def lib():
             "orc_update": (None, [vp]),
             "orc_get_stats": (None, [vp, P(OrcStats)]),
             "orc_traj_count": (u64, [vp]),
+            "orc_size": (u64, [vp]),
             "orc_traj_get": (None, [vp, vp]),
             "orc_intervals": (u64, [vp, i32, vp, u64]),
             "orc_resident": (u64, [vp, vp, vp, vp, vp, vp, vp, vp, vp, u64]),
@@ -210,6 +211,10 @@ class Replica:
         s = OrcStats()
         lib().orc_get_stats(self.h, C.byref(s))
         return s
+
+    def size(self) -> int:
+        """Number of resident blocks (cheap)."""
+        return int(lib().orc_size(self.h))
 
     def traj(self) -> list:
         n = lib().orc_traj_count(self.h)

@@ -951,6 +951,7 @@ void orc_get_stats(void* h, orc_stats* out) {
 }
 
 uint64_t orc_traj_count(void* h) { return ((Replica*)h)->traj.size(); }
+uint64_t orc_size(void* h) { return ((Replica*)h)->res.size(); }
 void orc_traj_get(void* h, orc_traj* out) {
   Replica& R = *(Replica*)h;
   for (size_t i = 0; i < R.traj.size(); ++i) out[i] = R.traj[i];

@@ -126,7 +126,7 @@ struct Dev {
   uint32_t* bmeta;
   uint32_t* bob;
   uint32_t* bomax;
-  double* bps;
+  float* blr;           // ln(o_b/o_max) as fp32 (-inf for o_b = 0): gamma-independent prefilter input
   uint32_t* bacc;
   uint32_t* bpin;
   uint32_t* freestk;
@@ -209,6 +209,19 @@ __device__ double p_struct(uint32_t ob, uint32_t omax, double gam) {
   double r = __ddiv_rn((double)ob, (double)omax);
   return __dsub_rn(1.0, dm::ex(__dmul_rn(gam, dm::ln(r))));
 }
+// gamma-independent per-block input of the STRUCT prefilter
+__device__ __forceinline__ float lr_of(uint32_t ob, uint32_t omax) {
+  if (ob == 0) return __int_as_float(0xff800000);   // -inf: p = 1
+  return (float)dm::ln(__ddiv_rn((double)ob, (double)omax));
+}
+// A guaranteed lower bound of Eq.(2)'s p = 1 - exp(gamma * ln(o/o_max)): fp32 exp (relative
+// error < 1e-5 over the argument range [-34, 0]) inflated by 2^-10.  Used only to decide
+// which STRUCT blocks need their exact score; never to order them.
+__device__ __forceinline__ double p_struct_lo(float lr, float gam) {
+  const double e = (double)__expf(gam * lr);
+  return 1.0 - fmin(1.0, e * (1.0 + 0x1p-10));
+}
+
 // Alg.1 Classify
 __device__ __forceinline__ uint32_t classify(uint32_t tau, bool mt, bool ag, bool cid, bool is_struct,
                                              bool untempl) {
@@ -502,6 +515,7 @@ struct Smem {
   uint64_t k, admit;
   uint64_t pfx[16], pmask[16];
   uint32_t below[16], target[16];
+  unsigned long long kmin[16];
   uint32_t nv;
   uint32_t rhist[NSEG * 256];   // radix-select histograms (one 256-bin digit per segment)
   __align__(8) uint64_t mbar[4];  // bulk-copy stage barriers (worker scan pipeline)
@@ -563,7 +577,7 @@ __device__ void group_bar(Ctx& c) {
 
 // Parameters of a scan, from the leader's smem (leader) or the control block (workers).
 struct ScanP {
-  double now, dt_eps, z_cut;
+  double now, dt_eps, z_cut, gamma;
   uint32_t stamp;
   const unsigned long long* thr;
   const double* cw;        // [3][5]
@@ -598,14 +612,19 @@ __device__ __forceinline__ bool score_one(const Dev& d, const ScanP& P, uint32_t
     x.k1 = 0;
     x.k2 = 0;
     take = x.k0 <= P.thr[seg];
-  } else if (q == Q_STRUCT) {           // Eq.(2)+(3) with the cached p_struct
+  } else if (q == Q_STRUCT) {           // Eq.(2)+(3): prefilter by a lower bound, then exact
     double dt = __dsub_rn(P.now, last);
     if (dt < P.dt_eps) dt = P.dt_eps;
-    const double Pv = __ddiv_rn(__dmul_rn(P.cw[10 + tau], __ldcg(d.bps + gi)), dt);
-    x.k0 = obits(Pv);
-    x.k1 = obits(last);
-    x.k2 = id;
-    take = x.k0 <= P.thr[seg];
+    const double T = P.thr[seg] == ~0ull ? __longlong_as_double(0x7ff0000000000000ll) : from_obits(P.thr[seg]);
+    take = __dmul_rn(P.cw[10 + tau], p_struct_lo(__ldcg(d.blr + gi), (float)P.gamma)) <=
+           __dmul_rn(__dmul_rn(T, dt), 1.0 + 0x1p-40);
+    if (take) {
+      const double ps = p_struct(__ldcg(d.bob + gi), __ldcg(d.bomax + gi), P.gamma);
+      x.k0 = obits(__ddiv_rn(__dmul_rn(P.cw[10 + tau], ps), dt));
+      x.k1 = obits(last);
+      x.k2 = id;
+      take = x.k0 <= P.thr[seg];
+    }
   } else {                              // multi-turn class (queue, tau): Eq.(1)+(3) for heads
     x.k1 = obits(last);
     x.k2 = id;
@@ -738,7 +757,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // shared memory by bulk asynchronous copies, BSTAGES tiles in flight, and scored from
 // shared memory.  Same outputs as scan_range.
 constexpr int BTILE = 1024, BSTAGES = 4;
-constexpr uint32_t BTILE_BYTES = BTILE * (4 + 4 + 8 + 8);
+constexpr uint32_t BTILE_BYTES = BTILE * (4 + 4 + 8 + 4);
 __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P) {
   const Dev& d = *c.d;
   Smem& s = *c.s;
@@ -747,12 +766,12 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
   unsigned char* buf = reinterpret_cast<unsigned char*>(c.cand);
   uint64_t tot[4] = {0, 0, 0, 0}, cnt[4] = {0, 0, 0, 0};
   const uint64_t ntiles = (hi - lo + BTILE - 1) / BTILE;
-  auto stage_ptrs = [&](int st, uint32_t*& m, uint32_t*& iv, double*& l, double*& ps) {
+  auto stage_ptrs = [&](int st, uint32_t*& m, uint32_t*& iv, double*& l, float*& lr) {
     unsigned char* b = buf + (size_t)st * BTILE_BYTES;
     m = reinterpret_cast<uint32_t*>(b);
     iv = reinterpret_cast<uint32_t*>(b + BTILE * 4);
     l = reinterpret_cast<double*>(b + BTILE * 8);
-    ps = reinterpret_cast<double*>(b + BTILE * 16);
+    lr = reinterpret_cast<float*>(b + BTILE * 16);
   };
   auto issue_tile = [&](uint64_t t) {
     const int st = (int)(t % BSTAGES);
@@ -760,13 +779,14 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
     const uint32_t n = (uint32_t)min((uint64_t)BTILE, hi - t0);
     const uint32_t n4 = (n + 3) & ~3u;                 // 16-byte multiple (SoA is padded)
     uint32_t *m, *iv;
-    double *l, *ps;
-    stage_ptrs(st, m, iv, l, ps);
-    mbar_expect_tx(&s.mbar[st], n4 * 24u);
+    double* l;
+    float* lrs;
+    stage_ptrs(st, m, iv, l, lrs);
+    mbar_expect_tx(&s.mbar[st], n4 * 20u);
     bulk_g2s(m, d.bmeta + c.base + t0, n4 * 4u, &s.mbar[st]);
     bulk_g2s(iv, d.bid + c.base + t0, n4 * 4u, &s.mbar[st]);
     bulk_g2s(l, d.blast + c.base + t0, n4 * 8u, &s.mbar[st]);
-    bulk_g2s(ps, d.bps + c.base + t0, n4 * 8u, &s.mbar[st]);
+    bulk_g2s(lrs, d.blr + c.base + t0, n4 * 4u, &s.mbar[st]);
   };
   if (tid == 0) {
     for (int st = 0; st < BSTAGES; ++st) mbar_init(&s.mbar[st], 1);
@@ -782,12 +802,14 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
   }
   __syncthreads();
   const double inflate = 1.0 + 0x1p-40;
+  const float gamf = (float)P.gamma;
   for (uint64_t t = 0; t < ntiles; ++t) {
     const int st = (int)(t % BSTAGES);
     mbar_wait(&s.mbar[st], (uint32_t)((t / BSTAGES) & 1));
     uint32_t *m, *iv;
-    double *l, *ps;
-    stage_ptrs(st, m, iv, l, ps);
+    double* l;
+    float* lrs;
+    stage_ptrs(st, m, iv, l, lrs);
     const uint64_t t0 = lo + t * BTILE;
     const uint32_t n = (uint32_t)min((uint64_t)BTILE, hi - t0);
 #pragma unroll
@@ -804,10 +826,11 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
         if (q == Q_EF) {
           take = ((((uint64_t)meta_ntok(meta)) << 32) | iv[k]) <= P.thr[0];
         } else if (q == Q_STRUCT) {
-          // prefilter (a superset of P <= T): cw*ps <= T*dt*(1+2^-40); exact P below
+          // prefilter (a superset of P <= T) with a lower bound of p; exact P below
           double dt = __dsub_rn(P.now, l[k]);
           if (dt < P.dt_eps) dt = P.dt_eps;
-          take = __dmul_rn(P.cw[10 + tau], ps[k]) <= __dmul_rn(__dmul_rn(thrD[seg], dt), inflate);
+          take = __dmul_rn(P.cw[10 + tau], p_struct_lo(lrs[k], gamf)) <=
+                 __dmul_rn(__dmul_rn(thrD[seg], dt), inflate);
         } else {
           take = l[k] <= thrD[seg];
         }
@@ -828,7 +851,9 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
           x.k1 = obits(last);
           x.k2 = id;
           if (q == Q_STRUCT) {
-            x.k0 = obits(__ddiv_rn(__dmul_rn(P.cw[10 + tau], ps[k]), dt));
+            const uint64_t gi = c.base + t0 + k;
+            const double ps = p_struct(__ldcg(d.bob + gi), __ldcg(d.bomax + gi), P.gamma);
+            x.k0 = obits(__ddiv_rn(__dmul_rn(P.cw[10 + tau], ps), dt));
             take = x.k0 <= P.thr[seg];
           } else {
             const double pv = survival(dt, P.mu[q - 1], P.sg[q - 1], P.z_cut);
@@ -894,6 +919,7 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
         P.thr = (const unsigned long long*)s.wthr; P.cw = s.wcw; P.mu = s.wmu; P.sg = s.wsg;
       }
       P.stamp = __ldcg(&g->stamp);
+      P.gamma = leader ? s.st.par.gamma : __ldcg(&g->gamma);
       P.dt_eps = d.dt_eps;
       P.z_cut = d.z_cut;
       if (c.GP > 1) {
@@ -971,17 +997,8 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
       }
       break;
     }
-    case CMD_REFRESH: {  // gamma changed: recompute the cached structural priorities
-      const double gam = leader ? s.st.par.gamma : __ldcg(&g->gamma);
-      part_range(d.C, c.rank, c.GP, lo, hi);
-      for (uint64_t sl = lo + tid; sl < hi; sl += NT) {
-        const uint64_t gi = c.base + sl;
-        const uint32_t m = __ldcg(d.bmeta + gi);
-        if ((m & M_LIVE) && meta_q(m) == Q_STRUCT)
-          d.bps[gi] = p_struct(__ldcg(d.bob + gi), __ldcg(d.bomax + gi), gam);
-      }
+    case CMD_REFRESH:    // (no cached structural priority any more: nothing to refresh)
       break;
-    }
     case CMD_CLEAR_T: {
       const uint64_t tb = (uint64_t)d.tmask + 1;
       part_range(tb, c.rank, c.GP, lo, hi);
@@ -1242,7 +1259,6 @@ __device__ void learn(Ctx& c) {
   __syncthreads();
   double cw_old[4];
   for (int t = 0; t < 4; ++t) cw_old[t] = s.cw[2][t];
-  if (p.gamma != gamma_old) refresh_pstruct(c);
   recompute_cw(s);
   __syncthreads();
   // STRUCT-class thresholds follow a pure rescaling of alpha*w (heuristic only; the
@@ -1356,6 +1372,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
         for (int i = 0; i < 16; ++i) { g->segtot[i] = 0; g->cnt[i] = 0; g->thr[i] = st.thr[i]; }
         for (int q = 0; q < 3; ++q) for (int t = 0; t < 5; ++t) g->cw[q][t] = s.cw[q][t];
         for (int i = 0; i < 2; ++i) { g->mu[i] = st.par.mu[i]; g->sigma[i] = st.par.sigma[i]; }
+        g->gamma = st.par.gamma;
       }
     }
     __syncthreads();
@@ -1436,9 +1453,11 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
   uint64_t Kth = nc >= m ? s.pfx[0] : ~0ull;
   // ---- stage the victims: every candidate with k0 <= Kth (the m smallest plus key ties)
   if (tid == 0) s.nv = 0;
+  if (tid < 16) s.kmin[tid] = ~0ull;
   __syncthreads();
   for (uint32_t i0 = 0; i0 < nc; i0 += NT) {
     const uint32_t i = i0 + tid;
+    if (i < nc) atomicMin(&s.kmin[c.cand[i].seg], (unsigned long long)seg_key(c.cand[i]));
     const bool take = i < nc && c.cand[i].k0 <= Kth;
     const uint32_t bal = __ballot_sync(~0u, take);
     uint32_t basep = 0;
@@ -1486,6 +1505,30 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
     if (tid < NSEG && ((shrink >> tid) & 1u)) st.thr[tid] = s.pfx[tid];
     __syncthreads();
   }
+  // ---- grow a segment's threshold before its reserve runs dry (avoids refills): double
+  //      the key distance from the smallest candidate (keys: EF (ntok,id); class last;
+  //      STRUCT P).  Heuristic only -- exactness is re-proved every pass.
+  if (tid < NSEG && !((shrink >> tid) & 1u)) {
+    const uint32_t g = tid;
+    const uint64_t T = st.thr[g];
+    const uint32_t left = s.cnt[g] - min(s.cnt[g], s.used[g]);
+    if (T != ~0ull && s.segtot[g] > s.cnt[g] && left < 2 * s.used[g] + SLACK) {
+      const uint64_t km = s.kmin[g] == ~0ull ? T : (uint64_t)s.kmin[g];
+      uint64_t Tn;
+      if (g == 0) {
+        const uint64_t dlt = max(T - min(km, T), (uint64_t)4096);
+        Tn = T + dlt < T ? ~0ull : T + dlt;
+      } else if (g <= 8) {
+        const double Tl = from_obits(T), kl = from_obits(km);
+        Tn = obits(Tl + fmax(Tl - kl, 1.0));
+      } else {
+        const double Tp = from_obits(T), kp = from_obits(km);
+        Tn = obits(fmax(2.0 * Tp - kp, 1.5 * Tp));
+      }
+      st.thr[g] = Tn;
+    }
+  }
+  __syncthreads();
   for (uint32_t v = tid; v < m; v += NT) c.cand[v] = c.vbuf[v];
   __syncthreads();
 }
@@ -1755,7 +1798,7 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
         d.bmeta[gi] = meta_pack(q, tau, meta_ntok(meta)) | M_PIN;   // pinned for this round (A11)
         d.bob[gi] = j;
         d.bomax[gi] = omax;
-        if (q == Q_STRUCT) d.bps[gi] = p_struct(j, omax, st.par.gamma);
+        d.blr[gi] = lr_of(j, omax);
       } else if (j >= h) {  // O9 miss-after-evict, consumed (A30)
         const uint64_t H = b.h[bo + j];
         const int32_t gp = tbl_find_pos(gkey, d.gmask, H);
@@ -1830,7 +1873,7 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
     d.bmeta[gi] = meta_pack(q, tau, b.ntok[bo + j]);
     d.bob[gi] = j;
     d.bomax[gi] = omax;
-    d.bps[gi] = q == Q_STRUCT ? p_struct(j, omax, st.par.gamma) : 0.0;
+    d.blr[gi] = lr_of(j, omax);
     tbl_insert(tkey, tval, d.tmask, H, sl, &st.tbl_used);
   }
   __syncthreads();
@@ -1989,18 +2032,7 @@ __global__ void k_params_gather(Dev d, sae_params* out) {
 }
 // replace parameters; the cached p_struct of a replica is refreshed if its gamma changed
 __global__ void k_params_scatter(Dev d, const sae_params* in, uint32_t r0, uint32_t nr) {
-  const uint32_t r = r0 + blockIdx.y;
-  if (r >= d.R || blockIdx.y >= nr) return;
-  const double g_old = d.st[r].par.gamma;
-  const sae_params np = in[blockIdx.y];
-  __syncthreads();
-  const uint64_t base = (uint64_t)r * d.C;
-  if (np.gamma != g_old) {
-    for (uint32_t sl = blockIdx.x * blockDim.x + threadIdx.x; sl < d.C; sl += gridDim.x * blockDim.x) {
-      const uint32_t m = d.bmeta[base + sl];
-      if ((m & M_LIVE) && meta_q(m) == Q_STRUCT) d.bps[base + sl] = p_struct(d.bob[base + sl], d.bomax[base + sl], np.gamma);
-    }
-  }
+  // parameters only feed the kernels through RState (no cached gamma-dependent state)
 }
 __global__ void k_params_commit(Dev d, const sae_params* in, uint32_t r0, uint32_t nr) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += gridDim.x * blockDim.x)
@@ -2152,7 +2184,7 @@ sae_status sae_create(const sae_config* cfg, sae_ctx** out) {
   CK(dalloc(ctx, &d.bmeta, RC + 4));   // +4: bulk-copy tail padding
   CK(dalloc(ctx, &d.bob, RC));
   CK(dalloc(ctx, &d.bomax, RC));
-  CK(dalloc(ctx, &d.bps, RC + 4));   // +4: bulk-copy tail padding
+  CK(dalloc(ctx, &d.blr, RC + 4));   // +4: bulk-copy tail padding
   CK(dalloc(ctx, &d.bacc, RC));
   CK(dalloc(ctx, &d.bpin, RC));
   CK(dalloc(ctx, &d.freestk, RC));
