@@ -516,7 +516,7 @@ struct Smem {
   uint64_t pfx[16], pmask[16];
   uint32_t below[16], target[16];
   unsigned long long kmin[16];
-  uint32_t nv;
+  uint32_t nv, nw;          // nw: this CTA's candidates awaiting finalize_key (global mode)
   uint32_t rhist[NSEG * 256];   // radix-select histograms (one 256-bin digit per segment)
   __align__(8) uint64_t mbar[4];  // bulk-copy stage barriers (worker scan pipeline)
   uint64_t wthr[16], wpfx[16], wpmask[16];   // worker copies of the leader's command parameters
@@ -601,44 +601,80 @@ __device__ __forceinline__ void pk_add(uint64_t (&pk)[4], uint32_t seg) {
   }
 }
 
+// Candidacy of one resident, unpinned block (a4).  Exact for EF (key (ntok, id)) and the
+// multi-turn classes (key: last); conservative for STRUCT (a lower bound of P against the
+// threshold).  The exact Eq.(1)-(3) scores of the (few) candidates are computed afterwards
+// by finalize_keys, outside the streaming loop.
 __device__ __forceinline__ bool score_one(const Dev& d, const ScanP& P, uint32_t meta, uint32_t id,
                                           double last, uint64_t gi, uint32_t sl, Cand& x,
                                           uint32_t& seg) {
   const uint32_t q = meta_q(meta), tau = meta_tau(meta);
   seg = seg_of(q, tau);
   bool take;
+  x.k2 = id;
+  x.k1 = obits(last);
   if (q == Q_EF) {                      // Stage 1 key (num_tokens, id)
     x.k0 = ((uint64_t)meta_ntok(meta) << 32) | id;
     x.k1 = 0;
     x.k2 = 0;
     take = x.k0 <= P.thr[seg];
-  } else if (q == Q_STRUCT) {           // Eq.(2)+(3): prefilter by a lower bound, then exact
+  } else if (q == Q_STRUCT) {           // prefilter: lower bound of Eq.(2)+(3) vs threshold
     double dt = __dsub_rn(P.now, last);
     if (dt < P.dt_eps) dt = P.dt_eps;
     const double T = P.thr[seg] == ~0ull ? __longlong_as_double(0x7ff0000000000000ll) : from_obits(P.thr[seg]);
     take = __dmul_rn(P.cw[10 + tau], p_struct_lo(__ldcg(d.blr + gi), (float)P.gamma)) <=
            __dmul_rn(__dmul_rn(T, dt), 1.0 + 0x1p-40);
-    if (take) {
-      const double ps = p_struct(__ldcg(d.bob + gi), __ldcg(d.bomax + gi), P.gamma);
-      x.k0 = obits(__ddiv_rn(__dmul_rn(P.cw[10 + tau], ps), dt));
-      x.k1 = obits(last);
-      x.k2 = id;
-      take = x.k0 <= P.thr[seg];
-    }
-  } else {                              // multi-turn class (queue, tau): Eq.(1)+(3) for heads
-    x.k1 = obits(last);
-    x.k2 = id;
+    x.k0 = 0;
+  } else {                              // multi-turn class (queue, tau): key last
     take = x.k1 <= P.thr[seg];
-    if (take) {
-      double dt = __dsub_rn(P.now, last);
-      if (dt < P.dt_eps) dt = P.dt_eps;
-      const double p = survival(dt, P.mu[q - 1], P.sg[q - 1], P.z_cut);
-      x.k0 = obits(__ddiv_rn(__dmul_rn(P.cw[(q - 1) * 5 + tau], p), dt));
-    }
+    x.k0 = 0;
   }
   x.ss = sl | ((q == Q_EF ? 0u : 1u) << 28);
   x.seg = seg;
   return take;
+}
+
+// Exact score of a scored candidate: Eq.(1) survival (multi-turn) or Eq.(2) (STRUCT),
+// then Eq.(3) P = ((alpha_q * w_tau) * p) / dt, fixed op order (SURVEY c.4).
+__device__ __forceinline__ void finalize_key(const Dev& d, uint64_t base, const ScanP& P, Cand& x) {
+  if (x.seg == 0 || x.seg >= 16) return;
+  const double last = from_obits(x.k1);
+  double dt = __dsub_rn(P.now, last);
+  if (dt < P.dt_eps) dt = P.dt_eps;
+  if (x.seg <= 8) {
+    const uint32_t q = 1 + (x.seg - 1) / 4, tau = (x.seg - 1) & 3;
+    const double p = survival(dt, P.mu[q - 1], P.sg[q - 1], P.z_cut);
+    x.k0 = obits(__ddiv_rn(__dmul_rn(P.cw[(q - 1) * 5 + tau], p), dt));
+  } else {
+    const uint32_t tau = x.seg - 9;
+    const uint64_t gi = base + (x.ss & SLOT_MASK);
+    const double ps = p_struct(__ldcg(d.bob + gi), __ldcg(d.bomax + gi), P.gamma);
+    x.k0 = obits(__ddiv_rn(__dmul_rn(P.cw[10 + tau], ps), dt));
+  }
+}
+
+// The scanning CTA keeps the positions of its scored candidates in smem (reusing the
+// radix histogram area) and scores them exactly after streaming (no transcendental inside
+// the streaming loop); overflow is scored in place.
+constexpr uint32_t WCAP = NSEG * 256;
+__device__ __forceinline__ void note_cand(Ctx& c, const ScanP& P, Cand* gdst, uint32_t pos) {
+  const uint32_t w = atomicAdd(&c.s->nw, 1u);
+  if (w < WCAP) {
+    c.s->rhist[w] = pos;
+  } else {
+    Cand x = gdst[pos];
+    finalize_key(*c.d, c.base, P, x);
+    gdst[pos].k0 = x.k0;
+  }
+}
+__device__ void finalize_noted(Ctx& c, const ScanP& P, Cand* gdst) {
+  const uint32_t n = min(c.s->nw, WCAP);
+  for (uint32_t i = threadIdx.x; i < n; i += NT) {
+    const uint32_t pos = c.s->rhist[i];
+    Cand x = gdst[pos];
+    finalize_key(*c.d, c.base, P, x);
+    gdst[pos].k0 = x.k0;
+  }
 }
 
 __device__ void scan_range(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P) {
@@ -696,7 +732,11 @@ __device__ void scan_range(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P) {
           uint32_t basep = 0;
           if (lane == 0) basep = atomicAdd(&c.ctl->ncand, (unsigned)__popc(bal));
           basep = __shfl_sync(~0u, basep, 0);
-          if (take) gdst[basep + __popc(bal & ((1u << lane) - 1u))] = x;
+          if (take) {
+            const uint32_t pos = basep + __popc(bal & ((1u << lane) - 1u));
+            gdst[pos] = x;
+            if (x.seg != 0) note_cand(c, P, gdst, pos);
+          }
         }
       } else if (take) {
         c.cand[atomicAdd(&s.ncand, 1u)] = x;
@@ -705,6 +745,12 @@ __device__ void scan_range(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P) {
 #pragma unroll
     for (int u = 0; u < 4; ++u) { mt[u] = mn[u]; idv[u] = in_[u]; lt[u] = ln_[u]; }
     s0 = sn;
+  }
+  __syncthreads();
+  if (gm) {
+    finalize_noted(c, P, gdst);
+  } else {
+    for (uint32_t i = tid; i < s.ncand; i += NT) finalize_key(d, c.base, P, c.cand[i]);
   }
   // reduce the packed per-thread counts: warp shuffles, then one smem atomic per warp
 #pragma unroll
@@ -836,9 +882,8 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
         }
       }
       Cand x;
-      if (take) {                         // exact keys for the (few) candidates
+      if (take) {                         // raw record; exact scores after streaming
         const uint32_t id = iv[k];
-        const double last = l[k];
         x.ss = (uint32_t)(t0 + k) | ((q == Q_EF ? 0u : 1u) << 28);
         x.seg = seg;
         if (q == Q_EF) {
@@ -846,33 +891,29 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
           x.k1 = 0;
           x.k2 = 0;
         } else {
-          double dt = __dsub_rn(P.now, last);
-          if (dt < P.dt_eps) dt = P.dt_eps;
-          x.k1 = obits(last);
+          x.k0 = 0;
+          x.k1 = obits(l[k]);
           x.k2 = id;
-          if (q == Q_STRUCT) {
-            const uint64_t gi = c.base + t0 + k;
-            const double ps = p_struct(__ldcg(d.bob + gi), __ldcg(d.bomax + gi), P.gamma);
-            x.k0 = obits(__ddiv_rn(__dmul_rn(P.cw[10 + tau], ps), dt));
-            take = x.k0 <= P.thr[seg];
-          } else {
-            const double pv = survival(dt, P.mu[q - 1], P.sg[q - 1], P.z_cut);
-            x.k0 = obits(__ddiv_rn(__dmul_rn(P.cw[(q - 1) * 5 + tau], pv), dt));
-          }
         }
-        if (take) pk_add(cnt, seg);
+        pk_add(cnt, seg);
       }
       const uint32_t bal = __ballot_sync(~0u, take);
       if (bal) {
         uint32_t basep = 0;
         if (lane == 0) basep = atomicAdd(&c.ctl->ncand, (unsigned)__popc(bal));
         basep = __shfl_sync(~0u, basep, 0);
-        if (take) gdst[basep + __popc(bal & ((1u << lane) - 1u))] = x;
+        if (take) {
+          const uint32_t pos = basep + __popc(bal & ((1u << lane) - 1u));
+          gdst[pos] = x;
+          if (x.seg != 0) note_cand(c, P, gdst, pos);
+        }
       }
     }
     __syncthreads();                       // stage st fully consumed
     if (tid == 0 && t + BSTAGES < ntiles) issue_tile(t + BSTAGES);
   }
+  __syncthreads();
+  finalize_noted(c, P, gdst);
 #pragma unroll
   for (int w = 0; w < 4; ++w) {
     for (int o = 16; o > 0; o >>= 1) {
@@ -903,7 +944,7 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
   switch (cmd) {
     case CMD_SCAN: {
       if (tid < 16) { s.segtot[tid] = 0; s.cnt[tid] = 0; }
-      if (tid == 0) s.ncand = 0;
+      if (tid == 0) { s.ncand = 0; s.nw = 0; }
       __syncthreads();
       ScanP P;
       if (leader) {   // the leader scans with its own smem copies
