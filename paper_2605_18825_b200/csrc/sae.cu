@@ -518,7 +518,7 @@ struct Smem {
   unsigned long long kmin[16];
   uint32_t nv, nw;          // nw: this CTA's candidates awaiting finalize_key (global mode)
   uint32_t rhist[NSEG * 256];   // radix-select histograms (one 256-bin digit per segment)
-  __align__(8) uint64_t mbar[4];  // bulk-copy stage barriers (worker scan pipeline)
+  __align__(8) uint64_t mbar[8];  // bulk-copy stage barriers (worker scan pipeline)
   uint64_t wthr[16], wpfx[16], wpmask[16];   // worker copies of the leader's command parameters
   double wcw[15], wmu[2], wsg[2];
 };
@@ -689,7 +689,15 @@ __device__ void scan_range(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P) {
   uint32_t mt[4], idv[4];
   double lt[4];
   auto load = [&](uint64_t s0, uint32_t (&m)[4], uint32_t (&iv)[4], double (&l)[4]) {
-    if (vec && s0 + 3 < hi) {
+    if (vec && s0 + 3 < hi && !gm) {   // single-CTA replica: the SoA is private -> L1-cached loads
+      const uint4 m4 = *reinterpret_cast<const uint4*>(d.bmeta + c.base + s0);
+      const uint4 i4 = *reinterpret_cast<const uint4*>(d.bid + c.base + s0);
+      const double2 l0 = *reinterpret_cast<const double2*>(d.blast + c.base + s0);
+      const double2 l1 = *reinterpret_cast<const double2*>(d.blast + c.base + s0 + 2);
+      m[0] = m4.x; m[1] = m4.y; m[2] = m4.z; m[3] = m4.w;
+      iv[0] = i4.x; iv[1] = i4.y; iv[2] = i4.z; iv[3] = i4.w;
+      l[0] = l0.x; l[1] = l0.y; l[2] = l1.x; l[3] = l1.y;
+    } else if (vec && s0 + 3 < hi) {
       const uint4 m4 = __ldcg(reinterpret_cast<const uint4*>(d.bmeta + c.base + s0));
       const uint4 i4 = __ldcg(reinterpret_cast<const uint4*>(d.bid + c.base + s0));
       const double2 l0 = __ldcg(reinterpret_cast<const double2*>(d.blast + c.base + s0));
@@ -1534,13 +1542,15 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
   // ---- carry thresholds: trim segments holding far more candidates than they use
   for (uint32_t v = tid; v < m; v += NT) atomicAdd(&s.used[c.vbuf[v].seg], 1u);
   __syncthreads();
+  // small private pools (rescans are cheap) trim hard; large pools trim lazily
+  const uint32_t trim_at = 8u, trim_to = 4u;
   uint32_t shrink = 0;
   for (int g = 0; g < NSEG; ++g) {
     const uint32_t want = 3 * s.used[g] + SLACK;
-    if (s.cnt[g] > 8 * want) shrink |= 1u << g;
+    if (s.cnt[g] > trim_at * want) shrink |= 1u << g;
   }
   if (shrink && nv <= VCAP) {
-    if (tid < NSEG) s.target[tid] = 4 * (3 * s.used[tid] + SLACK);
+    if (tid < NSEG) s.target[tid] = trim_to * (3 * s.used[tid] + SLACK);
     __syncthreads();
     radix_select(c.cand, nc, true, shrink, s);
     if (tid < NSEG && ((shrink >> tid) & 1u)) st.thr[tid] = s.pfx[tid];
