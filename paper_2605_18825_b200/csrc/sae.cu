@@ -918,7 +918,10 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
       }
     }
     __syncthreads();                       // stage st fully consumed
-    if (tid == 0 && t + BSTAGES < ntiles) issue_tile(t + BSTAGES);
+    if (tid == 0 && t + BSTAGES < ntiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads -> async writes
+      issue_tile(t + BSTAGES);
+    }
   }
   __syncthreads();
   finalize_noted(c, P, gdst);
@@ -1308,6 +1311,7 @@ __device__ void learn(Ctx& c) {
   __syncthreads();
   double cw_old[4];
   for (int t = 0; t < 4; ++t) cw_old[t] = s.cw[2][t];
+  __syncthreads();
   recompute_cw(s);
   __syncthreads();
   // STRUCT-class thresholds follow a pure rescaling of alpha*w (heuristic only; the
@@ -1385,6 +1389,7 @@ __device__ void radix_select(const Cand* a, uint32_t n, bool per_seg, uint32_t a
       const uint32_t need = s.target[g] - s.below[g];
       const uint32_t excl = inc - loc;
       const uint32_t bal = __ballot_sync(~0u, excl < need && inc >= need);
+      __syncwarp();
       if (lane == __ffs(bal) - 1) {
         uint32_t run = excl;
         int bsel = 0;
@@ -1626,6 +1631,7 @@ __device__ void narrow(Ctx& c, uint32_t e, uint32_t mp) {
       const uint32_t excl = inc - loc;
       const bool mine = excl < need && inc >= need;
       const uint32_t bal = __ballot_sync(~0u, mine);
+      __syncwarp();
       const int src = __ffs(bal) - 1;
       if (lane == src) {
         uint32_t run = excl;
