@@ -167,6 +167,7 @@ typedef struct {
    * scan passes, narrowing, sort+check, apply, learn, insert+outputs, table rebuild, and for
    * multi-CTA groups: command start barrier, leader's own partition, end barrier, spare */
   uint64_t phase_ns[12];
+  uint64_t select_narrow, select_raw;   /* narrowings (candidate sets > 4096) and raw candidates */
   sae_params params;
 } sae_replica_stats;
 

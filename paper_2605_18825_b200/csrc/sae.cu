@@ -73,6 +73,7 @@ struct RState {
   uint64_t evict_by_queue[4], evict_by_type[6], mae_by_type[6];
   uint64_t learner_firings, eviction_rounds, blocks_scored, blocks_scored_struct;
   uint64_t select_passes, select_cands, select_big, select_fail_seg[10];
+  uint64_t select_narrow, select_raw;
   uint64_t tph[12];         // leader phase timers (ns): probe, scan, narrow, select, apply, learn, insert, rebuild,
                             // + issue(): start barrier, own partition, end barrier, (spare)
   uint64_t thr[16];        // per-segment candidate thresholds on k0 (heuristic; exactness never depends on them)
@@ -1314,12 +1315,17 @@ __device__ void learn(Ctx& c) {
   __syncthreads();
   recompute_cw(s);
   __syncthreads();
-  // STRUCT-class thresholds follow a pure rescaling of alpha*w (heuristic only; the
-  // exactness check in select_chunk never depends on them)
-  if (threadIdx.x < 4 && p.gamma == gamma_old && st.thr[9 + threadIdx.x] != ~0ull &&
-      s.cw[2][threadIdx.x] != cw_old[threadIdx.x] && cw_old[threadIdx.x] > 0.0) {
-    const double T = from_obits(st.thr[9 + threadIdx.x]);
-    st.thr[9 + threadIdx.x] = obits(T * (s.cw[2][threadIdx.x] / cw_old[threadIdx.x]) * (1.0 + 0x1p-40));
+  // STRUCT-class thresholds follow the parameter change (heuristic only; the exactness
+  // check in select_chunk never depends on them): P scales with alpha*w, and for a gamma
+  // decrease p(gamma')/p(gamma) lies in [gamma'/gamma, 1], so T' = T * gamma'/gamma keeps
+  // the new candidate set inside the old one (no candidate explosion after a firing).
+  if (threadIdx.x < 4 && st.thr[9 + threadIdx.x] != ~0ull && cw_old[threadIdx.x] > 0.0) {
+    double f = s.cw[2][threadIdx.x] / cw_old[threadIdx.x];
+    if (p.gamma < gamma_old) f *= p.gamma / gamma_old;
+    if (f != 1.0) {
+      const double T = from_obits(st.thr[9 + threadIdx.x]);
+      st.thr[9 + threadIdx.x] = obits(T * f);
+    }
   }
   if (threadIdx.x == 0) {
     st.learner_firings++;
@@ -1439,6 +1445,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
       __syncthreads();
       const uint32_t e0 = min(m, s.segtot[0]);
       const bool narrowed = s.ncand > (uint32_t)CAND_MAX;
+      if (tid == 0) { st.select_raw += s.ncand; st.select_narrow += narrowed ? 1 : 0; }
       if (narrowed) narrow(c, e0, m - e0);
       if (tid == 0 && narrowed) { const uint64_t t1 = gtimer(); st.tph[2] += t1 - t0; t0 = t1; }
       const Cand* src = narrowed ? d.gsel + (uint64_t)c.r * CAND_MAX : d.gcand + c.base;
@@ -1511,7 +1518,12 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
   __syncthreads();
   for (uint32_t i0 = 0; i0 < nc; i0 += NT) {
     const uint32_t i = i0 + tid;
-    if (i < nc) atomicMin(&s.kmin[c.cand[i].seg], (unsigned long long)seg_key(c.cand[i]));
+    if (i < nc) {
+      const Cand& x = c.cand[i];
+      // EF grows within its threshold's num_tokens band: min over that band only
+      if (x.seg != 0 || (x.k0 >> 32) == (st.thr[0] >> 32))
+        atomicMin(&s.kmin[x.seg], (unsigned long long)seg_key(x));
+    }
     const bool take = i < nc && c.cand[i].k0 <= Kth;
     const uint32_t bal = __ballot_sync(~0u, take);
     uint32_t basep = 0;
@@ -1571,9 +1583,11 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
     if (T != ~0ull && s.segtot[g] > s.cnt[g] && left < 2 * s.used[g] + SLACK) {
       const uint64_t km = s.kmin[g] == ~0ull ? T : (uint64_t)s.kmin[g];
       uint64_t Tn;
-      if (g == 0) {
-        const uint64_t dlt = max(T - min(km, T), (uint64_t)4096);
-        Tn = T + dlt < T ? ~0ull : T + dlt;
+      if (g == 0) {                 // id part only, saturating inside the ntok band
+        const uint64_t band = T & ~0xFFFFFFFFull, idT = T & 0xFFFFFFFFull;
+        const uint64_t idm = (km & ~0xFFFFFFFFull) == band ? (km & 0xFFFFFFFFull) : idT;
+        const uint64_t dlt = max(idT - min(idm, idT), (uint64_t)4096);
+        Tn = band | min(idT + dlt, (uint64_t)0xFFFFFFFFull);
       } else if (g <= 8) {
         const double Tl = from_obits(T), kl = from_obits(km);
         Tn = obits(Tl + fmax(Tl - kl, 1.0));
@@ -2564,6 +2578,8 @@ sae_status sae_stats(sae_ctx* ctx, uint32_t replica, sae_replica_stats* out, sae
   out->select_big = rs.select_big;
   for (int g = 0; g < 10; ++g) out->select_fail_seg[g] = rs.select_fail_seg[g];
   for (int g = 0; g < 12; ++g) out->phase_ns[g] = rs.tph[g];
+  out->select_narrow = rs.select_narrow;
+  out->select_raw = rs.select_raw;
   {
     unsigned long long w = 0;
     CK(cudaMemcpy(&w, &ctx->d.ctl[replica].wscan_ns, 8, cudaMemcpyDeviceToHost));

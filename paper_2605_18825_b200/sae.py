@@ -79,6 +79,7 @@ class sae_replica_stats(C.Structure):
                 ("select_passes", C.c_uint64), ("select_cands", C.c_uint64),
                 ("select_big", C.c_uint64), ("select_fail_seg", C.c_uint64 * 10),
                 ("phase_ns", C.c_uint64 * 12),
+                ("select_narrow", C.c_uint64), ("select_raw", C.c_uint64),
                 ("params", sae_params)]
 
 

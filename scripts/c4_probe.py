@@ -35,5 +35,6 @@ for k in range(n_steps):
         st.select_big - s0.select_big, [a - b for a, b in zip(st.select_fail_seg, s0.select_fail_seg)],
         st.learner_firings - s0.learner_firings), flush=True)
     s0 = st
+print("narrows", st.select_narrow, "raw cands/pass", st.select_raw / max(1, st.select_passes))
 print("resident by queue", list(st.resident_by_queue), "hit rate", st.hit_tokens / st.prompt_tokens)
 print("phase ms", [round(x / 1e6, 1) for x in st.phase_ns])
