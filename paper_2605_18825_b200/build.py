@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libsae.so")
 SOURCES = ["sae.cu"]
-DEPS = ["sae.cu", "dmath.cuh", "xxh64.cuh"]
+DEPS = ["sae.cu", "replay_impl.cuh", "dmath.cuh", "xxh64.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

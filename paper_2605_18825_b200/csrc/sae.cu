@@ -35,9 +35,6 @@ namespace sae {
 
 constexpr uint64_t KEY_EMPTY = ~0ull;
 constexpr uint64_t KEY_TOMB = ~0ull - 1;
-constexpr int NT = 512;            // threads per replay CTA
-constexpr int NW = NT / 32;
-constexpr int CAND_MAX = 4096;     // candidate buffer (smem) per CTA
 constexpr uint32_t SLACK = 32;     // extra candidates kept per segment across chunks (min)
 constexpr int NSEG = 13;           // EF, 8 multi-turn classes (queue, tau), 4 STRUCT classes (tau)
 constexpr uint32_t MSUB = 96;      // victims selected per scan pass (keys are frozen within a chunk)
@@ -280,130 +277,6 @@ __device__ uint32_t tbl_insert(uint64_t* keys, uint32_t* vals, uint32_t mask, ui
 }
 
 // ---------------------------------------------------------------------------
-// Block-wide helpers (NT threads)
-// ---------------------------------------------------------------------------
-// exclusive scan of up to 3 flags per thread; returns ranks; totals in tot[3]
-__device__ __forceinline__ void block_scan3(uint32_t a, uint32_t b, uint32_t c, uint32_t& ra,
-                                            uint32_t& rb, uint32_t& rc, uint32_t* tot,
-                                            uint32_t* wsum /* [3*NW] smem */) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  uint32_t ba = __ballot_sync(~0u, a), bb = __ballot_sync(~0u, b), bc = __ballot_sync(~0u, c);
-  uint32_t lm = (1u << lane) - 1u;
-  ra = __popc(ba & lm); rb = __popc(bb & lm); rc = __popc(bc & lm);
-  if (lane == 0) { wsum[w] = __popc(ba); wsum[NW + w] = __popc(bb); wsum[2 * NW + w] = __popc(bc); }
-  __syncthreads();
-  uint32_t oa = 0, ob = 0, oc = 0, ta = 0, tb = 0, tc = 0;
-  for (int i = 0; i < NW; ++i) {
-    uint32_t x = wsum[i], y = wsum[NW + i], z = wsum[2 * NW + i];
-    if (i < w) { oa += x; ob += y; oc += z; }
-    ta += x; tb += y; tc += z;
-  }
-  ra += oa; rb += ob; rc += oc;
-  tot[0] = ta; tot[1] = tb; tot[2] = tc;
-  __syncthreads();
-}
-
-__device__ __forceinline__ bool cand_less(const Cand& a, const Cand& b) {
-  uint32_t sa = a.ss >> 28, sb = b.ss >> 28;
-  if (sa != sb) return sa < sb;
-  if (a.k0 != b.k0) return a.k0 < b.k0;
-  if (a.k1 != b.k1) return a.k1 < b.k1;
-  return a.k2 < b.k2;
-}
-
-// bitonic sort of cand[0..N), N a power of two, ascending by (seg, k0, k1, k2)
-__device__ void block_sort(Cand* cand, int N) {
-  for (int k = 2; k <= N; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < N; i += NT) {
-        int ixj = i ^ j;
-        if (ixj > i) {
-          Cand x = cand[i], y = cand[ixj];
-          bool up = (i & k) == 0;
-          if (cand_less(y, x) == up) { cand[i] = y; cand[ixj] = x; }
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
-
-__device__ __forceinline__ Cand shfl_cand(const Cand& x, int j) {
-  Cand y;
-  y.k0 = __shfl_xor_sync(~0u, x.k0, j);
-  y.k1 = __shfl_xor_sync(~0u, x.k1, j);
-  y.k2 = __shfl_xor_sync(~0u, x.k2, j);
-  y.ss = __shfl_xor_sync(~0u, x.ss, j);
-  y.seg = __shfl_xor_sync(~0u, x.seg, j);
-  return y;
-}
-
-// Bitonic sort of a[0..N) (N a power of two, 32 <= N <= E*NT) with E elements per
-// thread held in registers: element e of thread t is index e*NT + t.  Strides >= NT
-// stay inside a thread, strides < 32 use warp shuffles, the rest go through smem.
-template <int E>
-__device__ void sort_reg(Cand* a, int N) {
-  const int t = threadIdx.x;
-  Cand x[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int i = e * NT + t;
-    if (i < N) {
-      x[e] = a[i];
-    } else {
-      x[e].k0 = ~0ull; x[e].k1 = ~0ull; x[e].k2 = ~0u; x[e].ss = ~0u; x[e].seg = 15;
-    }
-  }
-  for (int k = 2; k <= N; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      if (j >= NT) {
-        const int pe = j / NT;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          if ((e & pe) == 0 && (e | pe) < E) {
-            const int i = e * NT + t;
-            const bool up = (i & k) == 0;
-            Cand& lo = x[e];
-            Cand& hi = x[e | pe];
-            if (cand_less(hi, lo) == up) { Cand tmp = lo; lo = hi; hi = tmp; }
-          }
-        }
-        continue;
-      }
-      Cand y[E];
-      if (j >= 32) {
-#pragma unroll
-        for (int e = 0; e < E; ++e) if (e * NT + t < N) a[e * NT + t] = x[e];
-        __syncthreads();
-#pragma unroll
-        for (int e = 0; e < E; ++e) y[e] = (e * NT + t < N) ? a[(e * NT + t) ^ j] : x[e];
-        __syncthreads();
-      } else {
-#pragma unroll
-        for (int e = 0; e < E; ++e) y[e] = shfl_cand(x[e], j);
-      }
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int i = e * NT + t;
-        const bool up = (i & k) == 0, lower = (i & j) == 0;
-        const bool take_y = (lower == up) ? cand_less(y[e], x[e]) : cand_less(x[e], y[e]);
-        if (take_y && i < N) x[e] = y[e];
-      }
-    }
-  }
-#pragma unroll
-  for (int e = 0; e < E; ++e) if (e * NT + t < N) a[e * NT + t] = x[e];
-  __syncthreads();
-}
-
-__device__ void sort_cands(Cand* a, int N) {
-  if (N <= NT) sort_reg<1>(a, N);
-  else if (N <= 2 * NT) sort_reg<2>(a, N);
-  else if (N <= 4 * NT) sort_reg<4>(a, N);
-  else block_sort(a, N);
-}
-
-// ---------------------------------------------------------------------------
 // Batch preparation kernels
 // ---------------------------------------------------------------------------
 __global__ void k_nblocks(BatchDev b, uint32_t B, uint64_t* cnt) {
@@ -501,1562 +374,18 @@ __global__ void __launch_bounds__(128) k_hash(BatchDev b, Dev d) {
   }
 }
 
-// ---------------------------------------------------------------------------
-// Replay CTA: shared state
-// ---------------------------------------------------------------------------
-struct Smem {
-  RState st;
-  double cw[3][5];         // alpha_q * w_tau per scored queue (CHAT, AGENT, STRUCT)
-  uint32_t wsum[16 * NW];
-  uint32_t tot[3];
-  uint32_t cnt[16], start[16], segtot[16], used[16];
-  uint32_t fail, ncand;
-  int32_t h;
-  uint32_t npin, matched;
-  uint64_t k, admit;
-  uint64_t pfx[16], pmask[16];
-  uint32_t below[16], target[16];
-  unsigned long long kmin[16];
-  uint32_t nv, nw;          // nw: this CTA's candidates awaiting finalize_key (global mode)
-  uint32_t rhist[NSEG * 256];   // radix-select histograms (one 256-bin digit per segment)
-  __align__(8) uint64_t mbar[8];  // bulk-copy stage barriers (worker scan pipeline)
-  uint64_t wthr[16], wpfx[16], wpmask[16];   // worker copies of the leader's command parameters
-  double wcw[15], wmu[2], wsg[2];
-};
-
-struct Ctx {               // per-CTA view of one replica (group)
-  const Dev* d;
-  Smem* s;
-  Cand* cand;
-  Cand* vbuf;              // [VCAP] victims staging
-  GroupCtl* ctl;
-  uint32_t r, rank, GP;
-  uint64_t base;           // r * C
-};
-
-__device__ void recompute_cw(Smem& s) {
-  if (threadIdx.x < 15) {
-    int q = threadIdx.x / 5, t = threadIdx.x % 5;
-    s.cw[q][t] = __dmul_rn(s.st.par.alpha[q], s.st.par.w[t]);
-  }
-}
-
-__device__ __forceinline__ uint32_t seg_of(uint32_t q, uint32_t tau) {
-  return q == Q_EF ? 0u : (q == Q_STRUCT ? 9u + (tau & 3u) : 1u + (q - 1u) * 4u + (tau & 3u));
-}
-// the key a segment's threshold applies to: (last) for multi-turn classes, k0 otherwise
-__device__ __forceinline__ uint64_t seg_key(const Cand& x) {
-  return (x.seg >= 1 && x.seg <= 8) ? x.k1 : x.k0;
-}
-__device__ __forceinline__ void part_range(uint64_t n, uint32_t rank, uint32_t GP, uint64_t& lo,
-                                           uint64_t& hi) {
-  lo = n * rank / GP;
-  hi = n * (rank + 1) / GP;
-}
-
-// ---------------------------------------------------------------------------
-// Group barrier over the GP CTAs of one replica (co-resident by cooperative launch).
-// ---------------------------------------------------------------------------
-__device__ void group_bar(Ctx& c) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    GroupCtl* g = c.ctl;
-    volatile unsigned* genp = &g->bar_gen;
-    const unsigned gen = *genp;
-    __threadfence();
-    if (atomicAdd(&g->bar_count, 1u) == c.GP - 1) {
-      atomicExch(&g->bar_count, 0u);
-      __threadfence();
-      atomicAdd(&g->bar_gen, 1u);
-    } else {
-      while (*genp == gen) __nanosleep(64);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-// Parameters of a scan, from the leader's smem (leader) or the control block (workers).
-struct ScanP {
-  double now, dt_eps, z_cut, gamma;
-  uint32_t stamp;
-  const unsigned long long* thr;
-  const double* cw;        // [3][5]
-  const double* mu;
-  const double* sg;
-};
-
-// One pass over slots [lo, hi) of the replica's SoA: segment + key of every resident,
-// unpinned block (a4); those at or below the segment's threshold become candidates.
-// Each thread handles 4 consecutive slots per step with 128-bit cache-global loads
-// (meta, id, last; p_struct only for STRUCT blocks); per-segment counts accumulate in
-// registers (16-bit fields) and are reduced once per pass.  Counts go to smem
-// (segtot, cnt); candidates to smem (cand_smem) or the group's global buffer.
-__device__ __forceinline__ void pk_add(uint64_t (&pk)[4], uint32_t seg) {
-  const uint64_t inc = 1ull << ((seg & 3u) * 16u);
-  switch (seg >> 2) {
-    case 0: pk[0] += inc; break;
-    case 1: pk[1] += inc; break;
-    case 2: pk[2] += inc; break;
-    default: pk[3] += inc; break;
-  }
-}
-
-// Candidacy of one resident, unpinned block (a4).  Exact for EF (key (ntok, id)) and the
-// multi-turn classes (key: last); conservative for STRUCT (a lower bound of P against the
-// threshold).  The exact Eq.(1)-(3) scores of the (few) candidates are computed afterwards
-// by finalize_keys, outside the streaming loop.
-__device__ __forceinline__ bool score_one(const Dev& d, const ScanP& P, uint32_t meta, uint32_t id,
-                                          double last, uint64_t gi, uint32_t sl, Cand& x,
-                                          uint32_t& seg) {
-  const uint32_t q = meta_q(meta), tau = meta_tau(meta);
-  seg = seg_of(q, tau);
-  bool take;
-  x.k2 = id;
-  x.k1 = obits(last);
-  if (q == Q_EF) {                      // Stage 1 key (num_tokens, id)
-    x.k0 = ((uint64_t)meta_ntok(meta) << 32) | id;
-    x.k1 = 0;
-    x.k2 = 0;
-    take = x.k0 <= P.thr[seg];
-  } else if (q == Q_STRUCT) {           // prefilter: lower bound of Eq.(2)+(3) vs threshold
-    double dt = __dsub_rn(P.now, last);
-    if (dt < P.dt_eps) dt = P.dt_eps;
-    const double T = P.thr[seg] == ~0ull ? __longlong_as_double(0x7ff0000000000000ll) : from_obits(P.thr[seg]);
-    take = __dmul_rn(P.cw[10 + tau], p_struct_lo(__ldcg(d.blr + gi), (float)P.gamma)) <=
-           __dmul_rn(__dmul_rn(T, dt), 1.0 + 0x1p-40);
-    x.k0 = 0;
-  } else {                              // multi-turn class (queue, tau): key last
-    take = x.k1 <= P.thr[seg];
-    x.k0 = 0;
-  }
-  x.ss = sl | ((q == Q_EF ? 0u : 1u) << 28);
-  x.seg = seg;
-  return take;
-}
-
-// Exact score of a scored candidate: Eq.(1) survival (multi-turn) or Eq.(2) (STRUCT),
-// then Eq.(3) P = ((alpha_q * w_tau) * p) / dt, fixed op order (SURVEY c.4).
-__device__ __forceinline__ void finalize_key(const Dev& d, uint64_t base, const ScanP& P, Cand& x) {
-  if (x.seg == 0 || x.seg >= 16) return;
-  const double last = from_obits(x.k1);
-  double dt = __dsub_rn(P.now, last);
-  if (dt < P.dt_eps) dt = P.dt_eps;
-  if (x.seg <= 8) {
-    const uint32_t q = 1 + (x.seg - 1) / 4, tau = (x.seg - 1) & 3;
-    const double p = survival(dt, P.mu[q - 1], P.sg[q - 1], P.z_cut);
-    x.k0 = obits(__ddiv_rn(__dmul_rn(P.cw[(q - 1) * 5 + tau], p), dt));
-  } else {
-    const uint32_t tau = x.seg - 9;
-    const uint64_t gi = base + (x.ss & SLOT_MASK);
-    const double ps = p_struct(__ldcg(d.bob + gi), __ldcg(d.bomax + gi), P.gamma);
-    x.k0 = obits(__ddiv_rn(__dmul_rn(P.cw[10 + tau], ps), dt));
-  }
-}
-
-// The scanning CTA keeps the positions of its scored candidates in smem (reusing the
-// radix histogram area) and scores them exactly after streaming (no transcendental inside
-// the streaming loop); overflow is scored in place.
-constexpr uint32_t WCAP = NSEG * 256;
-__device__ __forceinline__ void note_cand(Ctx& c, const ScanP& P, Cand* gdst, uint32_t pos) {
-  const uint32_t w = atomicAdd(&c.s->nw, 1u);
-  if (w < WCAP) {
-    c.s->rhist[w] = pos;
-  } else {
-    Cand x = gdst[pos];
-    finalize_key(*c.d, c.base, P, x);
-    gdst[pos].k0 = x.k0;
-  }
-}
-__device__ void finalize_noted(Ctx& c, const ScanP& P, Cand* gdst) {
-  const uint32_t n = min(c.s->nw, WCAP);
-  for (uint32_t i = threadIdx.x; i < n; i += NT) {
-    const uint32_t pos = c.s->rhist[i];
-    Cand x = gdst[pos];
-    finalize_key(*c.d, c.base, P, x);
-    gdst[pos].k0 = x.k0;
-  }
-}
-
-__device__ void scan_range(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P) {
-  const Dev& d = *c.d;
-  Smem& s = *c.s;
-  const int tid = threadIdx.x, lane = tid & 31;
-  const bool gm = !d.cand_smem;
-  Cand* gdst = gm ? d.gcand + c.base : nullptr;
-  uint64_t tot[4] = {0, 0, 0, 0}, cnt[4] = {0, 0, 0, 0};
-  const bool vec = ((c.base + lo) & 3u) == 0;
-  // software pipeline: the next step's 4 slots are loaded before this step is scored
-  uint32_t mt[4], idv[4];
-  double lt[4];
-  auto load = [&](uint64_t s0, uint32_t (&m)[4], uint32_t (&iv)[4], double (&l)[4]) {
-    if (vec && s0 + 3 < hi && !gm) {   // single-CTA replica: the SoA is private -> L1-cached loads
-      const uint4 m4 = *reinterpret_cast<const uint4*>(d.bmeta + c.base + s0);
-      const uint4 i4 = *reinterpret_cast<const uint4*>(d.bid + c.base + s0);
-      const double2 l0 = *reinterpret_cast<const double2*>(d.blast + c.base + s0);
-      const double2 l1 = *reinterpret_cast<const double2*>(d.blast + c.base + s0 + 2);
-      m[0] = m4.x; m[1] = m4.y; m[2] = m4.z; m[3] = m4.w;
-      iv[0] = i4.x; iv[1] = i4.y; iv[2] = i4.z; iv[3] = i4.w;
-      l[0] = l0.x; l[1] = l0.y; l[2] = l1.x; l[3] = l1.y;
-    } else if (vec && s0 + 3 < hi) {
-      const uint4 m4 = __ldcg(reinterpret_cast<const uint4*>(d.bmeta + c.base + s0));
-      const uint4 i4 = __ldcg(reinterpret_cast<const uint4*>(d.bid + c.base + s0));
-      const double2 l0 = __ldcg(reinterpret_cast<const double2*>(d.blast + c.base + s0));
-      const double2 l1 = __ldcg(reinterpret_cast<const double2*>(d.blast + c.base + s0 + 2));
-      m[0] = m4.x; m[1] = m4.y; m[2] = m4.z; m[3] = m4.w;
-      iv[0] = i4.x; iv[1] = i4.y; iv[2] = i4.z; iv[3] = i4.w;
-      l[0] = l0.x; l[1] = l0.y; l[2] = l1.x; l[3] = l1.y;
-    } else {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const bool ok = s0 + u < hi;
-        m[u] = ok ? __ldcg(d.bmeta + c.base + s0 + u) : 0u;
-        iv[u] = ok ? __ldcg(d.bid + c.base + s0 + u) : 0u;
-        l[u] = ok ? __ldcg(d.blast + c.base + s0 + u) : 0.0;
-      }
-    }
-  };
-  uint64_t s0 = lo + 4ull * tid;
-  if (s0 < hi) load(s0, mt, idv, lt);
-  else { mt[0] = mt[1] = mt[2] = mt[3] = 0; }
-  for (uint64_t i0 = lo; i0 < hi; i0 += 4 * NT) {
-    const uint64_t sn = s0 + 4ull * NT;
-    uint32_t mn[4] = {0, 0, 0, 0}, in_[4] = {0, 0, 0, 0};
-    double ln_[4] = {0.0, 0.0, 0.0, 0.0};
-    if (sn < hi) load(sn, mn, in_, ln_);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      bool take = false;
-      Cand x;
-      const uint32_t meta = s0 < hi ? mt[u] : 0u;
-      if ((meta & (M_LIVE | M_PIN)) == M_LIVE) {
-        uint32_t seg;
-        take = score_one(d, P, meta, idv[u], lt[u], c.base + s0 + u, (uint32_t)(s0 + u), x, seg);
-        pk_add(tot, seg);
-        if (take) pk_add(cnt, seg);
-      }
-      if (gm) {
-        const uint32_t bal = __ballot_sync(~0u, take);
-        if (bal) {
-          uint32_t basep = 0;
-          if (lane == 0) basep = atomicAdd(&c.ctl->ncand, (unsigned)__popc(bal));
-          basep = __shfl_sync(~0u, basep, 0);
-          if (take) {
-            const uint32_t pos = basep + __popc(bal & ((1u << lane) - 1u));
-            gdst[pos] = x;
-            if (x.seg != 0) note_cand(c, P, gdst, pos);
-          }
-        }
-      } else if (take) {
-        c.cand[atomicAdd(&s.ncand, 1u)] = x;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) { mt[u] = mn[u]; idv[u] = in_[u]; lt[u] = ln_[u]; }
-    s0 = sn;
-  }
-  __syncthreads();
-  if (gm) {
-    finalize_noted(c, P, gdst);
-  } else {
-    for (uint32_t i = tid; i < s.ncand; i += NT) finalize_key(d, c.base, P, c.cand[i]);
-  }
-  // reduce the packed per-thread counts: warp shuffles, then one smem atomic per warp
-#pragma unroll
-  for (int w = 0; w < 4; ++w) {
-    for (int o = 16; o > 0; o >>= 1) {
-      tot[w] += __shfl_xor_sync(~0u, tot[w], o);
-      cnt[w] += __shfl_xor_sync(~0u, cnt[w], o);
-    }
-  }
-  if (lane < NSEG) {
-    const int w = lane >> 2, f = (lane & 3) * 16;
-    uint64_t tv = w == 0 ? tot[0] : w == 1 ? tot[1] : w == 2 ? tot[2] : tot[3];
-    uint64_t cv = w == 0 ? cnt[0] : w == 1 ? cnt[1] : w == 2 ? cnt[2] : cnt[3];
-    const uint32_t t16 = (uint32_t)((tv >> f) & 0xFFFFu), c16 = (uint32_t)((cv >> f) & 0xFFFFu);
-    if (t16) atomicAdd(&s.segtot[lane], t16);
-    if (c16) atomicAdd(&s.cnt[lane], c16);
-  }
-}
-
-// ---- bulk asynchronous copies (cp.async.bulk, completion on an mbarrier) -------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// Worker scan over [lo, hi) (lo a multiple of 4, replica base 16-byte aligned): the SoA
-// columns (meta u32, id u32, last f64, p_struct f64) are streamed tile by tile into
-// shared memory by bulk asynchronous copies, BSTAGES tiles in flight, and scored from
-// shared memory.  Same outputs as scan_range.
-constexpr int BTILE = 1024, BSTAGES = 4;
-constexpr uint32_t BTILE_BYTES = BTILE * (4 + 4 + 8 + 4);
-__device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P) {
-  const Dev& d = *c.d;
-  Smem& s = *c.s;
-  const int tid = threadIdx.x, lane = tid & 31;
-  Cand* gdst = d.gcand + c.base;
-  unsigned char* buf = reinterpret_cast<unsigned char*>(c.cand);
-  uint64_t tot[4] = {0, 0, 0, 0}, cnt[4] = {0, 0, 0, 0};
-  const uint64_t ntiles = (hi - lo + BTILE - 1) / BTILE;
-  auto stage_ptrs = [&](int st, uint32_t*& m, uint32_t*& iv, double*& l, float*& lr) {
-    unsigned char* b = buf + (size_t)st * BTILE_BYTES;
-    m = reinterpret_cast<uint32_t*>(b);
-    iv = reinterpret_cast<uint32_t*>(b + BTILE * 4);
-    l = reinterpret_cast<double*>(b + BTILE * 8);
-    lr = reinterpret_cast<float*>(b + BTILE * 16);
-  };
-  auto issue_tile = [&](uint64_t t) {
-    const int st = (int)(t % BSTAGES);
-    const uint64_t t0 = lo + t * BTILE;
-    const uint32_t n = (uint32_t)min((uint64_t)BTILE, hi - t0);
-    const uint32_t n4 = (n + 3) & ~3u;                 // 16-byte multiple (SoA is padded)
-    uint32_t *m, *iv;
-    double* l;
-    float* lrs;
-    stage_ptrs(st, m, iv, l, lrs);
-    mbar_expect_tx(&s.mbar[st], n4 * 20u);
-    bulk_g2s(m, d.bmeta + c.base + t0, n4 * 4u, &s.mbar[st]);
-    bulk_g2s(iv, d.bid + c.base + t0, n4 * 4u, &s.mbar[st]);
-    bulk_g2s(l, d.blast + c.base + t0, n4 * 8u, &s.mbar[st]);
-    bulk_g2s(lrs, d.blr + c.base + t0, n4 * 4u, &s.mbar[st]);
-  };
-  if (tid == 0) {
-    for (int st = 0; st < BSTAGES; ++st) mbar_init(&s.mbar[st], 1);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    for (uint64_t t = 0; t < ntiles && t < (uint64_t)BSTAGES; ++t) issue_tile(t);
-  }
-  __syncthreads();
-  // thresholds as doubles (multi-turn: last; STRUCT: P) for the division-free prefilter
-  double* thrD = reinterpret_cast<double*>(&s.wpfx[0]);   // 16 doubles of scratch
-  if (tid < NSEG) {
-    const uint64_t T = P.thr[tid];
-    thrD[tid] = (T == ~0ull || tid == 0) ? __longlong_as_double(0x7ff0000000000000ll) : from_obits(T);
-  }
-  __syncthreads();
-  const double inflate = 1.0 + 0x1p-40;
-  const float gamf = (float)P.gamma;
-  for (uint64_t t = 0; t < ntiles; ++t) {
-    const int st = (int)(t % BSTAGES);
-    mbar_wait(&s.mbar[st], (uint32_t)((t / BSTAGES) & 1));
-    uint32_t *m, *iv;
-    double* l;
-    float* lrs;
-    stage_ptrs(st, m, iv, l, lrs);
-    const uint64_t t0 = lo + t * BTILE;
-    const uint32_t n = (uint32_t)min((uint64_t)BTILE, hi - t0);
-#pragma unroll
-    for (int u = 0; u < BTILE / NT; ++u) {
-      const uint32_t k = (uint32_t)(u * NT + tid);
-      bool take = false;
-      const uint32_t meta = k < n ? m[k] : 0u;
-      uint32_t q = 0, tau = 0, seg = 0;
-      if ((meta & (M_LIVE | M_PIN)) == M_LIVE) {
-        q = meta_q(meta);
-        tau = meta_tau(meta);
-        seg = seg_of(q, tau);
-        pk_add(tot, seg);
-        if (q == Q_EF) {
-          take = ((((uint64_t)meta_ntok(meta)) << 32) | iv[k]) <= P.thr[0];
-        } else if (q == Q_STRUCT) {
-          // prefilter (a superset of P <= T) with a lower bound of p; exact P below
-          double dt = __dsub_rn(P.now, l[k]);
-          if (dt < P.dt_eps) dt = P.dt_eps;
-          take = __dmul_rn(P.cw[10 + tau], p_struct_lo(lrs[k], gamf)) <=
-                 __dmul_rn(__dmul_rn(thrD[seg], dt), inflate);
-        } else {
-          take = l[k] <= thrD[seg];
-        }
-      }
-      Cand x;
-      if (take) {                         // raw record; exact scores after streaming
-        const uint32_t id = iv[k];
-        x.ss = (uint32_t)(t0 + k) | ((q == Q_EF ? 0u : 1u) << 28);
-        x.seg = seg;
-        if (q == Q_EF) {
-          x.k0 = ((uint64_t)meta_ntok(meta) << 32) | id;
-          x.k1 = 0;
-          x.k2 = 0;
-        } else {
-          x.k0 = 0;
-          x.k1 = obits(l[k]);
-          x.k2 = id;
-        }
-        pk_add(cnt, seg);
-      }
-      const uint32_t bal = __ballot_sync(~0u, take);
-      if (bal) {
-        uint32_t basep = 0;
-        if (lane == 0) basep = atomicAdd(&c.ctl->ncand, (unsigned)__popc(bal));
-        basep = __shfl_sync(~0u, basep, 0);
-        if (take) {
-          const uint32_t pos = basep + __popc(bal & ((1u << lane) - 1u));
-          gdst[pos] = x;
-          if (x.seg != 0) note_cand(c, P, gdst, pos);
-        }
-      }
-    }
-    __syncthreads();                       // stage st fully consumed
-    if (tid == 0 && t + BSTAGES < ntiles) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads -> async writes
-      issue_tile(t + BSTAGES);
-    }
-  }
-  __syncthreads();
-  finalize_noted(c, P, gdst);
-#pragma unroll
-  for (int w = 0; w < 4; ++w) {
-    for (int o = 16; o > 0; o >>= 1) {
-      tot[w] += __shfl_xor_sync(~0u, tot[w], o);
-      cnt[w] += __shfl_xor_sync(~0u, cnt[w], o);
-    }
-  }
-  if (lane < NSEG) {
-    const int w = lane >> 2, f = (lane & 3) * 16;
-    uint64_t tv = w == 0 ? tot[0] : w == 1 ? tot[1] : w == 2 ? tot[2] : tot[3];
-    uint64_t cv = w == 0 ? cnt[0] : w == 1 ? cnt[1] : w == 2 ? cnt[2] : cnt[3];
-    const uint32_t t16 = (uint32_t)((tv >> f) & 0xFFFFu), c16 = (uint32_t)((cv >> f) & 0xFFFFu);
-    if (t16) atomicAdd(&s.segtot[lane], t16);
-    if (c16) atomicAdd(&s.cnt[lane], c16);
-  }
-}
-
-// stride-halving tree sum over y[0..P) in smem (SURVEY c.3 TREE)
-__device__ double tree_sum(double* y, int P);
-
-// Execute this CTA's share of a group command (all CTAs of the group, or the only CTA).
-__device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
-  const Dev& d = *c.d;
-  Smem& s = *c.s;
-  GroupCtl* g = c.ctl;
-  const int tid = threadIdx.x;
-  uint64_t lo, hi;
-  switch (cmd) {
-    case CMD_SCAN: {
-      if (tid < 16) { s.segtot[tid] = 0; s.cnt[tid] = 0; }
-      if (tid == 0) { s.ncand = 0; s.nw = 0; }
-      __syncthreads();
-      ScanP P;
-      if (leader) {   // the leader scans with its own smem copies
-        P.now = s.st.now;
-        P.thr = (const unsigned long long*)s.st.thr; P.cw = &s.cw[0][0];
-        P.mu = s.st.par.mu; P.sg = s.st.par.sigma;
-      } else {        // published by the leader before the command: stage into smem
-        if (tid < 16) s.wthr[tid] = __ldcg(&g->thr[tid]);
-        if (tid < 15) s.wcw[tid] = __ldcg(&g->cw[0][0] + tid);
-        if (tid < 2) { s.wmu[tid] = __ldcg(&g->mu[tid]); s.wsg[tid] = __ldcg(&g->sigma[tid]); }
-        __syncthreads();
-        P.now = __ldcg(&g->now);
-        P.thr = (const unsigned long long*)s.wthr; P.cw = s.wcw; P.mu = s.wmu; P.sg = s.wsg;
-      }
-      P.stamp = __ldcg(&g->stamp);
-      P.gamma = leader ? s.st.par.gamma : __ldcg(&g->gamma);
-      P.dt_eps = d.dt_eps;
-      P.z_cut = d.z_cut;
-      if (c.GP > 1) {
-        // the leader's smem holds the candidates: workers 1..GP-1 split the pool in
-        // 4-slot-aligned slices and stream it through shared memory
-        if (!leader) {
-          const uint64_t nw = c.GP - 1, w = c.rank - 1;
-          lo = ((uint64_t)d.C * w / nw) & ~3ull;
-          hi = w + 1 == nw ? d.C : (((uint64_t)d.C * (w + 1) / nw) & ~3ull);
-          const uint64_t tw0 = gtimer();
-          if (d.bulk_ok) scan_range_bulk(c, lo, hi, P);
-          else scan_range(c, lo, hi, P);
-          if (c.rank == 1 && tid == 0) g->wscan_ns += gtimer() - tw0;
-        }
-      } else {
-        part_range(d.C, c.rank, c.GP, lo, hi);
-        scan_range(c, lo, hi, P);
-      }
-      __syncthreads();
-      if (!d.cand_smem && tid < NSEG) {
-        if (s.segtot[tid]) atomicAdd(&g->segtot[tid], s.segtot[tid]);
-        if (s.cnt[tid]) atomicAdd(&g->cnt[tid], s.cnt[tid]);
-      }
-      break;
-    }
-    case CMD_HIST: {   // radix histograms of the active segments' keys (global candidates)
-      unsigned* h = reinterpret_cast<unsigned*>(c.cand);
-      for (int i = tid; i < NSEG * 256; i += NT) h[i] = 0;
-      __syncthreads();
-      if (tid < 16) { s.wpfx[tid] = __ldcg(&g->pfx[tid]); s.wpmask[tid] = __ldcg(&g->pmask[tid]); }
-      __syncthreads();
-      const unsigned shift = __ldcg(&g->shift), active = __ldcg(&g->active);
-      part_range(__ldcg(&g->ncand), c.rank, c.GP, lo, hi);
-      const Cand* src = d.gcand + c.base;
-      for (uint64_t i = lo + tid; i < hi; i += NT) {
-        const uint32_t seg = __ldcg(&src[i].seg);
-        if (!((active >> seg) & 1u)) continue;
-        const uint64_t key = seg >= 1 && seg <= 8 ? __ldcg(&src[i].k1) : __ldcg(&src[i].k0);
-        if ((key & s.wpmask[seg]) != s.wpfx[seg]) continue;
-        atomicAdd(&h[seg * 256 + ((key >> shift) & 255u)], 1u);
-      }
-      __syncthreads();
-      for (int i = tid; i < NSEG * 256; i += NT)
-        if (h[i]) atomicAdd(&g->hist[i], h[i]);
-      __syncthreads();
-      break;
-    }
-    case CMD_COMPACT: {  // keep candidates at or below the (new) thresholds
-      if (tid < 16) s.wthr[tid] = __ldcg(&g->thr[tid]);
-      __syncthreads();
-      part_range(__ldcg(&g->ncand), c.rank, c.GP, lo, hi);
-      const Cand* src = d.gcand + c.base;
-      Cand* dst = d.gsel + (uint64_t)c.r * CAND_MAX;
-      const int lane = tid & 31;
-      for (uint64_t i0 = lo; i0 < hi; i0 += NT) {
-        const uint64_t i = i0 + tid;
-        bool take = false;
-        Cand x;
-        if (i < hi) {
-          x.k0 = __ldcg(&src[i].k0); x.k1 = __ldcg(&src[i].k1);
-          x.k2 = __ldcg(&src[i].k2); x.ss = __ldcg(&src[i].ss); x.seg = __ldcg(&src[i].seg);
-          take = seg_key(x) <= s.wthr[x.seg];
-        }
-        const uint32_t bal = __ballot_sync(~0u, take);
-        if (bal) {
-          uint32_t basep = 0;
-          if (lane == 0) basep = atomicAdd(&g->nsel, (unsigned)__popc(bal));
-          basep = __shfl_sync(~0u, basep, 0);
-          const uint32_t pos = basep + __popc(bal & ((1u << lane) - 1u));
-          if (take) {
-            atomicAdd(&g->selcnt[x.seg], 1u);
-            if (pos < (uint32_t)CAND_MAX) dst[pos] = x;
-          }
-        }
-      }
-      break;
-    }
-    case CMD_REFRESH:    // (no cached structural priority any more: nothing to refresh)
-      break;
-    case CMD_CLEAR_T: {
-      const uint64_t tb = (uint64_t)d.tmask + 1;
-      part_range(tb, c.rank, c.GP, lo, hi);
-      uint64_t* keys = d.tkey + (uint64_t)c.r * tb;
-      for (uint64_t i = lo + tid; i < hi; i += NT) keys[i] = KEY_EMPTY;
-      break;
-    }
-    case CMD_FILL_T: {
-      const uint64_t tb = (uint64_t)d.tmask + 1;
-      part_range(d.C, c.rank, c.GP, lo, hi);
-      uint64_t* keys = d.tkey + (uint64_t)c.r * tb;
-      uint32_t* vals = d.tval + (uint64_t)c.r * tb;
-      for (uint64_t sl = lo + tid; sl < hi; sl += NT) {
-        const uint64_t gi = c.base + sl;
-        if (__ldcg(d.bmeta + gi) & M_LIVE)
-          tbl_insert(keys, vals, d.tmask, __ldcg(d.bhash + gi), (uint32_t)sl, &g->tblcnt);
-      }
-      break;
-    }
-    case CMD_CLEAR_G: {
-      const uint64_t gt = (uint64_t)d.gmask + 1;
-      part_range(gt, c.rank, c.GP, lo, hi);
-      uint64_t* keys = d.gkey + (uint64_t)c.r * gt;
-      for (uint64_t i = lo + tid; i < hi; i += NT) keys[i] = KEY_EMPTY;
-      break;
-    }
-    case CMD_FILL_G: {
-      const uint64_t gt = (uint64_t)d.gmask + 1, gb = (uint64_t)c.r * d.G;
-      part_range(d.G, c.rank, c.GP, lo, hi);
-      uint64_t* keys = d.gkey + (uint64_t)c.r * gt;
-      uint32_t* vals = d.gval + (uint64_t)c.r * gt;
-      for (uint64_t p = lo + tid; p < hi; p += NT)
-        if (__ldcg(d.glive + gb + p))
-          d.gtslot[gb + p] = tbl_insert(keys, vals, d.gmask, __ldcg(d.ghash + gb + p), (uint32_t)p, &g->gtblcnt);
-      break;
-    }
-    case CMD_COUNTQ: {
-      if (tid < 4) s.cnt[tid] = 0;
-      __syncthreads();
-      part_range(d.C, c.rank, c.GP, lo, hi);
-      for (uint64_t sl = lo + tid; sl < hi; sl += NT) {
-        const uint32_t m = __ldcg(d.bmeta + c.base + sl);
-        if (m & M_LIVE) atomicAdd(&s.cnt[meta_q(m)], 1u);
-      }
-      __syncthreads();
-      if (tid < 4 && s.cnt[tid]) atomicAdd(&g->cntq[tid], s.cnt[tid]);
-      break;
-    }
-    default:
-      break;
-  }
-  __syncthreads();
-}
-
-// Leader: run a command on the whole group (GP == 1: just run it over everything).
-__device__ void issue(Ctx& c, unsigned cmd) {
-  if (c.GP == 1) {
-    run_cmd(c, cmd, true);
-    return;
-  }
-  if (threadIdx.x == 0) c.ctl->cmd = cmd;
-  uint64_t t0 = gtimer();
-  group_bar(c);                 // workers start
-  if (cmd == CMD_EXIT) return;
-  uint64_t t1 = gtimer();
-  run_cmd(c, cmd, true);
-  uint64_t t2 = gtimer();
-  group_bar(c);                 // everyone done
-  if (threadIdx.x == 0) {
-    const uint64_t t3 = gtimer();
-    c.s->st.tph[8] += t1 - t0;
-    c.s->st.tph[9] += t2 - t1;
-    c.s->st.tph[10] += t3 - t2;
-  }
-}
-
-__device__ void worker_loop(Ctx& c) {
-  while (true) {
-    group_bar(c);
-    const unsigned cmd = __ldcg(&c.ctl->cmd);
-    if (cmd == CMD_EXIT) return;
-    run_cmd(c, cmd, false);
-    group_bar(c);
-  }
-}
-
-// Recompute the cached structural priority of every live STRUCT block (gamma changed).
-__device__ void refresh_pstruct(Ctx& c) {
-  if (threadIdx.x == 0) c.ctl->gamma = c.s->st.par.gamma;
-  __syncthreads();
-  issue(c, CMD_REFRESH);
-}
-
-// Rebuild the resident table (tombstone cleanup) from the live SoA.
-__device__ void rebuild_table(Ctx& c) {
-  if (threadIdx.x == 0) c.ctl->tblcnt = 0;
-  __syncthreads();
-  issue(c, CMD_CLEAR_T);
-  issue(c, CMD_FILL_T);
-  if (threadIdx.x == 0) c.s->st.tbl_used = __ldcg(&c.ctl->tblcnt);
-  __syncthreads();
-}
-__device__ void rebuild_ghost(Ctx& c) {
-  if (threadIdx.x == 0) c.ctl->gtblcnt = 0;
-  __syncthreads();
-  issue(c, CMD_CLEAR_G);
-  issue(c, CMD_FILL_G);
-  if (threadIdx.x == 0) c.s->st.gtbl_used = __ldcg(&c.ctl->gtblcnt);
-  __syncthreads();
-}
-
-// stride-halving tree sum over y[0..P) in smem (SURVEY c.3 TREE)
-__device__ double tree_sum(double* y, int P) {
-  for (int h = P >> 1; h >= 1; h >>= 1) {
-    for (int i = threadIdx.x; i < h; i += NT) y[i] = __dadd_rn(y[i], y[i + h]);
-    __syncthreads();
-  }
-  double r = y[0];
-  __syncthreads();
-  return r;
-}
-
-__device__ __forceinline__ double clampd(double x, double lo, double hi) {
-  return x < lo ? lo : (x > hi ? hi : x);
-}
-
-// LEARN (SURVEY c.3): TokenWeights -> QueueWeights -> LognormalParams -> DecayPower.
-__device__ void learn(Ctx& c) {
-  const Dev& d = *c.d;
-  Smem& s = *c.s;
-  RState& st = s.st;
-  sae_params& p = st.par;
-  const uint32_t f = p.learn_flags;
-  const double gamma_old = p.gamma;
-  // L1 TokenWeights (A16, A17)
-  if ((f & SAE_L_TOKENS) && threadIdx.x == 0) {
-    for (int t = 0; t < 5; ++t) {
-      if (st.ts_ev[t] > 10) {
-        double rm = __ddiv_rn((double)st.ts_mae[t], (double)st.ts_ev[t]);
-        double rr = st.ts_acc[t] > 0 ? __ddiv_rn((double)st.ts_hit[t], (double)st.ts_acc[t]) : 0.0;
-        if (f & SAE_L_TOKEN_MULT) {
-          p.w[t] = __dmul_rn(p.w[t], __dadd_rn(1.0, __dmul_rn(p.eta, rm)));
-        } else {
-          double tgt = __dadd_rn(__dadd_rn(1.0, __dmul_rn(rm, p.a_miss)), __dmul_rn(rr, p.b_reuse));
-          p.w[t] = __dadd_rn(__dmul_rn(__dsub_rn(1.0, p.eta), p.w[t]), __dmul_rn(p.eta, tgt));
-        }
-        p.w[t] = clampd(p.w[t], 0.1, 5.0);
-      }
-    }
-    for (int t = 0; t < 5; ++t) {
-      st.ts_ev[t] = (99ull * st.ts_ev[t]) / 100ull;
-      st.ts_mae[t] = (99ull * st.ts_mae[t]) / 100ull;
-      st.ts_hit[t] = (99ull * st.ts_hit[t]) / 100ull;
-      st.ts_acc[t] = (99ull * st.ts_acc[t]) / 100ull;
-    }
-  }
-  // L2 QueueWeights (Alg. P:575-597 or relative rule P:814-817)
-  if (f & SAE_L_QUEUES) {
-    if (f & SAE_L_QUEUE_RELATIVE) {
-      if (threadIdx.x < 4) c.ctl->cntq[threadIdx.x] = 0;
-      __syncthreads();
-      issue(c, CMD_COUNTQ);
-      if (threadIdx.x < 3) s.cnt[threadIdx.x] = __ldcg(&c.ctl->cntq[threadIdx.x + 1]);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double Eq[3];
-        bool def[3];
-        double sum = 0.0;
-        int nd = 0;
-        for (int q = 0; q < 3; ++q) {
-          double frac = __ddiv_rn((double)s.cnt[q], (double)d.C);
-          def[q] = frac > 0.0;
-          if (def[q]) { Eq[q] = __ddiv_rn((double)st.qh[q], frac); sum = __dadd_rn(sum, Eq[q]); nd++; }
-        }
-        if (nd > 0) {
-          double Ebar = __ddiv_rn(sum, (double)nd);
-          if (Ebar > 0.0) {
-            for (int q = 0; q < 3; ++q) {
-              if (!def[q]) continue;
-              double x = __ddiv_rn(Eq[q], Ebar);
-              double pw = (x == 0.0) ? 0.0 : dm::ex(__ddiv_rn(dm::ln(x), p.T));
-              p.alpha[q] = __dadd_rn(p.alpha[q], __dmul_rn(p.beta_q, __dsub_rn(pw, p.alpha[q])));
-              p.alpha[q] = clampd(p.alpha[q], 0.1, 3.0);
-            }
-          }
-        }
-        for (int q = 0; q < 3; ++q) { st.qh[q] = 0; st.qe[q] = 0; }
-      }
-    } else if (threadIdx.x == 0) {
-      for (int q = 0; q < 3; ++q) {
-        if (st.qe[q] > 5) {
-          double eff = __ddiv_rn((double)st.qh[q], (double)st.qe[q]);
-          double tgt = __dadd_rn(1.0, __ddiv_rn(eff, p.T));
-          p.alpha[q] = __dadd_rn(p.alpha[q], __dmul_rn(p.beta_q, __dsub_rn(tgt, p.alpha[q])));
-          p.alpha[q] = clampd(p.alpha[q], 0.1, 3.0);
-        }
-      }
-      for (int q = 0; q < 3; ++q) { st.qh[q] = 0; st.qe[q] = 0; }
-    }
-  }
-  __syncthreads();
-  // L3 LognormalParams (Alg. P:762-784; A23, A24, A25)
-  if (f & SAE_L_LOGNORMAL) {
-    double* y = reinterpret_cast<double*>(c.cand);
-    for (int sidx = 0; sidx < 2; ++sidx) {
-      uint32_t n = st.iv_len[sidx];
-      if (n > d.iv_min) {
-        int P = 1;
-        while ((uint32_t)P < n) P <<= 1;
-        const double* ring = d.iv + ((uint64_t)c.r * 2 + sidx) * RMAX;
-        uint32_t first = (st.iv_head[sidx] + RMAX - n) % RMAX;
-        for (int i = threadIdx.x; i < P; i += NT) y[i] = (uint32_t)i < n ? ring[(first + i) % RMAX] : 0.0;
-        __syncthreads();
-        double sum = tree_sum(y, P);
-        double m = __ddiv_rn(sum, (double)n);
-        for (int i = threadIdx.x; i < P; i += NT) {
-          double x = (uint32_t)i < n ? ring[(first + i) % RMAX] : 0.0;
-          double dd = __dsub_rn(x, m);
-          y[i] = (uint32_t)i < n ? __dmul_rn(dd, dd) : 0.0;
-        }
-        __syncthreads();
-        double v = __ddiv_rn(tree_sum(y, P), (double)n);
-        if (threadIdx.x == 0) {
-          double sd = __dsqrt_rn(v);
-          p.mu[sidx] = __dadd_rn(p.mu[sidx], __dmul_rn(p.beta_ln, __dsub_rn(m, p.mu[sidx])));
-          p.sigma[sidx] = __dadd_rn(p.sigma[sidx], __dmul_rn(p.beta_ln, __dsub_rn(sd, p.sigma[sidx])));
-          if (p.sigma[sidx] < 0.1) p.sigma[sidx] = 0.1;
-          if (n > d.iv_keep) st.iv_len[sidx] = d.iv_keep;
-        }
-        __syncthreads();
-      }
-    }
-  }
-  // L4 DecayPower (A27)
-  if ((f & SAE_L_DECAY) && threadIdx.x == 0) {
-    uint32_t NB = d.nbins, half = NB / 2;
-    double fs = 0.0, bs = 0.0;
-    int fc = 0, bc = 0;
-    for (uint32_t i = 0; i < NB; ++i) {
-      if (st.pb_acc[i] == 0) continue;
-      double rate = __ddiv_rn((double)st.pb_hit[i], (double)st.pb_acc[i]);
-      if (i < half) { fs = __dadd_rn(fs, rate); fc++; } else { bs = __dadd_rn(bs, rate); bc++; }
-    }
-    if (fc > 0 && bc > 0) {
-      double fa = __ddiv_rn(fs, (double)fc), ba = __ddiv_rn(bs, (double)bc);
-      if (fa > 0.0) {
-        double ratio = __ddiv_rn(ba, fa);
-        double est = __ddiv_rn(1.0, __dadd_rn(ratio, 0.1));
-        p.gamma = __dadd_rn(p.gamma, __dmul_rn(p.beta_gamma, __dsub_rn(est, p.gamma)));
-        p.gamma = clampd(p.gamma, 0.3, 3.0);
-      }
-    }
-    for (uint32_t i = 0; i < NB; ++i) {
-      st.pb_hit[i] = (99ull * st.pb_hit[i]) / 100ull;
-      st.pb_acc[i] = (99ull * st.pb_acc[i]) / 100ull;
-    }
-  }
-  __syncthreads();
-  double cw_old[4];
-  for (int t = 0; t < 4; ++t) cw_old[t] = s.cw[2][t];
-  __syncthreads();
-  recompute_cw(s);
-  __syncthreads();
-  // STRUCT-class thresholds follow the parameter change (heuristic only; the exactness
-  // check in select_chunk never depends on them): P scales with alpha*w, and for a gamma
-  // decrease p(gamma')/p(gamma) lies in [gamma'/gamma, 1], so T' = T * gamma'/gamma keeps
-  // the new candidate set inside the old one (no candidate explosion after a firing).
-  if (threadIdx.x < 4 && st.thr[9 + threadIdx.x] != ~0ull && cw_old[threadIdx.x] > 0.0) {
-    double f = s.cw[2][threadIdx.x] / cw_old[threadIdx.x];
-    if (p.gamma < gamma_old) f *= p.gamma / gamma_old;
-    if (f != 1.0) {
-      const double T = from_obits(st.thr[9 + threadIdx.x]);
-      st.thr[9 + threadIdx.x] = obits(T * f);
-    }
-  }
-  if (threadIdx.x == 0) {
-    st.learner_firings++;
-    if (d.traj_cap > 0) {
-      sae_traj t;
-      t.E = st.E;
-      t.request = st.requests;
-      for (int i = 0; i < 5; ++i) t.w[i] = p.w[i];
-      for (int i = 0; i < 3; ++i) t.alpha[i] = p.alpha[i];
-      for (int i = 0; i < 2; ++i) { t.mu[i] = p.mu[i]; t.sigma[i] = p.sigma[i]; }
-      t.gamma = p.gamma;
-      d.traj[(uint64_t)c.r * d.traj_cap + (st.traj_n % d.traj_cap)] = t;
-      st.traj_n++;
-    }
-  }
-  __syncthreads();
-}
-
-// ---------------------------------------------------------------------------
-// Fused score + select (a4 + a5) for one chunk of m <= MSUB victims (no learner firing
-// inside).  Exact: key = (tier, primary, last, id) per SURVEY c.2 O11.  One pass over
-// the SoA (split over the group's CTAs) computes every resident, unpinned block's
-// segment (EF / 8 multi-turn classes (queue, tau) / 4 STRUCT classes (tau)) and key:
-// EF (ntok, id); multi-turn (last, id) -- P is strictly decreasing in dt within a class
-// (§8(a) a4), so only class heads need Eq.(1); STRUCT (P, last, id) with the cached
-// p_struct.  Blocks at or below their segment's carried threshold are candidates; the
-// candidates are sorted by (tier, key), an exactness check proves no excluded block can
-// be a victim (else the segment is rescanned), thresholds are re-carried.
-// Output: the victims' slots in eviction order in cand[0..m).
-// ---------------------------------------------------------------------------
-__device__ void narrow(Ctx& c, uint32_t e, uint32_t mp);
-
-// Block-wide MSB radix select over a[0..n): for every class g in `active` find the key of
-// rank s.target[g] (1-based) -> s.pfx[g], and the number of smaller keys -> s.below[g].
-// Global mode: one class (0), key k0.  Per-segment mode: class = segment, key = seg_key.
-__device__ void radix_select(const Cand* a, uint32_t n, bool per_seg, uint32_t active, Smem& s) {
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (tid < 16) { s.pfx[tid] = 0; s.pmask[tid] = 0; s.below[tid] = 0; }
-  __syncthreads();
-  for (int shift = 56; shift >= 0; shift -= 8) {
-    for (int i = tid; i < NSEG * 256; i += NT) s.rhist[i] = 0;
-    __syncthreads();
-    for (uint32_t i0 = 0; i0 < n; i0 += NT) {
-      const uint32_t i = i0 + tid;
-      uint32_t bin = 0xFFFFFFFFu;
-      if (i < n) {
-        const Cand& x = a[i];
-        const uint32_t g = per_seg ? x.seg : 0u;
-        if (g < 16 && ((active >> g) & 1u)) {
-          const uint64_t key = per_seg ? seg_key(x) : x.k0;
-          if ((key & s.pmask[g]) == s.pfx[g]) bin = g * 256u + (uint32_t)((key >> shift) & 255u);
-        }
-      }
-      const uint32_t peers = __match_any_sync(~0u, bin);
-      if (bin != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&s.rhist[bin], (uint32_t)__popc(peers));
-    }
-    __syncthreads();
-    for (int g = wid; g < NSEG; g += NW) {
-      if (!((active >> g) & 1u)) continue;
-      uint32_t v[8], loc = 0;
-      for (int j = 0; j < 8; ++j) { v[j] = s.rhist[g * 256 + lane * 8 + j]; loc += v[j]; }
-      uint32_t inc = loc;
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(~0u, inc, o);
-        if (lane >= o) inc += y;
-      }
-      const uint32_t need = s.target[g] - s.below[g];
-      const uint32_t excl = inc - loc;
-      const uint32_t bal = __ballot_sync(~0u, excl < need && inc >= need);
-      __syncwarp();
-      if (lane == __ffs(bal) - 1) {
-        uint32_t run = excl;
-        int bsel = 0;
-        for (int j = 0; j < 8; ++j) {
-          if (run + v[j] >= need) { bsel = lane * 8 + j; break; }
-          run += v[j];
-        }
-        s.below[g] += run;
-        s.pfx[g] |= (uint64_t)bsel << shift;
-        s.pmask[g] |= 0xFFull << shift;
-      }
-    }
-    __syncthreads();
-  }
-}
-
-__device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass) {
-  const Dev& d = *c.d;
-  Smem& s = *c.s;
-  RState& st = s.st;
-  GroupCtl* g = c.ctl;
-  const double now = st.now;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const bool gm = !d.cand_smem;
-  uint32_t e = 0, mp = 0, c0 = 0;
-  for (int attempt = 0; attempt < 3; ++attempt) {
-    if (tid < 16) { s.used[tid] = 0; }
-    if (tid == 0) {
-      s.fail = 0;
-      g->stamp = stamp;
-      if (gm) {
-        g->ncand = 0;
-        g->now = now;
-        for (int i = 0; i < 16; ++i) { g->segtot[i] = 0; g->cnt[i] = 0; g->thr[i] = st.thr[i]; }
-        for (int q = 0; q < 3; ++q) for (int t = 0; t < 5; ++t) g->cw[q][t] = s.cw[q][t];
-        for (int i = 0; i < 2; ++i) { g->mu[i] = st.par.mu[i]; g->sigma[i] = st.par.sigma[i]; }
-        g->gamma = st.par.gamma;
-      }
-    }
-    __syncthreads();
-    uint64_t t0 = gtimer();
-    issue(c, CMD_SCAN);
-    if (tid == 0) { const uint64_t t1 = gtimer(); st.tph[1] += t1 - t0; t0 = t1; }
-    if (gm) {            // gather the group's counts; bring the candidates into smem
-      if (tid < 16) { s.segtot[tid] = __ldcg(&g->segtot[tid]); s.cnt[tid] = __ldcg(&g->cnt[tid]); }
-      if (tid == 0) s.ncand = __ldcg(&g->ncand);
-      __syncthreads();
-      const uint32_t e0 = min(m, s.segtot[0]);
-      const bool narrowed = s.ncand > (uint32_t)CAND_MAX;
-      if (tid == 0) { st.select_raw += s.ncand; st.select_narrow += narrowed ? 1 : 0; }
-      if (narrowed) narrow(c, e0, m - e0);
-      if (tid == 0 && narrowed) { const uint64_t t1 = gtimer(); st.tph[2] += t1 - t0; t0 = t1; }
-      const Cand* src = narrowed ? d.gsel + (uint64_t)c.r * CAND_MAX : d.gcand + c.base;
-      for (uint32_t i = tid; i < s.ncand; i += NT) {
-        Cand x;
-        x.k0 = __ldcg(&src[i].k0); x.k1 = __ldcg(&src[i].k1); x.k2 = __ldcg(&src[i].k2);
-        x.ss = __ldcg(&src[i].ss); x.seg = __ldcg(&src[i].seg);
-        c.cand[i] = x;
-      }
-      __syncthreads();
-    }
-    const uint32_t nc = s.ncand;
-    if (tid == 0) {
-      st.select_passes++;
-      st.select_cands += nc;
-      if (nc > (uint32_t)NT) st.select_big++;
-      if (attempt == 0 && count_pass) {   // one required pass per chunk (extra passes are overhead)
-        uint32_t tot = 0;
-        for (int k = 0; k < NSEG; ++k) tot += s.segtot[k];
-        st.blocks_scored += tot;
-        for (int k = 9; k < NSEG; ++k) st.blocks_scored_struct += s.segtot[k];
-      }
-    }
-    __syncthreads();
-    // The victims are the m smallest candidates by (k0, k1, k2): EF keys (ntok, id) are
-    // < 2^63 <= obits(P), so Stage 1 precedes Stage 2 by construction.
-    c0 = s.cnt[0];
-    e = min(m, s.segtot[0]);
-    mp = m - e;
-    uint64_t Kth = ~0ull;
-    if (nc >= m) {
-      if (tid == 0) s.target[0] = m;
-      __syncthreads();
-      radix_select(c.cand, nc, false, 1u, s);
-      Kth = s.pfx[0];
-    }
-    // ---- exactness check: every block a threshold left out must lose to the mp-th
-    //      scored candidate.  EF: enough heads.  Class c: a non-candidate has last > T_c,
-    //      so dt < now - T_c and, P being strictly decreasing in dt within a class,
-    //      P > P_c(now - T_c).  STRUCT class: a non-candidate has P > T_S.
-    if (tid == 0 && c0 < e) atomicOr(&s.fail, 1u);
-    if (mp > 0 && tid >= 1 && tid < NSEG && s.segtot[tid] > s.cnt[tid]) {
-      const uint32_t gsg = tid;
-      const double Pth = nc >= m ? from_obits(Kth) : __longlong_as_double(0x7ff0000000000000ll);
-      bool ok;
-      if (gsg >= 9) {
-        ok = Pth <= from_obits(st.thr[gsg]);
-      } else {
-        const uint32_t q = 1 + (gsg - 1) / 4, tau = (gsg - 1) & 3;
-        double dt = __dsub_rn(now, from_obits(st.thr[gsg]));
-        if (dt < d.dt_eps) dt = d.dt_eps;
-        const double p = survival(dt, st.par.mu[q - 1], st.par.sigma[q - 1], d.z_cut);
-        ok = Pth < __ddiv_rn(__dmul_rn(s.cw[q - 1][tau], p), dt);
-      }
-      if (!ok) atomicOr(&s.fail, 1u << gsg);
-    }
-    __syncthreads();
-    const uint32_t fail = s.fail;
-    if (tid == 0) st.tph[3] += gtimer() - t0;
-    if (fail == 0) break;
-    if (tid < 10 && ((fail >> tid) & 1u)) st.select_fail_seg[tid]++;
-    if (tid < NSEG && (((fail >> tid) & 1u) || attempt >= 1)) st.thr[tid] = ~0ull;
-    __syncthreads();
-  }
-  const uint32_t nc = s.ncand;
-  uint64_t Kth = nc >= m ? s.pfx[0] : ~0ull;
-  // ---- stage the victims: every candidate with k0 <= Kth (the m smallest plus key ties)
-  if (tid == 0) s.nv = 0;
-  if (tid < 16) s.kmin[tid] = ~0ull;
-  __syncthreads();
-  for (uint32_t i0 = 0; i0 < nc; i0 += NT) {
-    const uint32_t i = i0 + tid;
-    if (i < nc) {
-      const Cand& x = c.cand[i];
-      // EF grows within its threshold's num_tokens band: min over that band only
-      if (x.seg != 0 || (x.k0 >> 32) == (st.thr[0] >> 32))
-        atomicMin(&s.kmin[x.seg], (unsigned long long)seg_key(x));
-    }
-    const bool take = i < nc && c.cand[i].k0 <= Kth;
-    const uint32_t bal = __ballot_sync(~0u, take);
-    uint32_t basep = 0;
-    if (lane == 0 && bal) basep = atomicAdd(&s.nv, (uint32_t)__popc(bal));
-    basep = __shfl_sync(~0u, basep, 0);
-    const uint32_t pos = basep + __popc(bal & ((1u << lane) - 1u));
-    if (take && pos < VCAP) c.vbuf[pos] = c.cand[i];
-  }
-  __syncthreads();
-  uint32_t nv = s.nv;
-  if (nv > VCAP) {               // pathological key ties: fall back to a full sort
-    int N = 32;
-    while ((uint32_t)N < nc) N <<= 1;
-    for (uint32_t i = nc + tid; i < (uint32_t)N; i += NT) {
-      c.cand[i].k0 = ~0ull; c.cand[i].k1 = ~0ull; c.cand[i].k2 = ~0u; c.cand[i].ss = 15u << 28;
-      c.cand[i].seg = 15;
-    }
-    __syncthreads();
-    sort_cands(c.cand, N);
-    for (uint32_t v = tid; v < m; v += NT) c.vbuf[v] = c.cand[v];
-    nv = m;
-    __syncthreads();
-  } else {
-    int N = 32;
-    while ((uint32_t)N < nv) N <<= 1;
-    for (uint32_t i = nv + tid; i < (uint32_t)N; i += NT) {
-      c.vbuf[i].k0 = ~0ull; c.vbuf[i].k1 = ~0ull; c.vbuf[i].k2 = ~0u; c.vbuf[i].ss = 15u << 28;
-      c.vbuf[i].seg = 15;
-    }
-    __syncthreads();
-    sort_cands(c.vbuf, N);       // small: the m victims in (k0, last, id) order
-  }
-  // ---- carry thresholds: trim segments holding far more candidates than they use
-  for (uint32_t v = tid; v < m; v += NT) atomicAdd(&s.used[c.vbuf[v].seg], 1u);
-  __syncthreads();
-  // small private pools (rescans are cheap) trim hard; large pools trim lazily
-  const uint32_t trim_at = 8u, trim_to = 4u;
-  uint32_t shrink = 0;
-  for (int g = 0; g < NSEG; ++g) {
-    const uint32_t want = 3 * s.used[g] + SLACK;
-    if (s.cnt[g] > trim_at * want) shrink |= 1u << g;
-  }
-  if (shrink && nv <= VCAP) {
-    if (tid < NSEG) s.target[tid] = trim_to * (3 * s.used[tid] + SLACK);
-    __syncthreads();
-    radix_select(c.cand, nc, true, shrink, s);
-    if (tid < NSEG && ((shrink >> tid) & 1u)) st.thr[tid] = s.pfx[tid];
-    __syncthreads();
-  }
-  // ---- grow a segment's threshold before its reserve runs dry (avoids refills): double
-  //      the key distance from the smallest candidate (keys: EF (ntok,id); class last;
-  //      STRUCT P).  Heuristic only -- exactness is re-proved every pass.
-  if (tid < NSEG && !((shrink >> tid) & 1u)) {
-    const uint32_t g = tid;
-    const uint64_t T = st.thr[g];
-    const uint32_t left = s.cnt[g] - min(s.cnt[g], s.used[g]);
-    if (T != ~0ull && s.segtot[g] > s.cnt[g] && left < 2 * s.used[g] + SLACK) {
-      const uint64_t km = s.kmin[g] == ~0ull ? T : (uint64_t)s.kmin[g];
-      uint64_t Tn;
-      if (g == 0) {                 // id part only, saturating inside the ntok band
-        const uint64_t band = T & ~0xFFFFFFFFull, idT = T & 0xFFFFFFFFull;
-        const uint64_t idm = (km & ~0xFFFFFFFFull) == band ? (km & 0xFFFFFFFFull) : idT;
-        const uint64_t dlt = max(idT - min(idm, idT), (uint64_t)4096);
-        Tn = band | min(idT + dlt, (uint64_t)0xFFFFFFFFull);
-      } else if (g <= 8) {
-        const double Tl = from_obits(T), kl = from_obits(km);
-        Tn = obits(Tl + fmax(Tl - kl, 1.0));
-      } else {
-        const double Tp = from_obits(T), kp = from_obits(km);
-        Tn = obits(fmax(2.0 * Tp - kp, 1.5 * Tp));
-      }
-      st.thr[g] = Tn;
-    }
-  }
-  __syncthreads();
-  for (uint32_t v = tid; v < m; v += NT) c.cand[v] = c.vbuf[v];
-  __syncthreads();
-}
-
-// Too many candidates for the leader's smem: choose, per over-full segment, the exact key
-// of rank target_s by a group-parallel MSB radix select over the candidate buffer, then
-// compact the candidates at or below the new thresholds.  The new thresholds are exact
-// bounds (every dropped candidate has a larger key), so the exactness check still holds.
-__device__ void narrow(Ctx& c, uint32_t e, uint32_t mp) {
-  Smem& s = *c.s;
-  RState& st = s.st;
-  GroupCtl* g = c.ctl;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (tid < NSEG) {
-    const uint32_t need = tid == 0 ? e : mp;
-    s.target[tid] = 3 * (need + SLACK);   // refill a reserve for several chunks
-    s.pfx[tid] = 0;
-    s.pmask[tid] = 0;
-    s.below[tid] = 0;
-  }
-  __syncthreads();
-  uint32_t active = 0;
-  for (int k = 0; k < NSEG; ++k) if (s.cnt[k] > s.target[k]) active |= 1u << k;
-  for (int shift = 56; shift >= 0 && active; shift -= 8) {
-    if (tid == 0) {
-      g->shift = (unsigned)shift;
-      g->active = active;
-      for (int k = 0; k < NSEG; ++k) { g->pfx[k] = s.pfx[k]; g->pmask[k] = s.pmask[k]; }
-    }
-    for (int i = tid; i < NSEG * 256; i += NT) g->hist[i] = 0;
-    __syncthreads();
-    issue(c, CMD_HIST);
-    // one warp per active segment: find the digit holding rank target
-    for (int k = wid; k < NSEG; k += NW) {
-      if (!((active >> k) & 1u)) continue;
-      uint32_t v[8], loc = 0;
-      for (int j = 0; j < 8; ++j) { v[j] = __ldcg(&g->hist[k * 256 + lane * 8 + j]); loc += v[j]; }
-      uint32_t inc = loc;
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(~0u, inc, o);
-        if (lane >= o) inc += y;
-      }
-      const uint32_t need = s.target[k] - s.below[k];     // >= 1
-      const uint32_t excl = inc - loc;
-      const bool mine = excl < need && inc >= need;
-      const uint32_t bal = __ballot_sync(~0u, mine);
-      __syncwarp();
-      const int src = __ffs(bal) - 1;
-      if (lane == src) {
-        uint32_t run = excl;
-        int b = 0;
-        for (int j = 0; j < 8; ++j) {
-          if (run + v[j] >= need) { b = lane * 8 + j; break; }
-          run += v[j];
-        }
-        s.below[k] += run;
-        s.pfx[k] |= (uint64_t)b << shift;
-        s.pmask[k] |= 0xFFull << shift;
-      }
-    }
-    __syncthreads();
-  }
-  if (tid == 0) {
-    for (int k = 0; k < NSEG; ++k) if ((active >> k) & 1u) st.thr[k] = s.pfx[k];
-    for (int k = 0; k < 16; ++k) { g->thr[k] = st.thr[k]; g->selcnt[k] = 0; }
-    g->nsel = 0;
-  }
-  __syncthreads();
-  issue(c, CMD_COMPACT);
-  if (tid < 16) s.cnt[tid] = __ldcg(&g->selcnt[tid]);
-  if (tid == 0) {
-    s.ncand = __ldcg(&g->nsel);
-    if (s.ncand > (uint32_t)CAND_MAX) {     // pathological key ties: cannot hold them all
-      st.err = (uint32_t)(-SAE_E_OVERFLOW);
-      raise_err(*c.d, SAE_E_OVERFLOW);
-      s.ncand = CAND_MAX;
-    }
-  }
-  __syncthreads();
-}
-
-// Apply a chunk of m victims (cand[0..m) in eviction order): SURVEY c.2 O11 steps 1-4.
-__device__ void apply_chunk(Ctx& c, uint32_t m, uint32_t* vids_out) {
-  const Dev& d = *c.d;
-  Smem& s = *c.s;
-  RState& st = s.st;
-  const uint64_t tb = (uint64_t)d.tmask + 1, gt = (uint64_t)d.gmask + 1;
-  uint64_t* tkey = d.tkey + (uint64_t)c.r * tb;
-  uint64_t* gkey = d.gkey + (uint64_t)c.r * gt;
-  uint32_t* gval = d.gval + (uint64_t)c.r * gt;
-  const uint64_t gb = (uint64_t)c.r * d.G;
-  for (uint32_t v0 = 0; v0 < m; v0 += d.G) {
-    const uint32_t mb = min(m - v0, d.G);
-    // phase 1: remove from the resident table, count, expire ghost slots
-    for (uint32_t v = threadIdx.x; v < mb; v += NT) {
-      const uint32_t sl = c.cand[v0 + v].ss & SLOT_MASK;
-      const uint64_t gi = c.base + sl;
-      const uint64_t H = d.bhash[gi];
-      const uint32_t meta = d.bmeta[gi];
-      const uint32_t q = meta_q(meta), tau = meta_tau(meta);
-      if (vids_out) vids_out[v0 + v] = d.bid[gi];
-      int32_t pos = tbl_find_pos(tkey, d.tmask, H);
-      if (pos >= 0) tkey[pos] = KEY_TOMB;
-      d.bmeta[gi] = 0;
-      if (tau < 5) atomicAdd((unsigned long long*)&st.ts_ev[tau], 1ull);
-      if (q != Q_EF) atomicAdd((unsigned long long*)&st.qe[q - 1], 1ull);
-      atomicAdd((unsigned long long*)&st.evict_by_queue[q], 1ull);
-      atomicAdd((unsigned long long*)&st.evict_by_type[tau], 1ull);
-      const uint32_t p = (uint32_t)((st.gseq + v0 + v) % d.G);
-      if (d.glive[gb + p]) {  // FIFO expiry of the oldest ghost (A30)
-        gkey[d.gtslot[gb + p]] = KEY_TOMB;
-        d.glive[gb + p] = 0;
-      }
-      d.ghash[gb + p] = H;
-      d.gtau[gb + p] = (uint8_t)tau;
-    }
-    __syncthreads();
-    // phase 2: ghost push (recently_evicted[hash] = tau), free the slot
-    for (uint32_t v = threadIdx.x; v < mb; v += NT) {
-      const uint32_t sl = c.cand[v0 + v].ss & SLOT_MASK;
-      const uint64_t gi = c.base + sl;
-      const uint32_t p = (uint32_t)((st.gseq + v0 + v) % d.G);
-      const uint64_t H = d.ghash[gb + p];
-      d.glive[gb + p] = 1;
-      d.gtslot[gb + p] = tbl_insert(gkey, gval, d.gmask, H, p, &st.gtbl_used);
-      d.freestk[c.base + st.free_top + v0 + v] = sl;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      st.free_top += mb;
-      st.live -= mb;
-      st.gseq += mb;
-      st.E += mb;
-      st.evictions += mb;
-    }
-    __syncthreads();
-  }
-}
-
-// Evict k victims with pin stamp (k <= unpinned residents), chunked at K crossings (A14)
-// and in passes of at most MSUB victims (keys are frozen between firings).
-__device__ void evict_k(Ctx& c, uint64_t k, uint32_t stamp, uint32_t* vids_out) {
-  const Dev& d = *c.d;
-  Smem& s = *c.s;
-  uint64_t done = 0, chunk_end = 0;
-  while (done < k) {
-    const uint64_t to_cross = d.K - (s.st.E % d.K);
-    const bool first = done >= chunk_end;          // first sub-pass of a chunk between firings
-    if (first) chunk_end = done + min(k - done, to_cross);
-    const uint32_t m = (uint32_t)min(min(k - done, to_cross), (uint64_t)MSUB);
-    select_chunk(c, m, stamp, first);
-    uint64_t t0 = gtimer();
-    apply_chunk(c, m, vids_out ? vids_out + done : nullptr);
-    if (threadIdx.x == 0) { const uint64_t t1 = gtimer(); s.st.tph[4] += t1 - t0; t0 = t1; }
-    done += m;
-    if (s.st.E % d.K == 0) {
-      learn(c);
-      if (threadIdx.x == 0) s.st.tph[5] += gtimer() - t0;
-    }
-  }
-  if (s.st.gtbl_used > ((d.gmask + 1) / 4) * 3) rebuild_ghost(c);
-}
-
-__device__ void load_state(Ctx& c) {
-  const Dev& d = *c.d;
-  const uint32_t* src = reinterpret_cast<const uint32_t*>(d.st + c.r);
-  uint32_t* dst = reinterpret_cast<uint32_t*>(&c.s->st);
-  for (int i = threadIdx.x; i < (int)(sizeof(RState) / 4); i += NT) dst[i] = __ldcg(src + i);
-  __syncthreads();
-  recompute_cw(*c.s);
-  __syncthreads();
-}
-__device__ void store_state(Ctx& c) {
-  __syncthreads();
-  const Dev& d = *c.d;
-  uint32_t* dst = reinterpret_cast<uint32_t*>(d.st + c.r);
-  const uint32_t* src = reinterpret_cast<const uint32_t*>(&c.s->st);
-  for (int i = threadIdx.x; i < (int)(sizeof(RState) / 4); i += NT) dst[i] = src[i];
-}
-
-// One request round (SURVEY c.2 O1-O13).  Returns false on a sticky error.
-__device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
-  const Dev& d = *c.d;
-  Smem& s = *c.s;
-  RState& st = s.st;
-  const uint64_t tb = (uint64_t)d.tmask + 1, gt = (uint64_t)d.gmask + 1;
-  uint64_t* tkey = d.tkey + (uint64_t)c.r * tb;
-  uint32_t* tval = d.tval + (uint64_t)c.r * tb;
-  uint64_t* gkey = d.gkey + (uint64_t)c.r * gt;
-  uint32_t* gval = d.gval + (uint64_t)c.r * gt;
-  const uint64_t gb = (uint64_t)c.r * d.G;
-  const double now = b.arrival[i];
-  const uint32_t L = b.plen[i], O = b.dlen[i];
-  // O1 / time check
-  if (L < 1 || (st.has_now && now < st.now)) {
-    if (threadIdx.x == 0) {
-      st.err = L < 1 ? (uint32_t)(-SAE_E_INVAL) : (uint32_t)(-SAE_E_TIME);
-      raise_err(d, L < 1 ? SAE_E_INVAL : SAE_E_TIME);
-    }
-    __syncthreads();
-    return false;
-  }
-  const uint32_t B = d.B;
-  const uint32_t np = (L + B - 1) / B, n = np + (O + B - 1) / B;
-  const uint64_t bo = b.boff[i];
-  const uint32_t fl = b.flags[i], spb = b.spb[i];
-  const bool mt = fl & 1, ag = fl & 2, cid = fl & 4;
-  const bool untempl = !mt && spb == 0;             // A31
-  const uint32_t omax = np > 1 ? np - 1 : 1;         // A8
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    st.now = now;
-    st.has_now = 1;
-    st.round++;
-    s.h = (int32_t)n;
-    s.npin = 0;
-    s.matched = 0;
-  }
-  __syncthreads();
-  const uint32_t stamp = (uint32_t)st.round;
-  uint64_t tA = gtimer();
-  // ---- O4/O5 classify + probe (Alg.1 Classify P:550-564; strict prefix P:158)
-  for (uint32_t j = threadIdx.x; j < n; j += NT) {
-    const uint64_t H = b.h[bo + j];
-    const uint32_t tau = b.tau[bo + j];
-    const int32_t sl = tbl_find(tkey, tval, d.tmask, H);
-    b.slot[bo + j] = sl;
-    b.q[bo + j] = (uint8_t)classify(tau, mt, ag, cid, j < spb, untempl);
-    if (sl < 0) atomicMin(&s.h, (int32_t)j);
-    else atomicAdd(&s.npin, 1u);
-  }
-  __syncthreads();
-  const uint32_t h = (uint32_t)s.h;
-  // ---- O6-O9 stats, touch, orphans, miss-after-evict; ordered ranks by block scans
-  uint32_t new_base = 0;
-  for (uint32_t j0 = 0; j0 < n; j0 += NT) {
-    const uint32_t j = j0 + threadIdx.x;
-    const bool valid = j < n;
-    uint32_t fc = 0, fa = 0, fn = 0;
-    double lnv = 0.0;
-    if (valid) {
-      const int32_t sl = b.slot[bo + j];
-      const uint32_t q = b.q[bo + j], tau = b.tau[bo + j];
-      const uint32_t bin = min(d.nbins - 1, (d.nbins * j) / omax);
-      if (tau < 5) atomicAdd((unsigned long long*)&st.ts_acc[tau], 1ull);
-      if (q == Q_STRUCT) atomicAdd((unsigned long long*)&st.pb_acc[bin], 1ull);
-      if (sl >= 0) {
-        const uint64_t gi = c.base + (uint32_t)sl;
-        const uint32_t meta = d.bmeta[gi];
-        if (j < h) {  // O7 hit (A9: credited to the old queue before re-routing)
-          double dt = __dsub_rn(now, d.blast[gi]);
-          if (dt < d.dt_eps) dt = d.dt_eps;
-          const uint32_t qo = meta_q(meta);
-          if (qo == Q_CHAT || qo == Q_AGENT) {
-            atomicAdd((unsigned long long*)&st.qh[qo - 1], 1ull);
-            lnv = dm::ln(dt);
-            if (qo == Q_CHAT) fc = 1; else fa = 1;
-          } else if (qo == Q_STRUCT) {
-            atomicAdd((unsigned long long*)&st.qh[2], 1ull);
-          }
-          if (tau < 5) atomicAdd((unsigned long long*)&st.ts_hit[tau], 1ull);
-          if (q == Q_STRUCT) atomicAdd((unsigned long long*)&st.pb_hit[bin], 1ull);
-          if (j < np) atomicAdd(&s.matched, (uint32_t)b.ntok[bo + j]);
-          d.bacc[gi] += 1;
-        }
-        // O7/O8 touch: last = now, hint overwritten (A9, A10)
-        d.blast[gi] = now;
-        d.bmeta[gi] = meta_pack(q, tau, meta_ntok(meta)) | M_PIN;   // pinned for this round (A11)
-        d.bob[gi] = j;
-        d.bomax[gi] = omax;
-        d.blr[gi] = lr_of(j, omax);
-      } else if (j >= h) {  // O9 miss-after-evict, consumed (A30)
-        const uint64_t H = b.h[bo + j];
-        const int32_t gp = tbl_find_pos(gkey, d.gmask, H);
-        if (gp >= 0) {
-          const uint32_t rp = gval[gp];
-          const uint32_t gtau = d.gtau[gb + rp];
-          if (gtau < 5) atomicAdd((unsigned long long*)&st.ts_mae[gtau], 1ull);
-          atomicAdd((unsigned long long*)&st.mae_by_type[gtau], 1ull);
-          gkey[gp] = KEY_TOMB;
-          d.glive[gb + rp] = 0;
-        }
-        fn = 1;
-      }
-    }
-    uint32_t rc, ra, rn;
-    block_scan3(fc, fa, fn, rc, ra, rn, s.tot, s.wsum);
-    if (fc) d.iv[((uint64_t)c.r * 2 + 0) * RMAX + (st.iv_head[0] + rc) % RMAX] = lnv;
-    if (fa) d.iv[((uint64_t)c.r * 2 + 1) * RMAX + (st.iv_head[1] + ra) % RMAX] = lnv;
-    if (valid) b.nrank[bo + j] = fn ? (int32_t)(new_base + rn) : -1;
-    new_base += s.tot[2];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int q = 0; q < 2; ++q) {
-        st.iv_head[q] = (st.iv_head[q] + s.tot[q]) % RMAX;
-        st.iv_len[q] = min(d.iv_ring, st.iv_len[q] + s.tot[q]);
-      }
-    }
-    __syncthreads();
-  }
-  // ---- O10 admission size (A11)
-  if (threadIdx.x == 0) {
-    const uint64_t f = d.C - st.live;
-    const uint64_t U = st.live - s.npin;
-    uint64_t k = new_base > f ? new_base - f : 0;
-    uint64_t admit = new_base;
-    if (k > U) { k = U; admit = f + U; }
-    s.k = k;
-    s.admit = admit;
-    if (k > 0) st.eviction_rounds++;
-    if (b.boff[i] + k > b.vcap) { st.err = (uint32_t)(-SAE_E_OVERFLOW); raise_err(d, SAE_E_OVERFLOW); }
-  }
-  __syncthreads();
-  if (st.err) return false;
-  const uint64_t k = s.k, admit = s.admit;
-  if (threadIdx.x == 0) st.tph[0] += gtimer() - tA;
-  // ---- O11 evictions (Alg.1 Evict x k, chunked at K crossings)
-  if (k > 0) evict_k(c, k, stamp, b.o_vids ? b.o_vids + b.boff[i] : nullptr);
-  tA = gtimer();
-  // ---- unpin this request's resident blocks
-  for (uint32_t j = threadIdx.x; j < n; j += NT) {
-    const int32_t sl = b.slot[bo + j];
-    if (sl >= 0) d.bmeta[c.base + (uint32_t)sl] &= ~M_PIN;
-  }
-  // ---- O12 insert New (Alg.1 Add: q.insert(b))
-  if (threadIdx.x == 0 && st.next_id + admit > 0xFFFFFFFFull) {
-    st.err = (uint32_t)(-SAE_E_OVERFLOW);
-    raise_err(d, SAE_E_OVERFLOW);
-  }
-  __syncthreads();
-  if (st.err) return false;
-  for (uint32_t j = threadIdx.x; j < n; j += NT) {
-    const int32_t rk = b.nrank[bo + j];
-    if (rk < 0 || (uint64_t)rk >= admit) continue;
-    const uint32_t sl = d.freestk[c.base + st.free_top - 1 - rk];
-    const uint64_t gi = c.base + sl;
-    const uint64_t H = b.h[bo + j];
-    const uint32_t q = b.q[bo + j], tau = b.tau[bo + j];
-    d.bhash[gi] = H;
-    d.blast[gi] = now;
-    d.bid[gi] = (uint32_t)(st.next_id + rk);
-    d.bacc[gi] = 1;
-    d.bmeta[gi] = meta_pack(q, tau, b.ntok[bo + j]);
-    d.bob[gi] = j;
-    d.bomax[gi] = omax;
-    d.blr[gi] = lr_of(j, omax);
-    tbl_insert(tkey, tval, d.tmask, H, sl, &st.tbl_used);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    st.free_top -= (uint32_t)admit;
-    st.live += (uint32_t)admit;
-    st.next_id += admit;
-    // ---- O13 outputs
-    if (b.o_hit) b.o_hit[i] = h;
-    if (b.o_miss) b.o_miss[i] = n - h;
-    if (b.o_matched) b.o_matched[i] = s.matched;
-    if (b.o_nvict) b.o_nvict[i] = (uint32_t)k;
-    st.requests++;
-    st.blocks_looked_up += n;
-    st.hit_blocks += h;
-    st.hit_tokens += s.matched;
-    st.prompt_tokens += L;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) { const uint64_t t1 = gtimer(); st.tph[6] += t1 - tA; tA = t1; }
-  if (st.tbl_used > (d.tmask + 1) / 4 * 3) {
-    rebuild_table(c);
-    if (threadIdx.x == 0) st.tph[7] += gtimer() - tA;
-  }
-  return true;
-}
-
-extern __shared__ __align__(16) unsigned char g_smem[];
-
-__device__ Ctx make_ctx(const Dev& d, uint32_t r, uint32_t rank) {
-  Ctx c;
-  c.d = &d;
-  c.s = reinterpret_cast<Smem*>(g_smem);
-  c.cand = reinterpret_cast<Cand*>(g_smem + ((sizeof(Smem) + 15) / 16) * 16);
-  c.vbuf = c.cand + CAND_MAX;
-  c.ctl = d.ctl + r;
-  c.r = r;
-  c.rank = rank;
-  c.GP = d.GP;
-  c.base = (uint64_t)r * d.C;
-  return c;
-}
-
-// Persistent replay: the group of GP CTAs (blockIdx / GP) owns replica r; its leader
-// (rank 0) replays the replica's run of the batch in order, the others execute the
-// leader's group commands (scan / histogram / compact / refresh / rebuild).
-__global__ void __launch_bounds__(NT, 1) k_replay(Dev d, BatchDev b) {
-  const uint32_t r = blockIdx.x / d.GP, rank = blockIdx.x % d.GP;
-  if (r >= d.R) return;
-  Ctx c = make_ctx(d, r, rank);
-  if (rank != 0) {
-    worker_loop(c);
-    return;
-  }
-  const uint32_t lo = b.run_start[r];
-  if (lo != 0xFFFFFFFFu) {
-    const uint32_t hi = b.run_end[r];
-    load_state(c);
-    if (c.s->st.err == 0) {
-      for (uint32_t i = lo; i < hi; ++i)
-        if (!admit_one(c, b, i)) break;
-    }
-    store_state(c);
-  }
-  if (c.GP > 1) issue(c, CMD_EXIT);
-}
-
-// sae_evict: Alg.1 Evict x k with an empty pin set.
-__global__ void __launch_bounds__(NT, 1) k_evict(Dev d, uint32_t r, uint32_t k, double now,
-                                                 uint32_t* vids, uint32_t* n_out) {
-  Ctx c = make_ctx(d, r, blockIdx.x);
-  if (blockIdx.x != 0) {
-    worker_loop(c);
-    return;
-  }
-  load_state(c);
-  RState& st = c.s->st;
-  if (st.err == 0) {
-    if (st.has_now && now < st.now) {
-      if (threadIdx.x == 0) { st.err = (uint32_t)(-SAE_E_TIME); raise_err(d, SAE_E_TIME); }
-    } else {
-      __syncthreads();
-      if (threadIdx.x == 0) { st.now = now; st.has_now = 1; st.round++; }
-      __syncthreads();
-      const uint32_t kk = min(k, st.live);
-      if (kk > 0) {
-        if (threadIdx.x == 0) st.eviction_rounds++;
-        evict_k(c, kk, 0xFFFFFFFFu /* no block carries this stamp */, vids);
-      }
-      if (threadIdx.x == 0) {
-        if (n_out) *n_out = kk;
-        if (kk < k) raise_err(d, SAE_E_EMPTY);
-      }
-    }
-  }
-  store_state(c);
-  if (c.GP > 1) issue(c, CMD_EXIT);
-}
-
-__global__ void __launch_bounds__(NT, 1) k_update(Dev d, uint32_t r0, uint32_t r1) {
-  const uint32_t r = r0 + blockIdx.x / d.GP, rank = blockIdx.x % d.GP;
-  if (r >= r1) return;
-  Ctx c = make_ctx(d, r, rank);
-  if (rank != 0) {
-    worker_loop(c);
-    return;
-  }
-  load_state(c);
-  learn(c);
-  store_state(c);
-  if (c.GP > 1) issue(c, CMD_EXIT);
-}
+namespace v512 {
+constexpr int NT = 512;
+constexpr int NW = NT / 32;
+constexpr int CAND_MAX = 4096;
+#include "replay_impl.cuh"
+}  // namespace v512
+namespace v256 {
+constexpr int NT = 256;
+constexpr int NW = NT / 32;
+constexpr int CAND_MAX = 2560;
+#include "replay_impl.cuh"
+}  // namespace v256
 
 // read-only probe, one warp per request
 __global__ void k_lookup(Dev d, BatchDev b, uint32_t* out) {
@@ -2163,6 +492,30 @@ __global__ void k_gen_tokens(uint64_t seed, uint64_t np, const uint64_t* stream,
 // ===========================================================================
 using namespace sae;
 
+// The two compiled replay variants (replay_impl.cuh).
+struct Variant {
+  const void* replay;
+  const void* evict;
+  const void* update;
+  int nt;
+  size_t smem;
+  uint32_t cand_max;
+};
+static Variant variant(int nt) {
+  if (nt == 256)
+    return {(const void*)v256::k_replay, (const void*)v256::k_evict, (const void*)v256::k_update, 256,
+            v256::smem_bytes(), (uint32_t)v256::CAND_MAX};
+  return {(const void*)v512::k_replay, (const void*)v512::k_evict, (const void*)v512::k_update, 512,
+          v512::smem_bytes(), (uint32_t)v512::CAND_MAX};
+}
+
+static cudaError_t launch_group(const Variant& v, const void* fn, uint32_t grid, bool coop, cudaStream_t s,
+                                Dev& d, BatchDev* x) {
+  void* args[] = {(void*)&d, (void*)x};
+  if (coop) return cudaLaunchCooperativeKernel(fn, grid, v.nt, args, v.smem, s);
+  return cudaLaunchKernel(fn, grid, v.nt, args, v.smem, s);
+}
+
 struct sae_ctx {
   sae_config cfg;
   Dev d;
@@ -2175,6 +528,7 @@ struct sae_ctx {
   std::vector<void*> allocs;
   // optional profiling: CUDA events around every k_replay launch (bench roofline)
   uint64_t coresident = 0;
+  Variant var;
   bool prof = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev;
 };
@@ -2199,17 +553,6 @@ static cudaError_t dalloc(sae_ctx* ctx, T** p, uint64_t n) {
   cudaError_t e = cudaMalloc((void**)p, (n ? n : 1) * sizeof(T));
   if (e == cudaSuccess) ctx->allocs.push_back((void*)*p);
   return e;
-}
-
-static size_t smem_bytes() {
-  return ((sizeof(Smem) + 15) / 16) * 16 + sizeof(Cand) * (CAND_MAX + VCAP);
-}
-
-static cudaError_t launch_group(const void* fn, uint32_t grid, bool coop, cudaStream_t s, Dev& d,
-                                BatchDev* x) {
-  void* args[] = {(void*)&d, (void*)x};
-  if (coop) return cudaLaunchCooperativeKernel(fn, grid, NT, args, smem_bytes(), s);
-  return cudaLaunchKernel(fn, grid, NT, args, smem_bytes(), s);
 }
 
 extern "C" {
@@ -2274,12 +617,21 @@ sae_status sae_create(const sae_config* cfg, sae_ctx** out) {
   // otherwise a co-resident group (cooperative launch) that splits every scan pass
   int nsm = 0, occ = 0;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg->device));
-  CK(cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes()));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_replay, NT, smem_bytes()));
+  for (int vnt : {256, 512}) {
+    const Variant v = variant(vnt);
+    for (const void* f : {v.replay, v.evict, v.update})
+      CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem));
+  }
+  // many small single-CTA replicas (more than SMs) take the 256-thread variant: two per SM
+  // hide each other's per-round latency; few replicas, groups and larger pools the 512-thread
+  // one (lower latency per replica)
+  const bool small = d.C <= variant(256).cand_max && cfg->ctas_per_replica <= 1 && R > (uint64_t)nsm;
+  ctx->var = variant(small ? 256 : 512);
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ctx->var.replay, ctx->var.nt, ctx->var.smem));
   const uint64_t coresident = (uint64_t)nsm * (uint64_t)(occ > 0 ? occ : 1);
   uint64_t gp = cfg->ctas_per_replica;
   if (gp == 0) {
-    if (d.C <= (uint32_t)CAND_MAX) gp = 1;
+    if (d.C <= ctx->var.cand_max) gp = 1;
     else gp = std::min<uint64_t>(std::max<uint64_t>(1, d.C / 8192), coresident / R);
   }
   if (gp == 0 || (gp > 1 && gp * R > coresident)) {
@@ -2287,14 +639,14 @@ sae_status sae_create(const sae_config* cfg, sae_ctx** out) {
     return SAE_E_INVAL;
   }
   d.GP = (uint32_t)gp;
-  d.cand_smem = (d.C <= (uint32_t)CAND_MAX && d.GP == 1) ? 1u : 0u;
+  d.cand_smem = (d.C <= ctx->var.cand_max && d.GP == 1) ? 1u : 0u;
   d.bulk_ok = (d.C % 4 == 0) ? 1u : 0u;
   ctx->coresident = coresident;
   CK(dalloc(ctx, &d.ctl, R));
   CK(cudaMemset(d.ctl, 0, R * sizeof(GroupCtl)));
   if (!d.cand_smem) {
     CK(dalloc(ctx, &d.gcand, RC));
-    CK(dalloc(ctx, &d.gsel, R * (uint64_t)CAND_MAX));
+    CK(dalloc(ctx, &d.gsel, R * (uint64_t)ctx->var.cand_max));
   }
   // initial scalar state
   std::vector<RState> st(R);
@@ -2311,9 +663,6 @@ sae_status sae_create(const sae_config* cfg, sae_ctx** out) {
   k_init<<<1024, 256>>>(d);
   ctx->launches++;
   CK(cudaGetLastError());
-  CK(cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes()));
-  CK(cudaFuncSetAttribute(k_evict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes()));
-  CK(cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes()));
   CK(cudaDeviceSynchronize());
   *out = ctx;
   return SAE_OK;
@@ -2470,7 +819,7 @@ sae_status sae_admit_batch(sae_ctx* ctx, const sae_batch* b, sae_admit_out* o, s
     CK(cudaEventCreate(&e1));
     CK(cudaEventRecord(e0, s));
   }
-  CK(launch_group((const void*)k_replay, ctx->d.R * ctx->d.GP, ctx->d.GP > 1, s, ctx->d, &x));
+  CK(launch_group(ctx->var, ctx->var.replay, ctx->d.R * ctx->d.GP, ctx->d.GP > 1, s, ctx->d, &x));
   ctx->launches++;
   if (ctx->prof) {
     CK(cudaEventRecord(e1, s));
@@ -2500,9 +849,9 @@ sae_status sae_evict(sae_ctx* ctx, uint32_t replica, uint32_t k, double now, uin
   if (!ctx || replica >= ctx->d.R || (k > 0 && !vids)) return SAE_E_INVAL;
   void* args[] = {(void*)&ctx->d, (void*)&replica, (void*)&k, (void*)&now, (void*)&vids, (void*)&n_out};
   if (ctx->d.GP > 1)
-    CK(cudaLaunchCooperativeKernel((const void*)k_evict, ctx->d.GP, NT, args, smem_bytes(), (cudaStream_t)st));
+    CK(cudaLaunchCooperativeKernel(ctx->var.evict, ctx->d.GP, ctx->var.nt, args, ctx->var.smem, (cudaStream_t)st));
   else
-    CK(cudaLaunchKernel((const void*)k_evict, 1, NT, args, smem_bytes(), (cudaStream_t)st));
+    CK(cudaLaunchKernel(ctx->var.evict, 1, ctx->var.nt, args, ctx->var.smem, (cudaStream_t)st));
   ctx->launches++;
   CK(cudaGetLastError());
   return SAE_OK;
@@ -2519,9 +868,9 @@ sae_status sae_update(sae_ctx* ctx, uint32_t replica, sae_stream st) {
     uint32_t b = std::min(r1, a + per);
     void* args[] = {(void*)&ctx->d, (void*)&a, (void*)&b};
     if (ctx->d.GP > 1)
-      CK(cudaLaunchCooperativeKernel((const void*)k_update, (b - a) * ctx->d.GP, NT, args, smem_bytes(), (cudaStream_t)st));
+      CK(cudaLaunchCooperativeKernel(ctx->var.update, (b - a) * ctx->d.GP, ctx->var.nt, args, ctx->var.smem, (cudaStream_t)st));
     else
-      CK(cudaLaunchKernel((const void*)k_update, b - a, NT, args, smem_bytes(), (cudaStream_t)st));
+      CK(cudaLaunchKernel(ctx->var.update, b - a, ctx->var.nt, args, ctx->var.smem, (cudaStream_t)st));
     ctx->launches++;
   }
   CK(cudaGetLastError());
