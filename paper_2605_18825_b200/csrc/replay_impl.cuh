@@ -8,6 +8,12 @@
 // ---------------------------------------------------------------------------
 // Block-wide helpers (NT threads)
 // ---------------------------------------------------------------------------
+// CTA barrier in its non-aligned form (barrier.sync): every thread arrives individually.
+// bar.sync / __syncthreads() is the .aligned form, which presumes that a warp reaches it
+// converged; the replay loops diverge lanes (hash probes, fdlibm calls) right before
+// block-wide steps, and with the aligned form a lane that reconverged late was observed to
+// drift one barrier generation behind its block ("CTA barriers").
+__device__ __forceinline__ void cta_sync() { asm volatile("barrier.sync 0;" ::: "memory"); }
 // exclusive scan of up to 3 flags per thread; returns ranks; totals in tot[3]
 __device__ __forceinline__ void block_scan3(uint32_t a, uint32_t b, uint32_t c, uint32_t& ra,
                                             uint32_t& rb, uint32_t& rc, uint32_t* tot,
@@ -17,7 +23,7 @@ __device__ __forceinline__ void block_scan3(uint32_t a, uint32_t b, uint32_t c, 
   uint32_t lm = (1u << lane) - 1u;
   ra = __popc(ba & lm); rb = __popc(bb & lm); rc = __popc(bc & lm);
   if (lane == 0) { wsum[w] = __popc(ba); wsum[NW + w] = __popc(bb); wsum[2 * NW + w] = __popc(bc); }
-  __syncthreads();
+  cta_sync();
   uint32_t oa = 0, ob = 0, oc = 0, ta = 0, tb = 0, tc = 0;
   for (int i = 0; i < NW; ++i) {
     uint32_t x = wsum[i], y = wsum[NW + i], z = wsum[2 * NW + i];
@@ -26,7 +32,7 @@ __device__ __forceinline__ void block_scan3(uint32_t a, uint32_t b, uint32_t c, 
   }
   ra += oa; rb += ob; rc += oc;
   tot[0] = ta; tot[1] = tb; tot[2] = tc;
-  __syncthreads();
+  cta_sync();
 }
 
 __device__ __forceinline__ bool cand_less(const Cand& a, const Cand& b) {
@@ -49,7 +55,7 @@ __device__ void block_sort(Cand* cand, int N) {
           if (cand_less(y, x) == up) { cand[i] = y; cand[ixj] = x; }
         }
       }
-      __syncthreads();
+      cta_sync();
     }
   }
 }
@@ -100,10 +106,10 @@ __device__ void sort_reg(Cand* a, int N) {
       if (j >= 32) {
 #pragma unroll
         for (int e = 0; e < E; ++e) if (e * NT + t < N) a[e * NT + t] = x[e];
-        __syncthreads();
+        cta_sync();
 #pragma unroll
         for (int e = 0; e < E; ++e) y[e] = (e * NT + t < N) ? a[(e * NT + t) ^ j] : x[e];
-        __syncthreads();
+        cta_sync();
       } else {
 #pragma unroll
         for (int e = 0; e < E; ++e) y[e] = shfl_cand(x[e], j);
@@ -119,7 +125,7 @@ __device__ void sort_reg(Cand* a, int N) {
   }
 #pragma unroll
   for (int e = 0; e < E; ++e) if (e * NT + t < N) a[e * NT + t] = x[e];
-  __syncthreads();
+  cta_sync();
 }
 
 __device__ void sort_cands(Cand* a, int N) {
@@ -186,7 +192,7 @@ __device__ __forceinline__ void part_range(uint64_t n, uint32_t rank, uint32_t G
 // Group barrier over the GP CTAs of one replica (co-resident by cooperative launch).
 // ---------------------------------------------------------------------------
 __device__ void group_bar(Ctx& c) {
-  __syncthreads();
+  cta_sync();
   if (threadIdx.x == 0) {
     GroupCtl* g = c.ctl;
     volatile unsigned* genp = &g->bar_gen;
@@ -201,7 +207,7 @@ __device__ void group_bar(Ctx& c) {
     }
     __threadfence();
   }
-  __syncthreads();
+  cta_sync();
 }
 
 // Parameters of a scan, from the leader's smem (leader) or the control block (workers).
@@ -383,7 +389,7 @@ __device__ void scan_range(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P) {
     for (int u = 0; u < 4; ++u) { mt[u] = mn[u]; idv[u] = in_[u]; lt[u] = ln_[u]; }
     s0 = sn;
   }
-  __syncthreads();
+  cta_sync();
   if (gm) {
     finalize_noted(c, P, gdst);
   } else {
@@ -476,14 +482,14 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     for (uint64_t t = 0; t < ntiles && t < (uint64_t)BSTAGES; ++t) issue_tile(t);
   }
-  __syncthreads();
+  cta_sync();
   // thresholds as doubles (multi-turn: last; STRUCT: P) for the division-free prefilter
   double* thrD = reinterpret_cast<double*>(&s.wpfx[0]);   // 16 doubles of scratch
   if (tid < NSEG) {
     const uint64_t T = P.thr[tid];
     thrD[tid] = (T == ~0ull || tid == 0) ? __longlong_as_double(0x7ff0000000000000ll) : from_obits(T);
   }
-  __syncthreads();
+  cta_sync();
   const double inflate = 1.0 + 0x1p-40;
   const float gamf = (float)P.gamma;
   for (uint64_t t = 0; t < ntiles; ++t) {
@@ -546,13 +552,13 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
         }
       }
     }
-    __syncthreads();                       // stage st fully consumed
+    cta_sync();                       // stage st fully consumed
     if (tid == 0 && t + BSTAGES < ntiles) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads -> async writes
       issue_tile(t + BSTAGES);
     }
   }
-  __syncthreads();
+  cta_sync();
   finalize_noted(c, P, gdst);
 #pragma unroll
   for (int w = 0; w < 4; ++w) {
@@ -585,7 +591,7 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
     case CMD_SCAN: {
       if (tid < 16) { s.segtot[tid] = 0; s.cnt[tid] = 0; }
       if (tid == 0) { s.ncand = 0; s.nw = 0; }
-      __syncthreads();
+      cta_sync();
       ScanP P;
       if (leader) {   // the leader scans with its own smem copies
         P.now = s.st.now;
@@ -595,7 +601,7 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
         if (tid < 16) s.wthr[tid] = __ldcg(&g->thr[tid]);
         if (tid < 15) s.wcw[tid] = __ldcg(&g->cw[0][0] + tid);
         if (tid < 2) { s.wmu[tid] = __ldcg(&g->mu[tid]); s.wsg[tid] = __ldcg(&g->sigma[tid]); }
-        __syncthreads();
+        cta_sync();
         P.now = __ldcg(&g->now);
         P.thr = (const unsigned long long*)s.wthr; P.cw = s.wcw; P.mu = s.wmu; P.sg = s.wsg;
       }
@@ -619,7 +625,7 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
         part_range(d.C, c.rank, c.GP, lo, hi);
         scan_range(c, lo, hi, P);
       }
-      __syncthreads();
+      cta_sync();
       if (!d.cand_smem && tid < NSEG) {
         if (s.segtot[tid]) atomicAdd(&g->segtot[tid], s.segtot[tid]);
         if (s.cnt[tid]) atomicAdd(&g->cnt[tid], s.cnt[tid]);
@@ -629,9 +635,9 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
     case CMD_HIST: {   // radix histograms of the active segments' keys (global candidates)
       unsigned* h = reinterpret_cast<unsigned*>(c.cand);
       for (int i = tid; i < NSEG * 256; i += NT) h[i] = 0;
-      __syncthreads();
+      cta_sync();
       if (tid < 16) { s.wpfx[tid] = __ldcg(&g->pfx[tid]); s.wpmask[tid] = __ldcg(&g->pmask[tid]); }
-      __syncthreads();
+      cta_sync();
       const unsigned shift = __ldcg(&g->shift), active = __ldcg(&g->active);
       part_range(__ldcg(&g->ncand), c.rank, c.GP, lo, hi);
       const Cand* src = d.gcand + c.base;
@@ -642,15 +648,15 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
         if ((key & s.wpmask[seg]) != s.wpfx[seg]) continue;
         atomicAdd(&h[seg * 256 + ((key >> shift) & 255u)], 1u);
       }
-      __syncthreads();
+      cta_sync();
       for (int i = tid; i < NSEG * 256; i += NT)
         if (h[i]) atomicAdd(&g->hist[i], h[i]);
-      __syncthreads();
+      cta_sync();
       break;
     }
     case CMD_COMPACT: {  // keep candidates at or below the (new) thresholds
       if (tid < 16) s.wthr[tid] = __ldcg(&g->thr[tid]);
-      __syncthreads();
+      cta_sync();
       part_range(__ldcg(&g->ncand), c.rank, c.GP, lo, hi);
       const Cand* src = d.gcand + c.base;
       Cand* dst = d.gsel + (uint64_t)c.r * CAND_MAX;
@@ -718,20 +724,20 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
     }
     case CMD_COUNTQ: {
       if (tid < 4) s.cnt[tid] = 0;
-      __syncthreads();
+      cta_sync();
       part_range(d.C, c.rank, c.GP, lo, hi);
       for (uint64_t sl = lo + tid; sl < hi; sl += NT) {
         const uint32_t m = __ldcg(d.bmeta + c.base + sl);
         if (m & M_LIVE) atomicAdd(&s.cnt[meta_q(m)], 1u);
       }
-      __syncthreads();
+      cta_sync();
       if (tid < 4 && s.cnt[tid]) atomicAdd(&g->cntq[tid], s.cnt[tid]);
       break;
     }
     default:
       break;
   }
-  __syncthreads();
+  cta_sync();
 }
 
 // Leader: run a command on the whole group (GP == 1: just run it over everything).
@@ -769,36 +775,36 @@ __device__ void worker_loop(Ctx& c) {
 // Recompute the cached structural priority of every live STRUCT block (gamma changed).
 __device__ void refresh_pstruct(Ctx& c) {
   if (threadIdx.x == 0) c.ctl->gamma = c.s->st.par.gamma;
-  __syncthreads();
+  cta_sync();
   issue(c, CMD_REFRESH);
 }
 
 // Rebuild the resident table (tombstone cleanup) from the live SoA.
 __device__ void rebuild_table(Ctx& c) {
   if (threadIdx.x == 0) c.ctl->tblcnt = 0;
-  __syncthreads();
+  cta_sync();
   issue(c, CMD_CLEAR_T);
   issue(c, CMD_FILL_T);
   if (threadIdx.x == 0) c.s->st.tbl_used = __ldcg(&c.ctl->tblcnt);
-  __syncthreads();
+  cta_sync();
 }
 __device__ void rebuild_ghost(Ctx& c) {
   if (threadIdx.x == 0) c.ctl->gtblcnt = 0;
-  __syncthreads();
+  cta_sync();
   issue(c, CMD_CLEAR_G);
   issue(c, CMD_FILL_G);
   if (threadIdx.x == 0) c.s->st.gtbl_used = __ldcg(&c.ctl->gtblcnt);
-  __syncthreads();
+  cta_sync();
 }
 
 // stride-halving tree sum over y[0..P) in smem (SURVEY c.3 TREE)
 __device__ double tree_sum(double* y, int P) {
   for (int h = P >> 1; h >= 1; h >>= 1) {
     for (int i = threadIdx.x; i < h; i += NT) y[i] = __dadd_rn(y[i], y[i + h]);
-    __syncthreads();
+    cta_sync();
   }
   double r = y[0];
-  __syncthreads();
+  cta_sync();
   return r;
 }
 
@@ -840,10 +846,10 @@ __device__ void learn(Ctx& c) {
   if (f & SAE_L_QUEUES) {
     if (f & SAE_L_QUEUE_RELATIVE) {
       if (threadIdx.x < 4) c.ctl->cntq[threadIdx.x] = 0;
-      __syncthreads();
+      cta_sync();
       issue(c, CMD_COUNTQ);
       if (threadIdx.x < 3) s.cnt[threadIdx.x] = __ldcg(&c.ctl->cntq[threadIdx.x + 1]);
-      __syncthreads();
+      cta_sync();
       if (threadIdx.x == 0) {
         double Eq[3];
         bool def[3];
@@ -880,7 +886,7 @@ __device__ void learn(Ctx& c) {
       for (int q = 0; q < 3; ++q) { st.qh[q] = 0; st.qe[q] = 0; }
     }
   }
-  __syncthreads();
+  cta_sync();
   // L3 LognormalParams (Alg. P:762-784; A23, A24, A25)
   if (f & SAE_L_LOGNORMAL) {
     double* y = reinterpret_cast<double*>(c.cand);
@@ -892,7 +898,7 @@ __device__ void learn(Ctx& c) {
         const double* ring = d.iv + ((uint64_t)c.r * 2 + sidx) * RMAX;
         uint32_t first = (st.iv_head[sidx] + RMAX - n) % RMAX;
         for (int i = threadIdx.x; i < P; i += NT) y[i] = (uint32_t)i < n ? ring[(first + i) % RMAX] : 0.0;
-        __syncthreads();
+        cta_sync();
         double sum = tree_sum(y, P);
         double m = __ddiv_rn(sum, (double)n);
         for (int i = threadIdx.x; i < P; i += NT) {
@@ -900,7 +906,7 @@ __device__ void learn(Ctx& c) {
           double dd = __dsub_rn(x, m);
           y[i] = (uint32_t)i < n ? __dmul_rn(dd, dd) : 0.0;
         }
-        __syncthreads();
+        cta_sync();
         double v = __ddiv_rn(tree_sum(y, P), (double)n);
         if (threadIdx.x == 0) {
           double sd = __dsqrt_rn(v);
@@ -909,7 +915,7 @@ __device__ void learn(Ctx& c) {
           if (p.sigma[sidx] < 0.1) p.sigma[sidx] = 0.1;
           if (n > d.iv_keep) st.iv_len[sidx] = d.iv_keep;
         }
-        __syncthreads();
+        cta_sync();
       }
     }
   }
@@ -937,12 +943,12 @@ __device__ void learn(Ctx& c) {
       st.pb_acc[i] = (99ull * st.pb_acc[i]) / 100ull;
     }
   }
-  __syncthreads();
+  cta_sync();
   double cw_old[4];
   for (int t = 0; t < 4; ++t) cw_old[t] = s.cw[2][t];
-  __syncthreads();
+  cta_sync();
   recompute_cw(s);
-  __syncthreads();
+  cta_sync();
   // STRUCT-class thresholds follow the parameter change (heuristic only; the exactness
   // check in select_chunk never depends on them): P scales with alpha*w, and for a gamma
   // decrease p(gamma')/p(gamma) lies in [gamma'/gamma, 1], so T' = T * gamma'/gamma keeps
@@ -969,7 +975,7 @@ __device__ void learn(Ctx& c) {
       st.traj_n++;
     }
   }
-  __syncthreads();
+  cta_sync();
 }
 
 // ---------------------------------------------------------------------------
@@ -994,10 +1000,10 @@ __device__ void radix_select(const Cand* a, uint32_t n, bool per_seg, uint32_t a
   // tie = 1: key k1 over the candidates with k0 == K0; tie = 2: key k2 over k0 == K0 && k1 == K1
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid < 16) { s.pfx[tid] = 0; s.pmask[tid] = 0; s.below[tid] = 0; }
-  __syncthreads();
+  cta_sync();
   for (int shift = 56; shift >= 0; shift -= 8) {
     for (int i = tid; i < NSEG * 256; i += NT) s.rhist[i] = 0;
-    __syncthreads();
+    cta_sync();
     for (uint32_t i0 = 0; i0 < n; i0 += NT) {
       const uint32_t i = i0 + tid;
       uint32_t bin = 0xFFFFFFFFu;
@@ -1013,7 +1019,7 @@ __device__ void radix_select(const Cand* a, uint32_t n, bool per_seg, uint32_t a
       const uint32_t peers = __match_any_sync(~0u, bin);
       if (bin != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&s.rhist[bin], (uint32_t)__popc(peers));
     }
-    __syncthreads();
+    cta_sync();
     for (int g = wid; g < NSEG; g += NW) {
       if (!((active >> g) & 1u)) continue;
       uint32_t v[8], loc = 0;
@@ -1039,7 +1045,7 @@ __device__ void radix_select(const Cand* a, uint32_t n, bool per_seg, uint32_t a
         s.pmask[g] |= 0xFFull << shift;
       }
     }
-    __syncthreads();
+    cta_sync();
   }
 }
 
@@ -1066,14 +1072,14 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
         g->gamma = st.par.gamma;
       }
     }
-    __syncthreads();
+    cta_sync();
     uint64_t t0 = gtimer();
     issue(c, CMD_SCAN);
     if (tid == 0) { const uint64_t t1 = gtimer(); st.tph[1] += t1 - t0; t0 = t1; }
     if (gm) {            // gather the group's counts; bring the candidates into smem
       if (tid < 16) { s.segtot[tid] = __ldcg(&g->segtot[tid]); s.cnt[tid] = __ldcg(&g->cnt[tid]); }
       if (tid == 0) s.ncand = __ldcg(&g->ncand);
-      __syncthreads();
+      cta_sync();
       const uint32_t e0 = min(m, s.segtot[0]);
       const bool narrowed = s.ncand > (uint32_t)CAND_MAX;
       if (tid == 0) { st.select_raw += s.ncand; st.select_narrow += narrowed ? 1 : 0; }
@@ -1086,7 +1092,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
         x.ss = __ldcg(&src[i].ss); x.seg = __ldcg(&src[i].seg);
         c.cand[i] = x;
       }
-      __syncthreads();
+      cta_sync();
     }
     const uint32_t nc = s.ncand;
     if (tid == 0) {
@@ -1100,7 +1106,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
         for (int k = 9; k < NSEG; ++k) st.blocks_scored_struct += s.segtot[k];
       }
     }
-    __syncthreads();
+    cta_sync();
     // The victims are the m smallest candidates by (k0, k1, k2): EF keys (ntok, id) are
     // < 2^63 <= obits(P), so Stage 1 precedes Stage 2 by construction.
     c0 = s.cnt[0];
@@ -1109,7 +1115,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
     uint64_t Kth = ~0ull;
     if (nc >= m) {
       if (tid == 0) s.target[0] = m;
-      __syncthreads();
+      cta_sync();
       radix_select(c.cand, nc, false, 1u, s);
       Kth = s.pfx[0];
     }
@@ -1133,13 +1139,13 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
       }
       if (!ok) atomicOr(&s.fail, 1u << gsg);
     }
-    __syncthreads();
+    cta_sync();
     const uint32_t fail = s.fail;
     if (tid == 0) st.tph[3] += gtimer() - t0;
     if (fail == 0) break;
     if (tid < 10 && ((fail >> tid) & 1u)) st.select_fail_seg[tid]++;
     if (tid < NSEG && (((fail >> tid) & 1u) || attempt >= 1)) st.thr[tid] = ~0ull;
-    __syncthreads();
+    cta_sync();
   }
   const uint32_t nc = s.ncand;
   uint64_t Kth = nc >= m ? s.pfx[0] : ~0ull;
@@ -1149,25 +1155,27 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
   if (nc >= m) {
     const uint32_t nless = s.below[0];
     if (tid == 0) s.nv = 0;
-    __syncthreads();
+    cta_sync();
     for (uint32_t i = tid; i < nc; i += NT)          // size of the k0 tie group
       if (c.cand[i].k0 == Kth) atomicAdd(&s.nv, 1u);
-    __syncthreads();
-    if (nless + s.nv > m) {                          // the tie group straddles rank m
+    cta_sync();
+    const bool straddle = nless + s.nv > m;          // block-uniform decision...
+    cta_sync();                                 // ...taken before s.nv is reused
+    if (straddle) {                                  // the tie group straddles rank m
       if (tid == 0) s.target[0] = m - nless;
-      __syncthreads();
+      cta_sync();
       radix_select(c.cand, nc, false, 1u, s, 1, Kth);
       K1th = s.pfx[0];
       const uint32_t nless1 = s.below[0];
       if (tid == 0) s.target[0] = m - nless - nless1;
-      __syncthreads();
+      cta_sync();
       radix_select(c.cand, nc, false, 1u, s, 2, Kth, K1th);
       K2th = s.pfx[0];
     }
   }
   if (tid == 0) s.nv = 0;
   if (tid < 16) s.kmin[tid] = ~0ull;
-  __syncthreads();
+  cta_sync();
   for (uint32_t i0 = 0; i0 < nc; i0 += NT) {
     const uint32_t i = i0 + tid;
     if (i < nc) {
@@ -1188,7 +1196,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
     const uint32_t pos = basep + __popc(bal & ((1u << lane) - 1u));
     if (take && pos < VCAP) c.vbuf[pos] = c.cand[i];
   }
-  __syncthreads();
+  cta_sync();
   const uint32_t nv = min(s.nv, (uint32_t)VCAP);
   {
     int N = 32;
@@ -1197,12 +1205,12 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
       c.vbuf[i].k0 = ~0ull; c.vbuf[i].k1 = ~0ull; c.vbuf[i].k2 = ~0u; c.vbuf[i].ss = 15u << 28;
       c.vbuf[i].seg = 15;
     }
-    __syncthreads();
+    cta_sync();
     sort_cands(c.vbuf, N);       // small: the m victims in (k0, last, id) order
   }
   // ---- carry thresholds: trim segments holding far more candidates than they use
   for (uint32_t v = tid; v < m; v += NT) atomicAdd(&s.used[c.vbuf[v].seg], 1u);
-  __syncthreads();
+  cta_sync();
   // small private pools (rescans are cheap) trim hard; large pools trim lazily
   const uint32_t trim_at = 8u, trim_to = 4u;
   uint32_t shrink = 0;
@@ -1212,10 +1220,10 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
   }
   if (shrink) {
     if (tid < NSEG) s.target[tid] = trim_to * (3 * s.used[tid] + SLACK);
-    __syncthreads();
+    cta_sync();
     radix_select(c.cand, nc, true, shrink, s);
     if (tid < NSEG && ((shrink >> tid) & 1u)) st.thr[tid] = s.pfx[tid];
-    __syncthreads();
+    cta_sync();
   }
   // ---- grow a segment's threshold before its reserve runs dry (avoids refills): double
   //      the key distance from the smallest candidate (keys: EF (ntok,id); class last;
@@ -1242,9 +1250,9 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
       st.thr[g] = Tn;
     }
   }
-  __syncthreads();
+  cta_sync();
   for (uint32_t v = tid; v < m; v += NT) c.cand[v] = c.vbuf[v];
-  __syncthreads();
+  cta_sync();
 }
 
 // Too many candidates for the leader's smem: choose, per over-full segment, the exact key
@@ -1263,7 +1271,7 @@ __device__ void narrow(Ctx& c, uint32_t e, uint32_t mp) {
     s.pmask[tid] = 0;
     s.below[tid] = 0;
   }
-  __syncthreads();
+  cta_sync();
   uint32_t active = 0;
   for (int k = 0; k < NSEG; ++k) if (s.cnt[k] > s.target[k]) active |= 1u << k;
   for (int shift = 56; shift >= 0 && active; shift -= 8) {
@@ -1273,7 +1281,7 @@ __device__ void narrow(Ctx& c, uint32_t e, uint32_t mp) {
       for (int k = 0; k < NSEG; ++k) { g->pfx[k] = s.pfx[k]; g->pmask[k] = s.pmask[k]; }
     }
     for (int i = tid; i < NSEG * 256; i += NT) g->hist[i] = 0;
-    __syncthreads();
+    cta_sync();
     issue(c, CMD_HIST);
     // one warp per active segment: find the digit holding rank target
     for (int k = wid; k < NSEG; k += NW) {
@@ -1303,14 +1311,14 @@ __device__ void narrow(Ctx& c, uint32_t e, uint32_t mp) {
         s.pmask[k] |= 0xFFull << shift;
       }
     }
-    __syncthreads();
+    cta_sync();
   }
   if (tid == 0) {
     for (int k = 0; k < NSEG; ++k) if ((active >> k) & 1u) st.thr[k] = s.pfx[k];
     for (int k = 0; k < 16; ++k) { g->thr[k] = st.thr[k]; g->selcnt[k] = 0; }
     g->nsel = 0;
   }
-  __syncthreads();
+  cta_sync();
   issue(c, CMD_COMPACT);
   if (tid < 16) s.cnt[tid] = __ldcg(&g->selcnt[tid]);
   if (tid == 0) {
@@ -1321,7 +1329,7 @@ __device__ void narrow(Ctx& c, uint32_t e, uint32_t mp) {
       s.ncand = CAND_MAX;
     }
   }
-  __syncthreads();
+  cta_sync();
 }
 
 // Apply a chunk of m victims (cand[0..m) in eviction order): SURVEY c.2 O11 steps 1-4.
@@ -1359,7 +1367,7 @@ __device__ void apply_chunk(Ctx& c, uint32_t m, uint32_t* vids_out) {
       d.ghash[gb + p] = H;
       d.gtau[gb + p] = (uint8_t)tau;
     }
-    __syncthreads();
+    cta_sync();
     // phase 2: ghost push (recently_evicted[hash] = tau), free the slot
     for (uint32_t v = threadIdx.x; v < mb; v += NT) {
       const uint32_t sl = c.cand[v0 + v].ss & SLOT_MASK;
@@ -1370,7 +1378,7 @@ __device__ void apply_chunk(Ctx& c, uint32_t m, uint32_t* vids_out) {
       d.gtslot[gb + p] = tbl_insert(gkey, gval, d.gmask, H, p, &st.gtbl_used);
       d.freestk[c.base + st.free_top + v0 + v] = sl;
     }
-    __syncthreads();
+    cta_sync();
     if (threadIdx.x == 0) {
       st.free_top += mb;
       st.live -= mb;
@@ -1378,7 +1386,7 @@ __device__ void apply_chunk(Ctx& c, uint32_t m, uint32_t* vids_out) {
       st.E += mb;
       st.evictions += mb;
     }
-    __syncthreads();
+    cta_sync();
   }
 }
 
@@ -1411,12 +1419,12 @@ __device__ void load_state(Ctx& c) {
   const uint32_t* src = reinterpret_cast<const uint32_t*>(d.st + c.r);
   uint32_t* dst = reinterpret_cast<uint32_t*>(&c.s->st);
   for (int i = threadIdx.x; i < (int)(sizeof(RState) / 4); i += NT) dst[i] = __ldcg(src + i);
-  __syncthreads();
+  cta_sync();
   recompute_cw(*c.s);
-  __syncthreads();
+  cta_sync();
 }
 __device__ void store_state(Ctx& c) {
-  __syncthreads();
+  cta_sync();
   const Dev& d = *c.d;
   uint32_t* dst = reinterpret_cast<uint32_t*>(d.st + c.r);
   const uint32_t* src = reinterpret_cast<const uint32_t*>(&c.s->st);
@@ -1442,7 +1450,7 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
       st.err = L < 1 ? (uint32_t)(-SAE_E_INVAL) : (uint32_t)(-SAE_E_TIME);
       raise_err(d, L < 1 ? SAE_E_INVAL : SAE_E_TIME);
     }
-    __syncthreads();
+    cta_sync();
     return false;
   }
   const uint32_t B = d.B;
@@ -1452,7 +1460,7 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
   const bool mt = fl & 1, ag = fl & 2, cid = fl & 4;
   const bool untempl = !mt && spb == 0;             // A31
   const uint32_t omax = np > 1 ? np - 1 : 1;         // A8
-  __syncthreads();
+  cta_sync();
   if (threadIdx.x == 0) {
     st.now = now;
     st.has_now = 1;
@@ -1461,7 +1469,7 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
     s.npin = 0;
     s.matched = 0;
   }
-  __syncthreads();
+  cta_sync();
   const uint32_t stamp = (uint32_t)st.round;
   uint64_t tA = gtimer();
   // ---- O4/O5 classify + probe (Alg.1 Classify P:550-564; strict prefix P:158)
@@ -1474,7 +1482,7 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
     if (sl < 0) atomicMin(&s.h, (int32_t)j);
     else atomicAdd(&s.npin, 1u);
   }
-  __syncthreads();
+  cta_sync();
   const uint32_t h = (uint32_t)s.h;
   // ---- O6-O9 stats, touch, orphans, miss-after-evict; ordered ranks by block scans
   uint32_t new_base = 0;
@@ -1534,14 +1542,14 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
     if (fa) d.iv[((uint64_t)c.r * 2 + 1) * RMAX + (st.iv_head[1] + ra) % RMAX] = lnv;
     if (valid) b.nrank[bo + j] = fn ? (int32_t)(new_base + rn) : -1;
     new_base += s.tot[2];
-    __syncthreads();
+    cta_sync();
     if (threadIdx.x == 0) {
       for (int q = 0; q < 2; ++q) {
         st.iv_head[q] = (st.iv_head[q] + s.tot[q]) % RMAX;
         st.iv_len[q] = min(d.iv_ring, st.iv_len[q] + s.tot[q]);
       }
     }
-    __syncthreads();
+    cta_sync();
   }
   // ---- O10 admission size (A11)
   if (threadIdx.x == 0) {
@@ -1555,7 +1563,7 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
     if (k > 0) st.eviction_rounds++;
     if (b.boff[i] + k > b.vcap) { st.err = (uint32_t)(-SAE_E_OVERFLOW); raise_err(d, SAE_E_OVERFLOW); }
   }
-  __syncthreads();
+  cta_sync();
   if (st.err) return false;
   const uint64_t k = s.k, admit = s.admit;
   if (threadIdx.x == 0) st.tph[0] += gtimer() - tA;
@@ -1572,7 +1580,7 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
     st.err = (uint32_t)(-SAE_E_OVERFLOW);
     raise_err(d, SAE_E_OVERFLOW);
   }
-  __syncthreads();
+  cta_sync();
   if (st.err) return false;
   for (uint32_t j = threadIdx.x; j < n; j += NT) {
     const int32_t rk = b.nrank[bo + j];
@@ -1591,7 +1599,7 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
     d.blr[gi] = lr_of(j, omax);
     tbl_insert(tkey, tval, d.tmask, H, sl, &st.tbl_used);
   }
-  __syncthreads();
+  cta_sync();
   if (threadIdx.x == 0) {
     st.free_top -= (uint32_t)admit;
     st.live += (uint32_t)admit;
@@ -1607,7 +1615,7 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
     st.hit_tokens += s.matched;
     st.prompt_tokens += L;
   }
-  __syncthreads();
+  cta_sync();
   if (threadIdx.x == 0) { const uint64_t t1 = gtimer(); st.tph[6] += t1 - tA; tA = t1; }
   if (st.tbl_used > (d.tmask + 1) / 4 * 3) {
     rebuild_table(c);
@@ -1670,9 +1678,9 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_evict(Dev d, uint32_t
     if (st.has_now && now < st.now) {
       if (threadIdx.x == 0) { st.err = (uint32_t)(-SAE_E_TIME); raise_err(d, SAE_E_TIME); }
     } else {
-      __syncthreads();
+      cta_sync();
       if (threadIdx.x == 0) { st.now = now; st.has_now = 1; st.round++; }
-      __syncthreads();
+      cta_sync();
       const uint32_t kk = min(k, st.live);
       if (kk > 0) {
         if (threadIdx.x == 0) st.eviction_rounds++;

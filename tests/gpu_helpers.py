@@ -66,8 +66,8 @@ def assert_stats_equal(g, o):
                                                             list(getattr(o, k)))
 
 
-def compare_replay(tr, pol, lo=0, hi=None, check_hashes=True, ctas=0):
-    cache, b, out = gpu_replay(tr, pol, lo=lo, hi=hi, ctas=ctas)
+def compare_replay(tr, pol, lo=0, hi=None, check_hashes=True, ctas=0, traj=1 << 16):
+    cache, b, out = gpu_replay(tr, pol, lo=lo, hi=hi, ctas=ctas, traj=traj)
     R = oracle.Replica(pol)
     ref = R.replay(tr, lo, hi)
     n = (tr["n"] if hi is None else hi) - lo

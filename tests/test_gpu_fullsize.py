@@ -46,3 +46,50 @@ def test_c4_full_pool_first_eviction_rounds():
     assert st.resident == pol["capacity"]
     assert st.evictions == int(o4[:, 3].sum())
     assert sum(st.resident_by_queue) == st.resident
+
+
+def test_c2_full_trace_bit_exact():
+    """C2 at its full size (100K requests, C=2304), one replica: every output identical."""
+    from tests.gpu_helpers import compare_replay
+    tr = T.make("c2")
+    compare_replay(tr, C.policy_config(2304), check_hashes=True, traj=1 << 17)
+
+
+def test_c5_full_config_sampled_replicas():
+    """C5 exactly as bench.py runs it on one GPU (1024 replicas x 10K requests, C=2304,
+    the 256-thread two-CTAs-per-SM variant); sampled replicas replayed by the oracle."""
+    from paper_2605_18825_b200 import replicas as RP
+    n = 10_000
+    traces = []
+    for sd in range(32):
+        t = T.generate(C.get("c5", n_requests=n), seed=0x5AEC1000 + sd)
+        T.materialize(t)
+        traces.append(t)
+    R = 1024
+    pol = C.policy_config(2304)
+    cache = S.SaeCache(2304, n_replicas=R, policy=pol)
+    for r in range(R):
+        cache.set_params(r, C.c5_point_params(RP.layout(r)[1]))
+    batch = T.replicate(traces, [RP.layout(r)[0] for r in range(R)])
+    out = cache.admit_batch(S.batch_to_torch(batch))
+    torch.cuda.synchronize()
+    o4, _ = unpack(out, batch["n"])
+    vo = out["victim_off"].cpu().numpy()
+    vids = u32(out["victim_ids"])
+    for r in (0, 31, 32, 517, 1023):
+        sd, pt = RP.layout(r)
+        p = dict(pol)
+        p["params"] = C.c5_point_params(pt)
+        ref = oracle.Replica(p).replay(traces[sd], want_hashes=False)
+        off = r * n
+        assert np.array_equal(o4[off:off + n], ref.out4), r
+        got = np.concatenate([vids[vo[off + i]:vo[off + i] + o4[off + i, 3]] for i in range(n)])
+        assert np.array_equal(got, ref.victims), r
+
+
+def test_c3_pool_multi_cta_first_rounds():
+    """C3's 16384-block pool (multi-CTA group, as configured by default) on the C3 trace's
+    first 3000 requests (the pool fills after ~300)."""
+    from tests.gpu_helpers import compare_replay
+    tr = T.make("c3", n_requests=3000)
+    compare_replay(tr, C.policy_config(16384), check_hashes=True)
