@@ -410,7 +410,7 @@ def run_ours(args, wl, ws, rank, local):
             dist.destroy_process_group()
         return
     hbm, src = peaks()
-    alg_bytes = 14.0 * scored + 4.0 * scored_struct
+    alg_bytes = 12.0 * scored                            # meta u32 + key u64
     # device-timer view of the fused score/select scan (multi-CTA groups: worker 1's
     # streamed slice; single-CTA replicas: the leader's scan phase), per pass
     passes = d("select_passes")
@@ -420,7 +420,7 @@ def run_ours(args, wl, ws, rank, local):
     phase_info = {"passes_per_request": passes / max(req, 1),
                   "required_passes_per_request": (d("eviction_rounds") + d("learner_firings")) / max(req, 1),
                   "scan_ns_per_pass": scan_ns / max(passes / max(R, 1), 1),
-                  "bytes_streamed_per_pass": (20.0 * pol["capacity"]) if ph11 > 0 else None,
+                  "bytes_streamed_per_pass": (12.0 * pol["capacity"]) if ph11 > 0 else None,
                   "phase_ms_per_step": [round((b - a) / 1e6 / K, 3) for a, b in
                                         zip(st0[0].phase_ns, st1[0].phase_ns)]}
     if ph11 > 0:

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define SAE_ABI_VERSION 1u
+#define SAE_ABI_VERSION 2u
 
 typedef struct sae_ctx sae_ctx;
 typedef int sae_status;
@@ -165,8 +165,9 @@ typedef struct {
   uint64_t select_passes, select_cands, select_big, select_fail_seg[10];
   /* device time (ns, globaltimer) spent by the replica leader per phase: probe+touch,
    * scan passes, narrowing, sort+check, apply, learn, insert+outputs, table rebuild, and for
-   * multi-CTA groups: command start barrier, leader's own partition, end barrier, spare */
-  uint64_t phase_ns[12];
+   * multi-CTA groups: command post, leader's own partition, wait for the workers, worker 1's
+   * scan time; [12] victim staging + tie-break + victim sort + threshold carry; [13..15] spare */
+  uint64_t phase_ns[16];
   uint64_t select_narrow, select_raw;   /* narrowings (candidate sets > 4096) and raw candidates */
   sae_params params;
 } sae_replica_stats;

@@ -152,8 +152,9 @@ struct Smem {
   uint32_t below[16], target[16];
   unsigned long long kmin[16];
   uint32_t nv, nw;          // nw: this CTA's candidates awaiting finalize_key (global mode)
+  uint32_t cseq, wcmd;      // leader: commands posted this launch; worker: command to run
   uint32_t rhist[NSEG * 256];   // radix-select histograms (one 256-bin digit per segment)
-  __align__(8) uint64_t mbar[8];  // bulk-copy stage barriers (worker scan pipeline)
+  __align__(8) uint64_t mbar[16];  // bulk-copy stage barriers (worker scan pipeline): full[8], empty[8]
   uint64_t wthr[16], wpfx[16], wpmask[16];   // worker copies of the leader's command parameters
   double wcw[15], wmu[2], wsg[2];
 };
@@ -189,25 +190,22 @@ __device__ __forceinline__ void part_range(uint64_t n, uint32_t rank, uint32_t G
 }
 
 // ---------------------------------------------------------------------------
-// Group barrier over the GP CTAs of one replica (co-resident by cooperative launch).
+// Group command channel (GP CTAs of one replica, co-resident by cooperative launch).
+// The leader publishes command number seq of this launch as one 64-bit word
+// (epoch:24 | seq:32 | cmd:8) with a release store after its parameters; workers poll it
+// with acquire loads, run their partition and count themselves done on a cumulative
+// counter the leader waits on.  One hop each way (no all-to-all barrier).
 // ---------------------------------------------------------------------------
-__device__ void group_bar(Ctx& c) {
-  cta_sync();
-  if (threadIdx.x == 0) {
-    GroupCtl* g = c.ctl;
-    volatile unsigned* genp = &g->bar_gen;
-    const unsigned gen = *genp;
-    __threadfence();
-    if (atomicAdd(&g->bar_count, 1u) == c.GP - 1) {
-      atomicExch(&g->bar_count, 0u);
-      __threadfence();
-      atomicAdd(&g->bar_gen, 1u);
-    } else {
-      while (*genp == gen) __nanosleep(64);
-    }
-    __threadfence();
-  }
-  cta_sync();
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long cmd_tag(uint32_t epoch, uint32_t seq) {
+  return ((unsigned long long)(epoch & 0xFFFFFFu) << 32) | seq;
 }
 
 // Parameters of a scan, from the leader's smem (leader) or the control block (workers).
@@ -240,32 +238,31 @@ __device__ __forceinline__ void pk_add(uint64_t (&pk)[4], uint32_t seg) {
 // multi-turn classes (key: last); conservative for STRUCT (a lower bound of P against the
 // threshold).  The exact Eq.(1)-(3) scores of the (few) candidates are computed afterwards
 // by finalize_keys, outside the streaming loop.
-__device__ __forceinline__ bool score_one(const Dev& d, const ScanP& P, uint32_t meta, uint32_t id,
-                                          double last, uint64_t gi, uint32_t sl, Cand& x,
-                                          uint32_t& seg) {
+__device__ __forceinline__ bool score_one(const ScanP& P, uint32_t meta, uint64_t key, uint32_t sl,
+                                          Cand& x) {
   const uint32_t q = meta_q(meta), tau = meta_tau(meta);
-  seg = seg_of(q, tau);
+  const uint32_t seg = seg_of(q, tau);
   bool take;
-  x.k2 = id;
-  x.k1 = obits(last);
-  if (q == Q_EF) {                      // Stage 1 key (num_tokens, id), P:507
-    x.k0 = ((uint64_t)meta_ntok(meta) << 32) | id;
-    x.k1 = 0;
-    x.k2 = 0;
-    take = x.k0 <= P.thr[seg];
-  } else if (q == Q_STRUCT) {           // prefilter: lower bound of Eq.(2)+(3) vs threshold
-    double dt = __dsub_rn(P.now, last);
-    if (dt < P.dt_eps) dt = P.dt_eps;
-    const double T = P.thr[seg] == ~0ull ? __longlong_as_double(0x7ff0000000000000ll) : from_obits(P.thr[seg]);
-    take = __dmul_rn(P.cw[10 + tau], p_struct_lo(__ldcg(d.blr + gi), (float)P.gamma)) <=
-           __dmul_rn(__dmul_rn(T, dt), 1.0 + 0x1p-40);
-    x.k0 = 0;
-  } else {                              // multi-turn class (queue, tau): key last
-    take = x.k1 <= P.thr[seg];
-    x.k0 = 0;
-  }
   x.ss = sl | ((q == Q_EF ? 0u : 1u) << 28);
   x.seg = seg;
+  x.k2 = 0;                             // id of a scored candidate: loaded by finalize_key
+  if (q == Q_EF) {                      // Stage 1 key (num_tokens, id), P:507
+    x.k0 = key;
+    x.k1 = 0;
+    take = key <= P.thr[0];
+  } else if (q == Q_STRUCT) {           // prefilter: lower bound of Eq.(2)+(3) vs threshold
+    x.k0 = 0;
+    x.k1 = key;
+    double dt = __dsub_rn(P.now, from_obits(key));
+    if (dt < P.dt_eps) dt = P.dt_eps;
+    const double T = P.thr[seg] == ~0ull ? __longlong_as_double(0x7ff0000000000000ll) : from_obits(P.thr[seg]);
+    take = __dmul_rn(P.cw[10 + tau], p_struct_lo(meta_lrq(meta), (float)P.gamma)) <=
+           __dmul_rn(__dmul_rn(T, dt), 1.0 + 0x1p-40);
+  } else {                              // multi-turn class (queue, tau): key obits(last)
+    x.k0 = 0;
+    x.k1 = key;
+    take = key <= P.thr[seg];
+  }
   return take;
 }
 
@@ -273,6 +270,7 @@ __device__ __forceinline__ bool score_one(const Dev& d, const ScanP& P, uint32_t
 // then Eq.(3) P = ((alpha_q * w_tau) * p) / dt, fixed op order (SURVEY c.4).
 __device__ __forceinline__ void finalize_key(const Dev& d, uint64_t base, const ScanP& P, Cand& x) {
   if (x.seg == 0 || x.seg >= 16) return;
+  x.k2 = __ldcg(d.bid + base + (x.ss & SLOT_MASK));
   const double last = from_obits(x.k1);
   double dt = __dsub_rn(P.now, last);
   if (dt < P.dt_eps) dt = P.dt_eps;
@@ -300,6 +298,7 @@ __device__ __forceinline__ void note_cand(Ctx& c, const ScanP& P, Cand* gdst, ui
     Cand x = gdst[pos];
     finalize_key(*c.d, c.base, P, x);
     gdst[pos].k0 = x.k0;
+    gdst[pos].k2 = x.k2;
   }
 }
 __device__ void finalize_noted(Ctx& c, const ScanP& P, Cand* gdst) {
@@ -309,6 +308,7 @@ __device__ void finalize_noted(Ctx& c, const ScanP& P, Cand* gdst) {
     Cand x = gdst[pos];
     finalize_key(*c.d, c.base, P, x);
     gdst[pos].k0 = x.k0;
+    gdst[pos].k2 = x.k2;
   }
 }
 
@@ -321,53 +321,47 @@ __device__ void scan_range(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P) {
   uint64_t tot[4] = {0, 0, 0, 0}, cnt[4] = {0, 0, 0, 0};
   const bool vec = ((c.base + lo) & 3u) == 0;
   // software pipeline: the next step's 4 slots are loaded before this step is scored
-  uint32_t mt[4], idv[4];
-  double lt[4];
-  auto load = [&](uint64_t s0, uint32_t (&m)[4], uint32_t (&iv)[4], double (&l)[4]) {
+  uint32_t mt[4];
+  uint64_t kt[4];
+  auto load = [&](uint64_t s0, uint32_t (&m)[4], uint64_t (&k)[4]) {
     if (vec && s0 + 3 < hi && !gm) {   // single-CTA replica: the SoA is private -> L1-cached loads
       const uint4 m4 = *reinterpret_cast<const uint4*>(d.bmeta + c.base + s0);
-      const uint4 i4 = *reinterpret_cast<const uint4*>(d.bid + c.base + s0);
-      const double2 l0 = *reinterpret_cast<const double2*>(d.blast + c.base + s0);
-      const double2 l1 = *reinterpret_cast<const double2*>(d.blast + c.base + s0 + 2);
+      const ulonglong2 k0 = *reinterpret_cast<const ulonglong2*>(d.bkey + c.base + s0);
+      const ulonglong2 k1 = *reinterpret_cast<const ulonglong2*>(d.bkey + c.base + s0 + 2);
       m[0] = m4.x; m[1] = m4.y; m[2] = m4.z; m[3] = m4.w;
-      iv[0] = i4.x; iv[1] = i4.y; iv[2] = i4.z; iv[3] = i4.w;
-      l[0] = l0.x; l[1] = l0.y; l[2] = l1.x; l[3] = l1.y;
+      k[0] = k0.x; k[1] = k0.y; k[2] = k1.x; k[3] = k1.y;
     } else if (vec && s0 + 3 < hi) {
       const uint4 m4 = __ldcg(reinterpret_cast<const uint4*>(d.bmeta + c.base + s0));
-      const uint4 i4 = __ldcg(reinterpret_cast<const uint4*>(d.bid + c.base + s0));
-      const double2 l0 = __ldcg(reinterpret_cast<const double2*>(d.blast + c.base + s0));
-      const double2 l1 = __ldcg(reinterpret_cast<const double2*>(d.blast + c.base + s0 + 2));
+      const ulonglong2 k0 = __ldcg(reinterpret_cast<const ulonglong2*>(d.bkey + c.base + s0));
+      const ulonglong2 k1 = __ldcg(reinterpret_cast<const ulonglong2*>(d.bkey + c.base + s0 + 2));
       m[0] = m4.x; m[1] = m4.y; m[2] = m4.z; m[3] = m4.w;
-      iv[0] = i4.x; iv[1] = i4.y; iv[2] = i4.z; iv[3] = i4.w;
-      l[0] = l0.x; l[1] = l0.y; l[2] = l1.x; l[3] = l1.y;
+      k[0] = k0.x; k[1] = k0.y; k[2] = k1.x; k[3] = k1.y;
     } else {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const bool ok = s0 + u < hi;
         m[u] = ok ? __ldcg(d.bmeta + c.base + s0 + u) : 0u;
-        iv[u] = ok ? __ldcg(d.bid + c.base + s0 + u) : 0u;
-        l[u] = ok ? __ldcg(d.blast + c.base + s0 + u) : 0.0;
+        k[u] = ok ? __ldcg(d.bkey + c.base + s0 + u) : 0ull;
       }
     }
   };
   uint64_t s0 = lo + 4ull * tid;
-  if (s0 < hi) load(s0, mt, idv, lt);
+  if (s0 < hi) load(s0, mt, kt);
   else { mt[0] = mt[1] = mt[2] = mt[3] = 0; }
   for (uint64_t i0 = lo; i0 < hi; i0 += 4 * NT) {
     const uint64_t sn = s0 + 4ull * NT;
-    uint32_t mn[4] = {0, 0, 0, 0}, in_[4] = {0, 0, 0, 0};
-    double ln_[4] = {0.0, 0.0, 0.0, 0.0};
-    if (sn < hi) load(sn, mn, in_, ln_);
+    uint32_t mn[4] = {0, 0, 0, 0};
+    uint64_t kn[4] = {0, 0, 0, 0};
+    if (sn < hi) load(sn, mn, kn);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       bool take = false;
       Cand x;
       const uint32_t meta = s0 < hi ? mt[u] : 0u;
       if ((meta & (M_LIVE | M_PIN)) == M_LIVE) {
-        uint32_t seg;
-        take = score_one(d, P, meta, idv[u], lt[u], c.base + s0 + u, (uint32_t)(s0 + u), x, seg);
-        pk_add(tot, seg);
-        if (take) pk_add(cnt, seg);
+        take = score_one(P, meta, kt[u], (uint32_t)(s0 + u), x);
+        pk_add(tot, x.seg);
+        if (take) pk_add(cnt, x.seg);
       }
       if (gm) {
         const uint32_t bal = __ballot_sync(~0u, take);
@@ -386,7 +380,7 @@ __device__ void scan_range(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P) {
       }
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) { mt[u] = mn[u]; idv[u] = in_[u]; lt[u] = ln_[u]; }
+    for (int u = 0; u < 4; ++u) { mt[u] = mn[u]; kt[u] = kn[u]; }
     s0 = sn;
   }
   cta_sync();
@@ -441,12 +435,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// Worker scan over [lo, hi) (lo a multiple of 4, replica base 16-byte aligned): the SoA
-// columns (meta u32, id u32, last f64, p_struct f64) are streamed tile by tile into
-// shared memory by bulk asynchronous copies, BSTAGES tiles in flight, and scored from
-// shared memory.  Same outputs as scan_range.
-constexpr int BTILE = 1024, BSTAGES = 4;
-constexpr uint32_t BTILE_BYTES = BTILE * (4 + 4 + 8 + 4);
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Worker scan over [lo, hi) (lo a multiple of 4, replica base 16-byte aligned): the two
+// scan columns (meta u32, key u64: 12 B per slot) are streamed tile by tile into shared
+// memory by bulk asynchronous copies, BSTAGES tiles in flight, and scored from shared
+// memory.  Stage reuse is tracked per stage by a "full" mbarrier (transaction bytes) and an
+// "empty" mbarrier (one arrival per warp), so warps never wait for each other: only the
+// producer thread (thread 0) waits for a stage to drain before refilling it.  Same outputs
+// as scan_range.
+constexpr int BTILE = 2048;
+constexpr uint32_t BTILE_BYTES = BTILE * (4 + 8);
+constexpr int BSTAGES = (int)((CAND_MAX * sizeof(Cand)) / BTILE_BYTES) < 6
+                            ? (int)((CAND_MAX * sizeof(Cand)) / BTILE_BYTES) : 6;
+static_assert(BSTAGES >= 2, "bulk scan needs two stages");
 __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P) {
   const Dev& d = *c.d;
   Smem& s = *c.s;
@@ -455,35 +459,25 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
   unsigned char* buf = reinterpret_cast<unsigned char*>(c.cand);
   uint64_t tot[4] = {0, 0, 0, 0}, cnt[4] = {0, 0, 0, 0};
   const uint64_t ntiles = (hi - lo + BTILE - 1) / BTILE;
-  auto stage_ptrs = [&](int st, uint32_t*& m, uint32_t*& iv, double*& l, float*& lr) {
-    unsigned char* b = buf + (size_t)st * BTILE_BYTES;
-    m = reinterpret_cast<uint32_t*>(b);
-    iv = reinterpret_cast<uint32_t*>(b + BTILE * 4);
-    l = reinterpret_cast<double*>(b + BTILE * 8);
-    lr = reinterpret_cast<float*>(b + BTILE * 16);
-  };
+  uint64_t* full = &s.mbar[0];
+  uint64_t* empty = &s.mbar[8];
   auto issue_tile = [&](uint64_t t) {
     const int st = (int)(t % BSTAGES);
     const uint64_t t0 = lo + t * BTILE;
     const uint32_t n = (uint32_t)min((uint64_t)BTILE, hi - t0);
     const uint32_t n4 = (n + 3) & ~3u;                 // 16-byte multiple (SoA is padded)
-    uint32_t *m, *iv;
-    double* l;
-    float* lrs;
-    stage_ptrs(st, m, iv, l, lrs);
-    mbar_expect_tx(&s.mbar[st], n4 * 20u);
-    bulk_g2s(m, d.bmeta + c.base + t0, n4 * 4u, &s.mbar[st]);
-    bulk_g2s(iv, d.bid + c.base + t0, n4 * 4u, &s.mbar[st]);
-    bulk_g2s(l, d.blast + c.base + t0, n4 * 8u, &s.mbar[st]);
-    bulk_g2s(lrs, d.blr + c.base + t0, n4 * 4u, &s.mbar[st]);
+    unsigned char* b = buf + (size_t)st * BTILE_BYTES;
+    mbar_expect_tx(&full[st], n4 * 12u);
+    bulk_g2s(b, d.bmeta + c.base + t0, n4 * 4u, &full[st]);
+    bulk_g2s(b + BTILE * 4, d.bkey + c.base + t0, n4 * 8u, &full[st]);
   };
   if (tid == 0) {
-    for (int st = 0; st < BSTAGES; ++st) mbar_init(&s.mbar[st], 1);
+    for (int st = 0; st < BSTAGES; ++st) { mbar_init(&full[st], 1); mbar_init(&empty[st], NW); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     for (uint64_t t = 0; t < ntiles && t < (uint64_t)BSTAGES; ++t) issue_tile(t);
   }
-  cta_sync();
-  // thresholds as doubles (multi-turn: last; STRUCT: P) for the division-free prefilter
+  // thresholds as doubles (STRUCT: P) for the division-free prefilter
   double* thrD = reinterpret_cast<double*>(&s.wpfx[0]);   // 16 doubles of scratch
   if (tid < NSEG) {
     const uint64_t T = P.thr[tid];
@@ -494,71 +488,79 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
   const float gamf = (float)P.gamma;
   for (uint64_t t = 0; t < ntiles; ++t) {
     const int st = (int)(t % BSTAGES);
-    mbar_wait(&s.mbar[st], (uint32_t)((t / BSTAGES) & 1));
-    uint32_t *m, *iv;
-    double* l;
-    float* lrs;
-    stage_ptrs(st, m, iv, l, lrs);
+    const uint32_t par = (uint32_t)((t / BSTAGES) & 1);
+    mbar_wait(&full[st], par);
+    const unsigned char* b = buf + (size_t)st * BTILE_BYTES;
+    const uint32_t* m = reinterpret_cast<const uint32_t*>(b);
+    const uint64_t* kk = reinterpret_cast<const uint64_t*>(b + BTILE * 4);
     const uint64_t t0 = lo + t * BTILE;
     const uint32_t n = (uint32_t)min((uint64_t)BTILE, hi - t0);
+    uint32_t mv[BTILE / NT];
+    uint64_t kv[BTILE / NT];
 #pragma unroll
     for (int u = 0; u < BTILE / NT; ++u) {
       const uint32_t k = (uint32_t)(u * NT + tid);
+      mv[u] = k < n ? m[k] : 0u;
+      kv[u] = kk[k];
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);   // this warp is done reading stage st
+#pragma unroll
+    for (int u = 0; u < BTILE / NT; ++u) {
+      const uint32_t k = (uint32_t)(u * NT + tid);
+      const uint32_t meta = mv[u];
+      const uint64_t key = kv[u];
       bool take = false;
-      const uint32_t meta = k < n ? m[k] : 0u;
-      uint32_t q = 0, tau = 0, seg = 0;
+      uint32_t q = 0, seg = 0;
       if ((meta & (M_LIVE | M_PIN)) == M_LIVE) {
         q = meta_q(meta);
-        tau = meta_tau(meta);
+        const uint32_t tau = meta_tau(meta);
         seg = seg_of(q, tau);
         pk_add(tot, seg);
-        if (q == Q_EF) {
-          take = ((((uint64_t)meta_ntok(meta)) << 32) | iv[k]) <= P.thr[0];
-        } else if (q == Q_STRUCT) {
+        if (q == Q_STRUCT) {
           // prefilter (a superset of P <= T) with a lower bound of p; exact P below
-          double dt = __dsub_rn(P.now, l[k]);
+          double dt = __dsub_rn(P.now, from_obits(key));
           if (dt < P.dt_eps) dt = P.dt_eps;
-          take = __dmul_rn(P.cw[10 + tau], p_struct_lo(lrs[k], gamf)) <=
+          take = __dmul_rn(P.cw[10 + tau], p_struct_lo(meta_lrq(meta), gamf)) <=
                  __dmul_rn(__dmul_rn(thrD[seg], dt), inflate);
-        } else {
-          take = l[k] <= thrD[seg];
+        } else {                          // EF (ntok, id) / multi-turn obits(last)
+          take = key <= P.thr[seg];
         }
-      }
-      Cand x;
-      if (take) {                         // raw record; exact scores after streaming
-        const uint32_t id = iv[k];
-        x.ss = (uint32_t)(t0 + k) | ((q == Q_EF ? 0u : 1u) << 28);
-        x.seg = seg;
-        if (q == Q_EF) {
-          x.k0 = ((uint64_t)meta_ntok(meta) << 32) | id;
-          x.k1 = 0;
-          x.k2 = 0;
-        } else {
-          x.k0 = 0;
-          x.k1 = obits(l[k]);
-          x.k2 = id;
-        }
-        pk_add(cnt, seg);
+        if (take) pk_add(cnt, seg);
       }
       const uint32_t bal = __ballot_sync(~0u, take);
       if (bal) {
         uint32_t basep = 0;
         if (lane == 0) basep = atomicAdd(&c.ctl->ncand, (unsigned)__popc(bal));
         basep = __shfl_sync(~0u, basep, 0);
-        if (take) {
+        if (take) {                       // raw record; exact scores after streaming
           const uint32_t pos = basep + __popc(bal & ((1u << lane) - 1u));
+          Cand x;
+          x.ss = (uint32_t)(t0 + k) | ((q == Q_EF ? 0u : 1u) << 28);
+          x.seg = seg;
+          x.k0 = q == Q_EF ? key : 0ull;
+          x.k1 = q == Q_EF ? 0ull : key;
+          x.k2 = 0;
           gdst[pos] = x;
           if (x.seg != 0) note_cand(c, P, gdst, pos);
         }
       }
     }
-    cta_sync();                       // stage st fully consumed
-    if (tid == 0 && t + BSTAGES < ntiles) {
+    if (tid == 0 && t + BSTAGES < ntiles) {     // refill stage st once every warp drained it
+      mbar_wait(&empty[st], par);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads -> async writes
       issue_tile(t + BSTAGES);
     }
   }
   cta_sync();
+  if (tid == 0) {       // drain the empty barriers' last phases before the next scan re-inits them
+    for (uint64_t t = ntiles > (uint64_t)BSTAGES ? ntiles - BSTAGES : 0; t < ntiles; ++t)
+      mbar_wait(&empty[t % BSTAGES], (uint32_t)((t / BSTAGES) & 1));
+    for (int st = 0; st < BSTAGES; ++st) {
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[st])) : "memory");
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&empty[st])) : "memory");
+    }
+  }
   finalize_noted(c, P, gdst);
 #pragma unroll
   for (int w = 0; w < 4; ++w) {
@@ -746,29 +748,53 @@ __device__ void issue(Ctx& c, unsigned cmd) {
     run_cmd(c, cmd, true);
     return;
   }
-  if (threadIdx.x == 0) c.ctl->cmd = cmd;
-  uint64_t t0 = gtimer();
-  group_bar(c);                 // workers start
-  if (cmd == CMD_EXIT) return;
-  uint64_t t1 = gtimer();
-  run_cmd(c, cmd, true);
-  uint64_t t2 = gtimer();
-  group_bar(c);                 // everyone done
+  const uint64_t t0 = gtimer();
+  cta_sync();                   // every leader thread's parameter writes precede the post
   if (threadIdx.x == 0) {
+    const uint32_t seq = ++c.s->cseq;
+    __threadfence();
+    st_release_u64(&c.ctl->cmdw, (cmd_tag(c.d->epoch, seq) << 8) | cmd);
+  }
+  if (cmd == CMD_EXIT) return;
+  const uint64_t t1 = gtimer();
+  run_cmd(c, cmd, true);
+  const uint64_t t2 = gtimer();
+  if (threadIdx.x == 0) {
+    const unsigned long long target = (unsigned long long)(c.GP - 1) * c.s->cseq;
+    while (ld_acquire_u64(&c.ctl->done) < target) __nanosleep(20);
     const uint64_t t3 = gtimer();
     c.s->st.tph[8] += t1 - t0;
     c.s->st.tph[9] += t2 - t1;
     c.s->st.tph[10] += t3 - t2;
   }
+  cta_sync();
+}
+
+// Leader, before its first command of a launch: reset the done counter.
+__device__ void group_open(Ctx& c) {
+  if (threadIdx.x == 0) {
+    c.s->cseq = 0;
+    if (c.GP > 1) { c.ctl->done = 0; __threadfence(); }
+  }
+  cta_sync();
 }
 
 __device__ void worker_loop(Ctx& c) {
-  while (true) {
-    group_bar(c);
-    const unsigned cmd = __ldcg(&c.ctl->cmd);
+  for (uint32_t seq = 1;; ++seq) {
+    if (threadIdx.x == 0) {
+      const unsigned long long want = cmd_tag(c.d->epoch, seq);
+      unsigned long long w;
+      while (((w = ld_acquire_u64(&c.ctl->cmdw)) >> 8) != want) __nanosleep(20);
+      c.s->wcmd = (unsigned)(w & 0xFFu);
+    }
+    cta_sync();
+    const unsigned cmd = c.s->wcmd;
     if (cmd == CMD_EXIT) return;
-    run_cmd(c, cmd, false);
-    group_bar(c);
+    run_cmd(c, cmd, false);     // ends with a CTA barrier
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(&c.ctl->done, 1ull);
+    }
   }
 }
 
@@ -1001,8 +1027,13 @@ __device__ void radix_select(const Cand* a, uint32_t n, bool per_seg, uint32_t a
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid < 16) { s.pfx[tid] = 0; s.pmask[tid] = 0; s.below[tid] = 0; }
   cta_sync();
+  const uint32_t nact = __popc(active);
   for (int shift = 56; shift >= 0; shift -= 8) {
-    for (int i = tid; i < NSEG * 256; i += NT) s.rhist[i] = 0;
+    for (uint32_t i = tid; i < nact * 256; i += NT) {      // clear the active classes' bins only
+      uint32_t a = active;
+      for (uint32_t j = i >> 8; j > 0; --j) a &= a - 1;
+      s.rhist[(__ffs(a) - 1) * 256 + (i & 255u)] = 0;
+    }
     cta_sync();
     for (uint32_t i0 = 0; i0 < n; i0 += NT) {
       const uint32_t i = i0 + tid;
@@ -1147,6 +1178,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
     if (tid < NSEG && (((fail >> tid) & 1u) || attempt >= 1)) st.thr[tid] = ~0ull;
     cta_sync();
   }
+  const uint64_t tS = gtimer();
   const uint32_t nc = s.ncand;
   uint64_t Kth = nc >= m ? s.pfx[0] : ~0ull;
   // ---- stage exactly the m smallest by (k0, k1, k2): k0 < Kth, then inside the k0 tie
@@ -1252,6 +1284,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
   }
   cta_sync();
   for (uint32_t v = tid; v < m; v += NT) c.cand[v] = c.vbuf[v];
+  if (tid == 0) st.tph[12] += gtimer() - tS;
   cta_sync();
 }
 
@@ -1518,10 +1551,11 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
         }
         // O7/O8 touch: last = now, hint overwritten (A9, A10)
         d.blast[gi] = now;
-        d.bmeta[gi] = meta_pack(q, tau, meta_ntok(meta)) | M_PIN;   // pinned for this round (A11)
+        d.bkey[gi] = scan_key(q, meta_ntok(meta), q == Q_EF ? d.bid[gi] : 0u, now);
+        d.bmeta[gi] = meta_pack(q, tau, meta_ntok(meta)) | M_PIN |       // pinned for this round (A11)
+                      (lrq_of(j, omax) << M_LRQ_SHIFT);
         d.bob[gi] = j;
         d.bomax[gi] = omax;
-        d.blr[gi] = lr_of(j, omax);
       } else if (j >= h) {  // O9 miss-after-evict, consumed (A30)
         const uint64_t H = b.h[bo + j];
         const int32_t gp = tbl_find_pos(gkey, d.gmask, H);
@@ -1593,10 +1627,10 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
     d.blast[gi] = now;
     d.bid[gi] = (uint32_t)(st.next_id + rk);
     d.bacc[gi] = 1;
-    d.bmeta[gi] = meta_pack(q, tau, b.ntok[bo + j]);
+    d.bkey[gi] = scan_key(q, b.ntok[bo + j], (uint32_t)(st.next_id + rk), now);
+    d.bmeta[gi] = meta_pack(q, tau, b.ntok[bo + j]) | (lrq_of(j, omax) << M_LRQ_SHIFT);
     d.bob[gi] = j;
     d.bomax[gi] = omax;
-    d.blr[gi] = lr_of(j, omax);
     tbl_insert(tkey, tval, d.tmask, H, sl, &st.tbl_used);
   }
   cta_sync();
@@ -1651,6 +1685,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_replay(Dev d, BatchDe
     worker_loop(c);
     return;
   }
+  group_open(c);
   const uint32_t lo = b.run_start[r];
   if (lo != 0xFFFFFFFFu) {
     const uint32_t hi = b.run_end[r];
@@ -1672,6 +1707,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_evict(Dev d, uint32_t
     worker_loop(c);
     return;
   }
+  group_open(c);
   load_state(c);
   RState& st = c.s->st;
   if (st.err == 0) {
@@ -1704,6 +1740,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_update(Dev d, uint32_
     worker_loop(c);
     return;
   }
+  group_open(c);
   load_state(c);
   learn(c);
   store_state(c);

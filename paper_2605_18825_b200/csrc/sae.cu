@@ -45,6 +45,9 @@ constexpr double INV_SQRT2 = 0.70710678118654757;  // 0x3FE6A09E667F3BCD
 
 enum { Q_EF = 0, Q_CHAT = 1, Q_AGENT = 2, Q_STRUCT = 3 };
 enum { M_LIVE = 1u << 10, M_PIN = 1u << 11 };
+// meta bits 16..31: q16 = floor(-ln(o_b/o_max) * 4096) (0xFFFF for o_b = 0), the STRUCT
+// prefilter's gamma-independent input; -q16/4096 is an upper bound of ln(o_b/o_max).
+constexpr uint32_t M_LRQ_SHIFT = 16;
 
 __host__ __device__ inline uint32_t meta_pack(uint32_t q, uint32_t tau, uint32_t ntok) {
   return q | (tau << 2) | (ntok << 5) | M_LIVE;
@@ -71,7 +74,7 @@ struct RState {
   uint64_t learner_firings, eviction_rounds, blocks_scored, blocks_scored_struct;
   uint64_t select_passes, select_cands, select_big, select_fail_seg[10];
   uint64_t select_narrow, select_raw;
-  uint64_t tph[12];         // leader phase timers (ns): probe, scan, narrow, select, apply, learn, insert, rebuild,
+  uint64_t tph[16];         // leader phase timers (ns): probe, scan, narrow, select, apply, learn, insert, rebuild,
                             // + issue(): start barrier, own partition, end barrier, (spare)
   uint64_t thr[16];        // per-segment candidate thresholds on k0 (heuristic; exactness never depends on them)
   sae_params par;
@@ -89,8 +92,8 @@ struct Cand {           // one candidate victim: sort key (tier, k0, k1, k2) + s
 enum { CMD_SCAN = 1, CMD_HIST, CMD_COMPACT, CMD_REFRESH, CMD_CLEAR_T, CMD_FILL_T, CMD_CLEAR_G,
        CMD_FILL_G, CMD_COUNTQ, CMD_EXIT };
 struct GroupCtl {          // hot words on separate 128-byte lines (polled / atomically updated)
-  alignas(128) unsigned bar_count;
-  alignas(128) unsigned bar_gen;
+  alignas(128) unsigned long long cmdw;   // posted command word (epoch:24 | seq:32 | cmd:8)
+  alignas(128) unsigned long long done;   // cumulative worker completions this launch
   alignas(128) unsigned ncand;
   alignas(128) unsigned nsel;
   alignas(128) unsigned tblcnt;
@@ -110,6 +113,7 @@ struct GroupCtl {          // hot words on separate 128-byte lines (polled / ato
 struct Dev {
   uint32_t R, C, tmask, G, gmask, K, iv_ring, iv_keep, iv_min, nbins, B, traj_cap;
   uint32_t GP;          // CTAs per replica (group size)
+  uint32_t epoch;       // launch counter of the ctx (group command words are tagged with it)
   uint32_t cand_smem;   // 1: candidates live in the leader's smem (C <= CAND_MAX, GP == 1)
   uint32_t bulk_ok;     // 1: replica bases are 16-byte aligned (C % 4 == 0): bulk-copy scan
   Cand* gcand;          // [R*C] global candidate buffer (large pools)
@@ -124,7 +128,7 @@ struct Dev {
   uint32_t* bmeta;
   uint32_t* bob;
   uint32_t* bomax;
-  float* blr;           // ln(o_b/o_max) as fp32 (-inf for o_b = 0): gamma-independent prefilter input
+  uint64_t* bkey;       // scan key: EF ? (ntok << 32 | id) : obits(last)
   uint32_t* bacc;
   uint32_t* bpin;
   uint32_t* freestk;
@@ -207,17 +211,27 @@ __device__ double p_struct(uint32_t ob, uint32_t omax, double gam) {
   double r = __ddiv_rn((double)ob, (double)omax);
   return __dsub_rn(1.0, dm::ex(__dmul_rn(gam, dm::ln(r))));
 }
-// gamma-independent per-block input of the STRUCT prefilter
-__device__ __forceinline__ float lr_of(uint32_t ob, uint32_t omax) {
-  if (ob == 0) return __int_as_float(0xff800000);   // -inf: p = 1
-  return (float)dm::ln(__ddiv_rn((double)ob, (double)omax));
+// gamma-independent per-block input of the STRUCT prefilter, stored in meta bits 16..31:
+// q16 = floor(-ln(o_b/o_max) * 4096) (an upper bound -q16/4096 of ln(o_b/o_max), so the
+// bound below stays a lower bound of p); 0xFFFF encodes o_b = 0 (ln = -inf, p = 1).
+__device__ __forceinline__ uint32_t lrq_of(uint32_t ob, uint32_t omax) {
+  if (ob == 0) return 0xFFFFu;
+  const double x = -dm::ln(__ddiv_rn((double)ob, (double)omax)) * 4096.0;
+  const double f = floor(x * (1.0 - 0x1p-40));     // never rounds past the true value
+  return (uint32_t)fmin(fmax(f, 0.0), 65534.0);
 }
-// A guaranteed lower bound of Eq.(2)'s p = 1 - exp(gamma * ln(o/o_max)): fp32 exp (relative
-// error < 1e-5 over the argument range [-34, 0]) inflated by 2^-10.  Used only to decide
-// which STRUCT blocks need their exact score; never to order them.
-__device__ __forceinline__ double p_struct_lo(float lr, float gam) {
-  const double e = (double)__expf(gam * lr);
+__device__ __forceinline__ uint32_t meta_lrq(uint32_t m) { return m >> M_LRQ_SHIFT; }
+// A guaranteed lower bound of Eq.(2)'s p = 1 - exp(gamma * ln(o/o_max)) (gamma > 0) from
+// q16: fp32 exp (relative error < 1e-5 over the argument range) inflated by 2^-10.  Used
+// only to decide which STRUCT blocks need their exact score; never to order them.
+__device__ __forceinline__ double p_struct_lo(uint32_t q16, float gam) {
+  if (q16 == 0xFFFFu) return 1.0 - 0x1p-10;
+  const double e = (double)__expf(-gam * ((float)q16 * (1.0f / 4096.0f)));
   return 1.0 - fmin(1.0, e * (1.0 + 0x1p-10));
+}
+// scan key of a block (see Dev::bkey)
+__device__ __forceinline__ uint64_t scan_key(uint32_t q, uint32_t ntok, uint32_t id, double last) {
+  return q == Q_EF ? (((uint64_t)ntok << 32) | id) : obits(last);
 }
 
 // Alg.1 Classify
@@ -511,6 +525,7 @@ static Variant variant(int nt) {
 
 static cudaError_t launch_group(const Variant& v, const void* fn, uint32_t grid, bool coop, cudaStream_t s,
                                 Dev& d, BatchDev* x) {
+  d.epoch++;
   void* args[] = {(void*)&d, (void*)x};
   if (coop) return cudaLaunchCooperativeKernel(fn, grid, v.nt, args, v.smem, s);
   return cudaLaunchKernel(fn, grid, v.nt, args, v.smem, s);
@@ -598,7 +613,7 @@ sae_status sae_create(const sae_config* cfg, sae_ctx** out) {
   CK(dalloc(ctx, &d.bmeta, RC + 4));   // +4: bulk-copy tail padding
   CK(dalloc(ctx, &d.bob, RC));
   CK(dalloc(ctx, &d.bomax, RC));
-  CK(dalloc(ctx, &d.blr, RC + 4));   // +4: bulk-copy tail padding
+  CK(dalloc(ctx, &d.bkey, RC + 4));   // +4: bulk-copy tail padding
   CK(dalloc(ctx, &d.bacc, RC));
   CK(dalloc(ctx, &d.bpin, RC));
   CK(dalloc(ctx, &d.freestk, RC));
@@ -847,6 +862,7 @@ sae_status sae_lookup(sae_ctx* ctx, const sae_batch* b, uint32_t* hit, sae_strea
 sae_status sae_evict(sae_ctx* ctx, uint32_t replica, uint32_t k, double now, uint32_t* vids,
                      uint32_t* n_out, sae_stream st) {
   if (!ctx || replica >= ctx->d.R || (k > 0 && !vids)) return SAE_E_INVAL;
+  ctx->d.epoch++;
   void* args[] = {(void*)&ctx->d, (void*)&replica, (void*)&k, (void*)&now, (void*)&vids, (void*)&n_out};
   if (ctx->d.GP > 1)
     CK(cudaLaunchCooperativeKernel(ctx->var.evict, ctx->d.GP, ctx->var.nt, args, ctx->var.smem, (cudaStream_t)st));
@@ -866,6 +882,7 @@ sae_status sae_update(sae_ctx* ctx, uint32_t replica, sae_stream st) {
   const uint32_t per = ctx->d.GP > 1 ? (uint32_t)std::max<uint64_t>(1, ctx->coresident / ctx->d.GP) : (r1 - r0);
   for (uint32_t a = r0; a < r1; a += per) {
     uint32_t b = std::min(r1, a + per);
+    ctx->d.epoch++;
     void* args[] = {(void*)&ctx->d, (void*)&a, (void*)&b};
     if (ctx->d.GP > 1)
       CK(cudaLaunchCooperativeKernel(ctx->var.update, (b - a) * ctx->d.GP, ctx->var.nt, args, ctx->var.smem, (cudaStream_t)st));
@@ -926,7 +943,7 @@ sae_status sae_stats(sae_ctx* ctx, uint32_t replica, sae_replica_stats* out, sae
   out->select_cands = rs.select_cands;
   out->select_big = rs.select_big;
   for (int g = 0; g < 10; ++g) out->select_fail_seg[g] = rs.select_fail_seg[g];
-  for (int g = 0; g < 12; ++g) out->phase_ns[g] = rs.tph[g];
+  for (int g = 0; g < 16; ++g) out->phase_ns[g] = rs.tph[g];
   out->select_narrow = rs.select_narrow;
   out->select_raw = rs.select_raw;
   {

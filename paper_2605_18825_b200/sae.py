@@ -18,7 +18,7 @@ from . import configs as CFG
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsae.so")
 
-SAE_ABI_VERSION = 1
+SAE_ABI_VERSION = 2
 ERRORS = {0: "SAE_OK", -1: "SAE_E_INVAL", -2: "SAE_E_CAPACITY_ZERO", -3: "SAE_E_EMPTY",
           -4: "SAE_E_NOT_RESIDENT", -5: "SAE_E_TIME", -6: "SAE_E_OVERFLOW", -7: "SAE_E_OOM",
           -8: "SAE_E_CUDA", -9: "SAE_E_ABI"}
@@ -78,7 +78,7 @@ class sae_replica_stats(C.Structure):
                 ("iv_len", C.c_uint64 * 2), ("traj_count", C.c_uint64),
                 ("select_passes", C.c_uint64), ("select_cands", C.c_uint64),
                 ("select_big", C.c_uint64), ("select_fail_seg", C.c_uint64 * 10),
-                ("phase_ns", C.c_uint64 * 12),
+                ("phase_ns", C.c_uint64 * 16),
                 ("select_narrow", C.c_uint64), ("select_raw", C.c_uint64),
                 ("params", sae_params)]
 

@@ -77,8 +77,11 @@ int main() {
   auto rep2 = [&](const char* nm, float ms) { ms -= fl; printf("%-36s %8.2f us  %7.1f GB/s\n", nm, ms * 1e3, bytes / (ms * 1e-3) / 1e9); };
 #define BULK(T, S, NTH, C, GRID) { auto k = k_bulk<T, S, NTH, C>; cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, T * 24 * S); \
    rep2("bulk T" #T " S" #S " nth" #NTH " c" #C " g" #GRID, timeit([&] { cudaMemsetAsync(flush, 0, 512 << 20); k<<<GRID, NTH, T * 24 * S>>>(m, id, l, p, N, out); })); }
-  BULK(1024, 4, 512, true, 147) BULK(1024, 4, 512, false, 147) BULK(2048, 4, 512, false, 147) BULK(1024, 8, 512, false, 147)
+  BULK(1024, 4, 512, true, 147) BULK(1024, 8, 512, true, 147) BULK(2048, 4, 512, true, 147) BULK(1024, 6, 512, true, 148) BULK(1024, 4, 512, false, 147) BULK(2048, 4, 512, false, 147) BULK(1024, 8, 512, false, 147)
   BULK(1024, 4, 256, false, 296) BULK(512, 4, 256, false, 592) BULK(2048, 4, 1024, false, 147) BULK(4096, 2, 512, false, 147)
+#define BULKNF(T, S, NTH, C, GRID) { auto k = k_bulk<T, S, NTH, C>; cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, T * 24 * S); \
+   rep("noflush bulk T" #T " S" #S " nth" #NTH " c" #C " g" #GRID, timeit([&] { k<<<GRID, NTH, T * 24 * S>>>(m, id, l, p, N, out); })); }
+  BULKNF(1024, 4, 512, true, 147) BULKNF(1024, 8, 512, true, 147) BULKNF(2048, 4, 512, true, 147) BULKNF(1024, 4, 256, true, 296)
   rep2("ldg 4/thr g147", timeit([&] { cudaMemsetAsync(flush, 0, 512 << 20); k_ldg<<<G, NT>>>(m, id, l, p, N, out); }));
   rep2("ldg 4/thr g592", timeit([&] { cudaMemsetAsync(flush, 0, 512 << 20); k_ldg<<<G * 4, NT>>>(m, id, l, p, N, out); }));
   rep2("ldg 4/thr g2368", timeit([&] { cudaMemsetAsync(flush, 0, 512 << 20); k_ldg<<<G * 16, NT>>>(m, id, l, p, N, out); }));
