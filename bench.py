@@ -418,6 +418,8 @@ def run_ours(args, wl, ws, rank, local):
     ph11 = st1[0].phase_ns[11] - st0[0].phase_ns[11]
     scan_ns = ph11 if ph11 > 0 else ph1
     phase_info = {"passes_per_request": passes / max(req, 1),
+                  "cands_per_pass": d("select_cands") / max(passes, 1),
+                  "raw_cands_per_pass": d("select_raw") / max(passes, 1),
                   "required_passes_per_request": (d("eviction_rounds") + d("learner_firings")) / max(req, 1),
                   "scan_ns_per_pass": scan_ns / max(passes / max(R, 1), 1),
                   "bytes_streamed_per_pass": (12.0 * pol["capacity"]) if ph11 > 0 else None,

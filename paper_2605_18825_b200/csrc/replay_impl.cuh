@@ -149,10 +149,12 @@ struct Smem {
   uint32_t npin, matched;
   uint64_t k, admit;
   uint64_t pfx[16], pmask[16];
-  uint32_t below[16], target[16];
+  uint32_t below[16], target[16], binc[16];
   unsigned long long kmin[16];
+  unsigned long long drefs[16], dors[16];  // radix_select: first key per class; OR of key differences
   uint32_t nv, nw;          // nw: this CTA's candidates awaiting finalize_key (global mode)
   uint32_t cseq, wcmd;      // leader: commands posted this launch; worker: command to run
+  uint32_t gbase;           // worker: this CTA's reservation in the group candidate buffer
   uint32_t rhist[NSEG * 256];   // radix-select histograms (one 256-bin digit per segment)
   __align__(8) uint64_t mbar[16];  // bulk-copy stage barriers (worker scan pipeline): full[8], empty[8]
   uint64_t wthr[16], wpfx[16], wpmask[16];   // worker copies of the leader's command parameters
@@ -434,6 +436,21 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// same, with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void bulk_g2s_pol(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                             uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t l2_policy(uint32_t which) {
+  uint64_t p;
+  if (which == 1) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -468,8 +485,14 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
     const uint32_t n4 = (n + 3) & ~3u;                 // 16-byte multiple (SoA is padded)
     unsigned char* b = buf + (size_t)st * BTILE_BYTES;
     mbar_expect_tx(&full[st], n4 * 12u);
-    bulk_g2s(b, d.bmeta + c.base + t0, n4 * 4u, &full[st]);
-    bulk_g2s(b + BTILE * 4, d.bkey + c.base + t0, n4 * 8u, &full[st]);
+    if (d.scan_l2) {
+      const uint64_t pol = l2_policy(d.scan_l2);
+      bulk_g2s_pol(b, d.bmeta + c.base + t0, n4 * 4u, &full[st], pol);
+      bulk_g2s_pol(b + BTILE * 4, d.bkey + c.base + t0, n4 * 8u, &full[st], pol);
+    } else {
+      bulk_g2s(b, d.bmeta + c.base + t0, n4 * 4u, &full[st]);
+      bulk_g2s(b + BTILE * 4, d.bkey + c.base + t0, n4 * 8u, &full[st]);
+    }
   };
   if (tid == 0) {
     for (int st = 0; st < BSTAGES; ++st) { mbar_init(&full[st], 1); mbar_init(&empty[st], NW); }
@@ -529,20 +552,24 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
         if (take) pk_add(cnt, seg);
       }
       const uint32_t bal = __ballot_sync(~0u, take);
-      if (bal) {
+      if (bal) {                          // CTA-local list of candidate slots (smem)
         uint32_t basep = 0;
-        if (lane == 0) basep = atomicAdd(&c.ctl->ncand, (unsigned)__popc(bal));
+        if (lane == 0) basep = atomicAdd(&s.nw, (unsigned)__popc(bal));
         basep = __shfl_sync(~0u, basep, 0);
-        if (take) {                       // raw record; exact scores after streaming
-          const uint32_t pos = basep + __popc(bal & ((1u << lane) - 1u));
-          Cand x;
-          x.ss = (uint32_t)(t0 + k) | ((q == Q_EF ? 0u : 1u) << 28);
-          x.seg = seg;
-          x.k0 = q == Q_EF ? key : 0ull;
-          x.k1 = q == Q_EF ? 0ull : key;
-          x.k2 = 0;
-          gdst[pos] = x;
-          if (x.seg != 0) note_cand(c, P, gdst, pos);
+        if (take) {
+          const uint32_t w = basep + __popc(bal & ((1u << lane) - 1u));
+          if (w < WCAP) {
+            s.rhist[w] = (uint32_t)(t0 + k);
+          } else {                        // list full (rare): append to the group buffer directly
+            Cand x;
+            x.ss = (uint32_t)(t0 + k) | ((q == Q_EF ? 0u : 1u) << 28);
+            x.seg = seg;
+            x.k0 = q == Q_EF ? key : 0ull;
+            x.k1 = q == Q_EF ? 0ull : key;
+            x.k2 = 0;
+            finalize_key(d, c.base, P, x);
+            gdst[atomicAdd(&c.ctl->ncand, 1u)] = x;
+          }
         }
       }
     }
@@ -561,7 +588,26 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
       asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&empty[st])) : "memory");
     }
   }
-  finalize_noted(c, P, gdst);
+  // publish the CTA's candidates: one reservation in the group buffer, then the records
+  // (meta/key re-read from L2; exact Eq.(1)-(3) scores, ids) written contiguously
+  const uint32_t nl = min(s.nw, WCAP);
+  if (tid == 0) s.gbase = atomicAdd(&c.ctl->ncand, nl);
+  cta_sync();
+  const uint32_t gb0 = s.gbase;
+  for (uint32_t i = tid; i < nl; i += NT) {
+    const uint32_t sl = s.rhist[i];
+    const uint32_t meta = __ldcg(d.bmeta + c.base + sl);
+    const uint64_t key = __ldcg(d.bkey + c.base + sl);
+    const uint32_t q = meta_q(meta);
+    Cand x;
+    x.ss = sl | ((q == Q_EF ? 0u : 1u) << 28);
+    x.seg = seg_of(q, meta_tau(meta));
+    x.k0 = q == Q_EF ? key : 0ull;
+    x.k1 = q == Q_EF ? 0ull : key;
+    x.k2 = 0;
+    finalize_key(d, c.base, P, x);
+    gdst[gb0 + i] = x;
+  }
 #pragma unroll
   for (int w = 0; w < 4; ++w) {
     for (int o = 16; o > 0; o >>= 1) {
@@ -1022,13 +1068,65 @@ __device__ void narrow(Ctx& c, uint32_t e, uint32_t mp);
 // rank s.target[g] (1-based) -> s.pfx[g], and the number of smaller keys -> s.below[g].
 // Global mode: one class (0), key k0.  Per-segment mode: class = segment, key = seg_key.
 __device__ void radix_select(const Cand* a, uint32_t n, bool per_seg, uint32_t active, Smem& s,
-                             int tie = 0, uint64_t K0 = 0, uint64_t K1 = 0) {
+                             int tie = 0, uint64_t K0 = 0, uint64_t K1 = 0, int digits = 8,
+                             uint32_t early = 0) {
+  // early > 0 (global mode): stop as soon as the chosen bin and everything below it hold at
+  // most `early` keys (below[0] + binc[0]); the caller then sorts that prefix set
+  // digits < 8: stop after that many 8-bit digits (the rank-target key then lies in
+  // [pfx, pfx | ~pmask]; used for threshold trimming, where any bound is exact)
   // tie = 1: key k1 over the candidates with k0 == K0; tie = 2: key k2 over k0 == K0 && k1 == K1
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid < 16) { s.pfx[tid] = 0; s.pmask[tid] = 0; s.below[tid] = 0; }
+  // The digits above the highest bit in which two keys of one class differ are common to
+  // the whole class: start below them (per class: OR of key ^ the class's first key).
+  if (tid < 16) { s.drefs[tid] = ~0ull; s.dors[tid] = 0ull; }
+  cta_sync();
+  for (uint32_t i0 = 0; i0 < n; i0 += NT) {          // a reference key per class
+    const uint32_t i = i0 + tid;
+    if (i < n) {
+      const Cand& x = a[i];
+      const uint32_t g = per_seg ? x.seg : 0u;
+      if (g < 16 && ((active >> g) & 1u) && (tie == 0 || (x.k0 == K0 && (tie == 1 || x.k1 == K1)))) {
+        const uint64_t key = per_seg ? seg_key(x) : (tie == 0 ? x.k0 : tie == 1 ? x.k1 : (uint64_t)x.k2);
+        if (s.drefs[g] == ~0ull) atomicCAS(&s.drefs[g], ~0ull, (unsigned long long)key);
+      }
+    }
+  }
+  cta_sync();
+  for (uint32_t i0 = 0; i0 < n; i0 += NT) {
+    const uint32_t i = i0 + tid;
+    uint32_t g = 0xFFFFFFFFu;
+    uint64_t dx = 0;
+    if (i < n) {
+      const Cand& x = a[i];
+      const uint32_t gg = per_seg ? x.seg : 0u;
+      if (gg < 16 && ((active >> gg) & 1u) && (tie == 0 || (x.k0 == K0 && (tie == 1 || x.k1 == K1)))) {
+        const uint64_t key = per_seg ? seg_key(x) : (tie == 0 ? x.k0 : tie == 1 ? x.k1 : (uint64_t)x.k2);
+        g = gg;
+        dx = key ^ s.drefs[gg];
+      }
+    }
+    const uint32_t peers = __match_any_sync(~0u, g);
+    if (g != 0xFFFFFFFFu) {
+      const uint32_t ohi = __reduce_or_sync(peers, (uint32_t)(dx >> 32));
+      const uint32_t olo = __reduce_or_sync(peers, (uint32_t)dx);
+      if (lane == __ffs(peers) - 1 && (ohi | olo)) atomicOr(&s.dors[g], ((unsigned long long)ohi << 32) | olo);
+    }
+  }
+  cta_sync();
+  int top = 0;
+  for (int g = 0; g < 16; ++g)
+    if ((active >> g) & 1u) {
+      const uint64_t dif = s.dors[g];
+      if (dif) top = max(top, (63 - __clzll((long long)dif)) & ~7);
+    }
+  if (tid < 16 && ((active >> tid) & 1u) && top < 56 && s.drefs[tid] != ~0ull) {
+    s.pmask[tid] = ~0ull << (top + 8);
+    s.pfx[tid] = s.drefs[tid] & s.pmask[tid];
+  }
   cta_sync();
   const uint32_t nact = __popc(active);
-  for (int shift = 56; shift >= 0; shift -= 8) {
+  for (int shift = top; shift >= 0 && shift > top - 8 * digits; shift -= 8) {
     for (uint32_t i = tid; i < nact * 256; i += NT) {      // clear the active classes' bins only
       uint32_t a = active;
       for (uint32_t j = i >> 8; j > 0; --j) a &= a - 1;
@@ -1072,12 +1170,63 @@ __device__ void radix_select(const Cand* a, uint32_t n, bool per_seg, uint32_t a
           run += v[j];
         }
         s.below[g] += run;
+        s.binc[g] = v[bsel & 7];
         s.pfx[g] |= (uint64_t)bsel << shift;
         s.pmask[g] |= 0xFFull << shift;
       }
     }
     cta_sync();
+    if (early && s.below[0] + s.binc[0] <= early) break;
   }
+}
+
+// Stage the candidates with k0 <= Ub (at most VCAP) into vbuf and sort them by (k0, k1, k2);
+// also the per-segment minimum keys (kmin) over all candidates, for threshold growth.
+__device__ void stage_victims(Ctx& c, uint32_t nc, uint64_t Ub) {
+  Smem& s = *c.s;
+  RState& st = s.st;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) s.nv = 0;
+  if (tid < 16) s.kmin[tid] = ~0ull;
+  cta_sync();
+  for (uint32_t i0 = 0; i0 < nc; i0 += NT) {
+    const uint32_t i = i0 + tid;
+    uint32_t g = 0xFFFFFFFFu;
+    uint64_t key = ~0ull;
+    bool take = false;
+    if (i < nc) {
+      const Cand& x = c.cand[i];
+      // EF grows within its threshold's num_tokens band: min over that band only
+      if (x.seg != 0 || (x.k0 >> 32) == (st.thr[0] >> 32)) { g = x.seg; key = seg_key(x); }
+      take = x.k0 <= Ub;
+    }
+    const uint32_t peers = __match_any_sync(~0u, g);
+    if (g != 0xFFFFFFFFu) {
+      const uint32_t hi = (uint32_t)(key >> 32), lo = (uint32_t)key;
+      const uint32_t mhi = __reduce_min_sync(peers, hi);
+      const uint32_t p2 = peers & __ballot_sync(peers, hi == mhi);
+      if (hi == mhi) {
+        const uint32_t mlo = __reduce_min_sync(p2, lo);
+        if (lane == __ffs(p2) - 1) atomicMin(&s.kmin[g], ((unsigned long long)mhi << 32) | mlo);
+      }
+    }
+    const uint32_t bal = __ballot_sync(~0u, take);
+    uint32_t basep = 0;
+    if (lane == 0 && bal) basep = atomicAdd(&s.nv, (uint32_t)__popc(bal));
+    basep = __shfl_sync(~0u, basep, 0);
+    const uint32_t pos = basep + __popc(bal & ((1u << lane) - 1u));
+    if (take && pos < VCAP) c.vbuf[pos] = c.cand[i];
+  }
+  cta_sync();
+  const uint32_t nv = min(s.nv, (uint32_t)VCAP);
+  int N = 32;
+  while ((uint32_t)N < nv) N <<= 1;
+  for (uint32_t i = nv + tid; i < (uint32_t)N; i += NT) {
+    c.vbuf[i].k0 = ~0ull; c.vbuf[i].k1 = ~0ull; c.vbuf[i].k2 = ~0u; c.vbuf[i].ss = 15u << 28;
+    c.vbuf[i].seg = 15;
+  }
+  cta_sync();
+  sort_cands(c.vbuf, N);
 }
 
 __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass) {
@@ -1089,6 +1238,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const bool gm = !d.cand_smem;
   uint32_t e = 0, mp = 0, c0 = 0;
+  bool staged = false;
   for (int attempt = 0; attempt < 3; ++attempt) {
     if (tid < 16) { s.used[tid] = 0; }
     if (tid == 0) {
@@ -1116,6 +1266,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
       if (tid == 0) { st.select_raw += s.ncand; st.select_narrow += narrowed ? 1 : 0; }
       if (narrowed) narrow(c, e0, m - e0);
       if (tid == 0 && narrowed) { const uint64_t t1 = gtimer(); st.tph[2] += t1 - t0; t0 = t1; }
+      const uint64_t tL = gtimer();
       const Cand* src = narrowed ? d.gsel + (uint64_t)c.r * CAND_MAX : d.gcand + c.base;
       for (uint32_t i = tid; i < s.ncand; i += NT) {
         Cand x;
@@ -1124,6 +1275,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
         c.cand[i] = x;
       }
       cta_sync();
+      if (tid == 0) st.tph[13] += gtimer() - tL;
     }
     const uint32_t nc = s.ncand;
     if (tid == 0) {
@@ -1144,11 +1296,27 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
     e = min(m, s.segtot[0]);
     mp = m - e;
     uint64_t Kth = ~0ull;
+    staged = false;
+    const uint64_t tR = gtimer();
     if (nc >= m) {
       if (tid == 0) s.target[0] = m;
       cta_sync();
-      radix_select(c.cand, nc, false, 1u, s);
+      radix_select(c.cand, nc, false, 1u, s, 0, 0, 0, 8, VCAP / 2);
       Kth = s.pfx[0];
+      staged = s.below[0] + s.binc[0] <= VCAP;
+    } else {
+      staged = true;                     // nc < m <= MSUB < VCAP
+    }
+    const uint64_t tV = gtimer();
+    if (tid == 0) st.tph[14] += tV - tR;
+    if (staged) {
+      // stage every candidate whose k0 is at most the chosen bin's upper bound (a superset
+      // of the m smallest by (k0, k1, k2)), plus the per-segment minimum keys for threshold
+      // growth, then sort the staged set: its first m are the victims, in order
+      const uint64_t Ub = nc >= m ? (s.pfx[0] | ~s.pmask[0]) : ~0ull;
+      stage_victims(c, nc, Ub);
+      if (nc >= m) Kth = c.vbuf[m - 1].k0;
+      if (tid == 0) st.tph[15] += gtimer() - tV;
     }
     // ---- exactness check: every block a threshold left out must lose to the mp-th
     //      scored candidate.  EF: enough heads.  Class c: a non-candidate has last > T_c,
@@ -1181,6 +1349,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
   const uint64_t tS = gtimer();
   const uint32_t nc = s.ncand;
   uint64_t Kth = nc >= m ? s.pfx[0] : ~0ull;
+  if (!staged) {           // rare: a k0 tie group larger than the staging buffer
   // ---- stage exactly the m smallest by (k0, k1, k2): k0 < Kth, then inside the k0 tie
   //      group (k1, k2) < the tie-break rank found by two more radix selects (ids unique)
   uint64_t K1th = ~0ull, K2th = ~0ull;
@@ -1210,11 +1379,26 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
   cta_sync();
   for (uint32_t i0 = 0; i0 < nc; i0 += NT) {
     const uint32_t i = i0 + tid;
-    if (i < nc) {
-      const Cand& x = c.cand[i];
-      // EF grows within its threshold's num_tokens band: min over that band only
-      if (x.seg != 0 || (x.k0 >> 32) == (st.thr[0] >> 32))
-        atomicMin(&s.kmin[x.seg], (unsigned long long)seg_key(x));
+    {
+      // per-segment minimum key (threshold growth below): lanes of one segment reduce
+      // among themselves (64-bit min as two 32-bit reductions), one smem atomic per group
+      uint32_t g = 0xFFFFFFFFu;
+      uint64_t key = ~0ull;
+      if (i < nc) {
+        const Cand& x = c.cand[i];
+        // EF grows within its threshold's num_tokens band: min over that band only
+        if (x.seg != 0 || (x.k0 >> 32) == (st.thr[0] >> 32)) { g = x.seg; key = seg_key(x); }
+      }
+      const uint32_t peers = __match_any_sync(~0u, g);
+      if (g != 0xFFFFFFFFu) {
+        const uint32_t hi = (uint32_t)(key >> 32), lo = (uint32_t)key;
+        const uint32_t mhi = __reduce_min_sync(peers, hi);
+        const uint32_t p2 = peers & __ballot_sync(peers, hi == mhi);
+        if (hi == mhi) {
+          const uint32_t mlo = __reduce_min_sync(p2, lo);
+          if (lane == __ffs(p2) - 1) atomicMin(&s.kmin[g], ((unsigned long long)mhi << 32) | mlo);
+        }
+      }
     }
     bool take = false;
     if (i < nc) {
@@ -1240,11 +1424,12 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
     cta_sync();
     sort_cands(c.vbuf, N);       // small: the m victims in (k0, last, id) order
   }
+  }                        // !staged
   // ---- carry thresholds: trim segments holding far more candidates than they use
   for (uint32_t v = tid; v < m; v += NT) atomicAdd(&s.used[c.vbuf[v].seg], 1u);
   cta_sync();
   // small private pools (rescans are cheap) trim hard; large pools trim lazily
-  const uint32_t trim_at = 8u, trim_to = 4u;
+  const uint32_t trim_at = d.trim_at, trim_to = d.trim_to;
   uint32_t shrink = 0;
   for (int g = 0; g < NSEG; ++g) {
     const uint32_t want = 3 * s.used[g] + SLACK;
@@ -1253,8 +1438,8 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
   if (shrink) {
     if (tid < NSEG) s.target[tid] = trim_to * (3 * s.used[tid] + SLACK);
     cta_sync();
-    radix_select(c.cand, nc, true, shrink, s);
-    if (tid < NSEG && ((shrink >> tid) & 1u)) st.thr[tid] = s.pfx[tid];
+    radix_select(c.cand, nc, true, shrink, s, 0, 0, 0, 2);   // two digits: a bound, not a rank
+    if (tid < NSEG && ((shrink >> tid) & 1u)) st.thr[tid] = min(st.thr[tid], s.pfx[tid] | ~s.pmask[tid]);
     cta_sync();
   }
   // ---- grow a segment's threshold before its reserve runs dry (avoids refills): double

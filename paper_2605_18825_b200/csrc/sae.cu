@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -116,6 +117,10 @@ struct Dev {
   uint32_t epoch;       // launch counter of the ctx (group command words are tagged with it)
   uint32_t cand_smem;   // 1: candidates live in the leader's smem (C <= CAND_MAX, GP == 1)
   uint32_t bulk_ok;     // 1: replica bases are 16-byte aligned (C % 4 == 0): bulk-copy scan
+  uint32_t trim_at, trim_to;   // threshold trimming: a segment holding > trim_at x its want is
+                               // cut to trim_to x want (env SAE_TRIM="at,to"; default 8,4)
+  uint32_t scan_l2;     // L2 policy of the streamed scan columns: 1 evict_last (they fit in L2
+                        // next to the random-access state), 2 evict_first (they do not)
   Cand* gcand;          // [R*C] global candidate buffer (large pools)
   Cand* gsel;           // [R*CAND_MAX] compacted candidates after narrowing
   GroupCtl* ctl;        // [R]
@@ -656,6 +661,18 @@ sae_status sae_create(const sae_config* cfg, sae_ctx** out) {
   d.GP = (uint32_t)gp;
   d.cand_smem = (d.C <= ctx->var.cand_max && d.GP == 1) ? 1u : 0u;
   d.bulk_ok = (d.C % 4 == 0) ? 1u : 0u;
+  d.trim_at = 8;
+  d.trim_to = 4;
+  if (const char* e = getenv("SAE_TRIM")) {
+    unsigned a = 0, b = 0;
+    if (sscanf(e, "%u,%u", &a, &b) == 2 && a >= 2 && b >= 1 && b < a) { d.trim_at = a; d.trim_to = b; }
+  }
+  {
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, cfg->device);
+    const uint64_t scan_bytes = (uint64_t)d.R * d.C * 12ull;
+    d.scan_l2 = scan_bytes * 2 <= (uint64_t)l2 ? 1u : 2u;
+  }
   ctx->coresident = coresident;
   CK(dalloc(ctx, &d.ctl, R));
   CK(cudaMemset(d.ctl, 0, R * sizeof(GroupCtl)));
