@@ -155,6 +155,9 @@ struct Smem {
   uint32_t nv, nw;          // nw: this CTA's candidates awaiting finalize_key (global mode)
   uint32_t cseq, wcmd;      // leader: commands posted this launch; worker: command to run
   uint32_t gbase;           // worker: this CTA's reservation in the group candidate buffer
+  uint32_t pincnt[16];      // leader: this round's pinned blocks per segment
+  unsigned long long thr64[16];   // candidacy table of the current scan: keys (EF, multi-turn)
+  uint32_t thrS[1024];            // STRUCT: upper 32 bits of a bound on obits(last), per (tau, q8)
   uint32_t rhist[NSEG * 256];   // radix-select histograms (one 256-bin digit per segment)
   __align__(8) uint64_t mbar[16];  // bulk-copy stage barriers (worker scan pipeline): full[8], empty[8]
   uint64_t wthr[16], wpfx[16], wpmask[16];   // worker copies of the leader's command parameters
@@ -226,46 +229,55 @@ struct ScanP {
 // (meta, id, last; p_struct only for STRUCT blocks); per-segment counts accumulate in
 // registers (16-bit fields) and are reduced once per pass.  Counts go to smem
 // (segtot, cnt); candidates to smem (cand_smem) or the group's global buffer.
-__device__ __forceinline__ void pk_add(uint64_t (&pk)[4], uint32_t seg) {
-  const uint64_t inc = 1ull << ((seg & 3u) * 16u);
-  switch (seg >> 2) {
-    case 0: pk[0] += inc; break;
-    case 1: pk[1] += inc; break;
-    case 2: pk[2] += inc; break;
-    default: pk[3] += inc; break;
+
+// Candidacy table of one scan pass (a4), built by every scanning CTA from the pass
+// parameters: a block is a candidate iff its key is at or below its table entry.
+//  * EF / multi-turn class: entry = the segment's carried threshold (key (ntok, id) / obits(last)).
+//  * STRUCT class tau, bound q8: P = c * p / dt with p >= p_lo(q8), so P <= T implies
+//    dt >= A = c * p_lo / T, i.e. last <= now - A (or any block if A <= eps).  The entry is
+//    the upper 32 bits of obits(now - A * (1 - 2^-20)) rounded up: a superset of the
+//    blocks with P <= T (a non-candidate has P > T * (1 + 2^-20), far beyond rounding).
+// Exact Eq.(1)-(3) scores of the (few) candidates are computed afterwards by finalize_key.
+__device__ void build_thr_table(Smem& s, const ScanP& P) {
+  const int tid = threadIdx.x;
+  if (tid < 16) s.thr64[tid] = tid < NSEG ? P.thr[tid] : 0ull;
+  const float gamf = (float)P.gamma;
+  for (int e = tid; e < 1024; e += NT) {
+    const int tau = e >> 8;
+    const uint32_t q8 = (uint32_t)(e & 255);
+    const uint64_t T = P.thr[9 + tau];
+    uint32_t ent = 0xFFFFFFFFu;
+    if (T != ~0ull) {
+      const double Tp = from_obits(T);
+      const double pl = p_struct_lo8(q8, gamf);
+      const double num = __dmul_rn(P.cw[10 + tau], pl);
+      if (num > 0.0) {
+        const double A = __dmul_rn(__ddiv_rn(num, Tp), 1.0 - 0x1p-20);   // Tp = 0: A = inf
+        if (A > P.dt_eps) {
+          const double L = __dsub_rn(P.now, A);
+          const double Lu = __dadd_rn(__dadd_rn(L, fabs(L) * 0x1p-30), 0x1p-30);
+          ent = (uint32_t)(obits(Lu) >> 32);
+        }
+      }
+    }
+    s.thrS[e] = ent;
   }
 }
-
-// Candidacy of one resident, unpinned block (a4).  Exact for EF (key (ntok, id)) and the
-// multi-turn classes (key: last); conservative for STRUCT (a lower bound of P against the
-// threshold).  The exact Eq.(1)-(3) scores of the (few) candidates are computed afterwards
-// by finalize_keys, outside the streaming loop.
-__device__ __forceinline__ bool score_one(const ScanP& P, uint32_t meta, uint64_t key, uint32_t sl,
-                                          Cand& x) {
-  const uint32_t q = meta_q(meta), tau = meta_tau(meta);
-  const uint32_t seg = seg_of(q, tau);
-  bool take;
+__device__ __forceinline__ bool cand_test(const Smem& s, uint32_t meta, uint64_t key) {
+  const uint32_t tix = meta_tix(meta);
+  return tix < 16u ? key <= s.thr64[tix] : (uint32_t)(key >> 32) <= s.thrS[tix - 16u];
+}
+// The candidate record of a block (exact keys of scored ones are set by finalize_key).
+__device__ __forceinline__ Cand make_cand(uint32_t meta, uint64_t key, uint32_t sl) {
+  const uint32_t q = meta_q(meta);
+  Cand x;
   x.ss = sl | ((q == Q_EF ? 0u : 1u) << 28);
-  x.seg = seg;
-  x.k2 = 0;                             // id of a scored candidate: loaded by finalize_key
-  if (q == Q_EF) {                      // Stage 1 key (num_tokens, id)
-    x.k0 = key;
-    x.k1 = 0;
-    take = key <= P.thr[0];
-  } else if (q == Q_STRUCT) {           // prefilter: lower bound of Eq.(2)+(3) vs threshold
-    x.k0 = 0;
-    x.k1 = key;
-    double dt = __dsub_rn(P.now, from_obits(key));
-    if (dt < P.dt_eps) dt = P.dt_eps;
-    const double T = P.thr[seg] == ~0ull ? __longlong_as_double(0x7ff0000000000000ll) : from_obits(P.thr[seg]);
-    take = __dmul_rn(P.cw[10 + tau], p_struct_lo(meta_lrq(meta), (float)P.gamma)) <=
-           __dmul_rn(__dmul_rn(T, dt), 1.0 + 0x1p-40);
-  } else {                              // multi-turn class (queue, tau): key obits(last)
-    x.k0 = 0;
-    x.k1 = key;
-    take = key <= P.thr[seg];
-  }
-  return take;
+  x.seg = seg_of_tix(meta_tix(meta));
+  x.k0 = q == Q_EF ? key : 0ull;
+  x.k1 = q == Q_EF ? 0ull : key;
+  x.k2 = 0;
+  x.pad = 0;
+  return x;
 }
 
 // Exact score of a scored candidate: Eq.(1) survival (multi-turn) or Eq.(2) (STRUCT),
@@ -314,15 +326,17 @@ __device__ void finalize_noted(Ctx& c, const ScanP& P, Cand* gdst) {
   }
 }
 
+// One pass over slots [lo, hi) of the replica's SoA with 128-bit loads, 4 consecutive slots
+// per thread per step (software-pipelined one step ahead): candidacy by the table; the
+// candidates go to smem (cand_smem) or the group's global buffer, counted per segment in
+// s.cnt.  Exact scores after the stream.
 __device__ void scan_range(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P) {
   const Dev& d = *c.d;
   Smem& s = *c.s;
   const int tid = threadIdx.x, lane = tid & 31;
   const bool gm = !d.cand_smem;
   Cand* gdst = gm ? d.gcand + c.base : nullptr;
-  uint64_t tot[4] = {0, 0, 0, 0}, cnt[4] = {0, 0, 0, 0};
   const bool vec = ((c.base + lo) & 3u) == 0;
-  // software pipeline: the next step's 4 slots are loaded before this step is scored
   uint32_t mt[4];
   uint64_t kt[4];
   auto load = [&](uint64_t s0, uint32_t (&m)[4], uint64_t (&k)[4]) {
@@ -357,14 +371,8 @@ __device__ void scan_range(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P) {
     if (sn < hi) load(sn, mn, kn);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      bool take = false;
-      Cand x;
       const uint32_t meta = s0 < hi ? mt[u] : 0u;
-      if ((meta & (M_LIVE | M_PIN)) == M_LIVE) {
-        take = score_one(P, meta, kt[u], (uint32_t)(s0 + u), x);
-        pk_add(tot, x.seg);
-        if (take) pk_add(cnt, x.seg);
-      }
+      const bool take = (meta & (M_LIVE | M_PIN)) == M_LIVE && cand_test(s, meta, kt[u]);
       if (gm) {
         const uint32_t bal = __ballot_sync(~0u, take);
         if (bal) {
@@ -373,11 +381,15 @@ __device__ void scan_range(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P) {
           basep = __shfl_sync(~0u, basep, 0);
           if (take) {
             const uint32_t pos = basep + __popc(bal & ((1u << lane) - 1u));
+            const Cand x = make_cand(meta, kt[u], (uint32_t)(s0 + u));
+            atomicAdd(&s.cnt[x.seg], 1u);
             gdst[pos] = x;
             if (x.seg != 0) note_cand(c, P, gdst, pos);
           }
         }
       } else if (take) {
+        const Cand x = make_cand(meta, kt[u], (uint32_t)(s0 + u));
+        atomicAdd(&s.cnt[x.seg], 1u);
         c.cand[atomicAdd(&s.ncand, 1u)] = x;
       }
     }
@@ -390,22 +402,6 @@ __device__ void scan_range(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P) {
     finalize_noted(c, P, gdst);
   } else {
     for (uint32_t i = tid; i < s.ncand; i += NT) finalize_key(d, c.base, P, c.cand[i]);
-  }
-  // reduce the packed per-thread counts: warp shuffles, then one smem atomic per warp
-#pragma unroll
-  for (int w = 0; w < 4; ++w) {
-    for (int o = 16; o > 0; o >>= 1) {
-      tot[w] += __shfl_xor_sync(~0u, tot[w], o);
-      cnt[w] += __shfl_xor_sync(~0u, cnt[w], o);
-    }
-  }
-  if (lane < NSEG) {
-    const int w = lane >> 2, f = (lane & 3) * 16;
-    uint64_t tv = w == 0 ? tot[0] : w == 1 ? tot[1] : w == 2 ? tot[2] : tot[3];
-    uint64_t cv = w == 0 ? cnt[0] : w == 1 ? cnt[1] : w == 2 ? cnt[2] : cnt[3];
-    const uint32_t t16 = (uint32_t)((tv >> f) & 0xFFFFu), c16 = (uint32_t)((cv >> f) & 0xFFFFu);
-    if (t16) atomicAdd(&s.segtot[lane], t16);
-    if (c16) atomicAdd(&s.cnt[lane], c16);
   }
 }
 
@@ -474,7 +470,6 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
   const int tid = threadIdx.x, lane = tid & 31;
   Cand* gdst = d.gcand + c.base;
   unsigned char* buf = reinterpret_cast<unsigned char*>(c.cand);
-  uint64_t tot[4] = {0, 0, 0, 0}, cnt[4] = {0, 0, 0, 0};
   const uint64_t ntiles = (hi - lo + BTILE - 1) / BTILE;
   uint64_t* full = &s.mbar[0];
   uint64_t* empty = &s.mbar[8];
@@ -500,15 +495,7 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     for (uint64_t t = 0; t < ntiles && t < (uint64_t)BSTAGES; ++t) issue_tile(t);
   }
-  // thresholds as doubles (STRUCT: P) for the division-free prefilter
-  double* thrD = reinterpret_cast<double*>(&s.wpfx[0]);   // 16 doubles of scratch
-  if (tid < NSEG) {
-    const uint64_t T = P.thr[tid];
-    thrD[tid] = (T == ~0ull || tid == 0) ? __longlong_as_double(0x7ff0000000000000ll) : from_obits(T);
-  }
   cta_sync();
-  const double inflate = 1.0 + 0x1p-40;
-  const float gamf = (float)P.gamma;
   for (uint64_t t = 0; t < ntiles; ++t) {
     const int st = (int)(t % BSTAGES);
     const uint32_t par = (uint32_t)((t / BSTAGES) & 1);
@@ -530,44 +517,21 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
     if (lane == 0) mbar_arrive(&empty[st]);   // this warp is done reading stage st
 #pragma unroll
     for (int u = 0; u < BTILE / NT; ++u) {
-      const uint32_t k = (uint32_t)(u * NT + tid);
-      const uint32_t meta = mv[u];
-      const uint64_t key = kv[u];
-      bool take = false;
-      uint32_t q = 0, seg = 0;
-      if ((meta & (M_LIVE | M_PIN)) == M_LIVE) {
-        q = meta_q(meta);
-        const uint32_t tau = meta_tau(meta);
-        seg = seg_of(q, tau);
-        pk_add(tot, seg);
-        if (q == Q_STRUCT) {
-          // prefilter (a superset of P <= T) with a lower bound of p; exact P below
-          double dt = __dsub_rn(P.now, from_obits(key));
-          if (dt < P.dt_eps) dt = P.dt_eps;
-          take = __dmul_rn(P.cw[10 + tau], p_struct_lo(meta_lrq(meta), gamf)) <=
-                 __dmul_rn(__dmul_rn(thrD[seg], dt), inflate);
-        } else {                          // EF (ntok, id) / multi-turn obits(last)
-          take = key <= P.thr[seg];
-        }
-        if (take) pk_add(cnt, seg);
-      }
+      const bool take = (mv[u] & (M_LIVE | M_PIN)) == M_LIVE && cand_test(s, mv[u], kv[u]);
       const uint32_t bal = __ballot_sync(~0u, take);
       if (bal) {                          // CTA-local list of candidate slots (smem)
         uint32_t basep = 0;
         if (lane == 0) basep = atomicAdd(&s.nw, (unsigned)__popc(bal));
         basep = __shfl_sync(~0u, basep, 0);
         if (take) {
+          const uint32_t sl = (uint32_t)(t0 + u * NT + tid);
           const uint32_t w = basep + __popc(bal & ((1u << lane) - 1u));
           if (w < WCAP) {
-            s.rhist[w] = (uint32_t)(t0 + k);
+            s.rhist[w] = sl;
           } else {                        // list full (rare): append to the group buffer directly
-            Cand x;
-            x.ss = (uint32_t)(t0 + k) | ((q == Q_EF ? 0u : 1u) << 28);
-            x.seg = seg;
-            x.k0 = q == Q_EF ? key : 0ull;
-            x.k1 = q == Q_EF ? 0ull : key;
-            x.k2 = 0;
+            Cand x = make_cand(mv[u], kv[u], sl);
             finalize_key(d, c.base, P, x);
+            atomicAdd(&s.cnt[x.seg], 1u);
             gdst[atomicAdd(&c.ctl->ncand, 1u)] = x;
           }
         }
@@ -596,32 +560,10 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
   const uint32_t gb0 = s.gbase;
   for (uint32_t i = tid; i < nl; i += NT) {
     const uint32_t sl = s.rhist[i];
-    const uint32_t meta = __ldcg(d.bmeta + c.base + sl);
-    const uint64_t key = __ldcg(d.bkey + c.base + sl);
-    const uint32_t q = meta_q(meta);
-    Cand x;
-    x.ss = sl | ((q == Q_EF ? 0u : 1u) << 28);
-    x.seg = seg_of(q, meta_tau(meta));
-    x.k0 = q == Q_EF ? key : 0ull;
-    x.k1 = q == Q_EF ? 0ull : key;
-    x.k2 = 0;
+    Cand x = make_cand(__ldcg(d.bmeta + c.base + sl), __ldcg(d.bkey + c.base + sl), sl);
     finalize_key(d, c.base, P, x);
+    atomicAdd(&s.cnt[x.seg], 1u);
     gdst[gb0 + i] = x;
-  }
-#pragma unroll
-  for (int w = 0; w < 4; ++w) {
-    for (int o = 16; o > 0; o >>= 1) {
-      tot[w] += __shfl_xor_sync(~0u, tot[w], o);
-      cnt[w] += __shfl_xor_sync(~0u, cnt[w], o);
-    }
-  }
-  if (lane < NSEG) {
-    const int w = lane >> 2, f = (lane & 3) * 16;
-    uint64_t tv = w == 0 ? tot[0] : w == 1 ? tot[1] : w == 2 ? tot[2] : tot[3];
-    uint64_t cv = w == 0 ? cnt[0] : w == 1 ? cnt[1] : w == 2 ? cnt[2] : cnt[3];
-    const uint32_t t16 = (uint32_t)((tv >> f) & 0xFFFFu), c16 = (uint32_t)((cv >> f) & 0xFFFFu);
-    if (t16) atomicAdd(&s.segtot[lane], t16);
-    if (c16) atomicAdd(&s.cnt[lane], c16);
   }
 }
 
@@ -637,7 +579,7 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
   uint64_t lo, hi;
   switch (cmd) {
     case CMD_SCAN: {
-      if (tid < 16) { s.segtot[tid] = 0; s.cnt[tid] = 0; }
+      if (tid < 16) s.cnt[tid] = 0;
       if (tid == 0) { s.ncand = 0; s.nw = 0; }
       cta_sync();
       ScanP P;
@@ -657,6 +599,10 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
       P.gamma = leader ? s.st.par.gamma : __ldcg(&g->gamma);
       P.dt_eps = d.dt_eps;
       P.z_cut = d.z_cut;
+      if (c.GP == 1 || !leader) {
+        build_thr_table(s, P);
+        cta_sync();
+      }
       if (c.GP > 1) {
         // the leader's smem holds the candidates: workers 1..GP-1 split the pool in
         // 4-slot-aligned slices and stream it through shared memory
@@ -674,10 +620,7 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
         scan_range(c, lo, hi, P);
       }
       cta_sync();
-      if (!d.cand_smem && tid < NSEG) {
-        if (s.segtot[tid]) atomicAdd(&g->segtot[tid], s.segtot[tid]);
-        if (s.cnt[tid]) atomicAdd(&g->cnt[tid], s.cnt[tid]);
-      }
+      if (!d.cand_smem && tid < NSEG && s.cnt[tid]) atomicAdd(&g->cnt[tid], s.cnt[tid]);
       break;
     }
     case CMD_HIST: {   // radix histograms of the active segments' keys (global candidates)
@@ -1084,7 +1027,7 @@ __device__ void radix_select(const Cand* a, uint32_t n, bool per_seg, uint32_t a
   for (uint32_t i0 = 0; i0 < n; i0 += NT) {          // a reference key per class
     const uint32_t i = i0 + tid;
     if (i < n) {
-      const Cand& x = a[i];
+      const Cand x = a[i];
       const uint32_t g = per_seg ? x.seg : 0u;
       if (g < 16 && ((active >> g) & 1u) && (tie == 0 || (x.k0 == K0 && (tie == 1 || x.k1 == K1)))) {
         const uint64_t key = per_seg ? seg_key(x) : (tie == 0 ? x.k0 : tie == 1 ? x.k1 : (uint64_t)x.k2);
@@ -1098,7 +1041,7 @@ __device__ void radix_select(const Cand* a, uint32_t n, bool per_seg, uint32_t a
     uint32_t g = 0xFFFFFFFFu;
     uint64_t dx = 0;
     if (i < n) {
-      const Cand& x = a[i];
+      const Cand x = a[i];
       const uint32_t gg = per_seg ? x.seg : 0u;
       if (gg < 16 && ((active >> gg) & 1u) && (tie == 0 || (x.k0 == K0 && (tie == 1 || x.k1 == K1)))) {
         const uint64_t key = per_seg ? seg_key(x) : (tie == 0 ? x.k0 : tie == 1 ? x.k1 : (uint64_t)x.k2);
@@ -1137,7 +1080,7 @@ __device__ void radix_select(const Cand* a, uint32_t n, bool per_seg, uint32_t a
       const uint32_t i = i0 + tid;
       uint32_t bin = 0xFFFFFFFFu;
       if (i < n) {
-        const Cand& x = a[i];
+        const Cand x = a[i];
         const uint32_t g = per_seg ? x.seg : 0u;
         const bool in_tie = tie == 0 || (x.k0 == K0 && (tie == 1 || x.k1 == K1));
         if (g < 16 && ((active >> g) & 1u) && in_tie) {
@@ -1195,7 +1138,7 @@ __device__ void stage_victims(Ctx& c, uint32_t nc, uint64_t Ub) {
     uint64_t key = ~0ull;
     bool take = false;
     if (i < nc) {
-      const Cand& x = c.cand[i];
+      const Cand x = c.cand[i];
       // EF grows within its threshold's num_tokens band: min over that band only
       if (x.seg != 0 || (x.k0 >> 32) == (st.thr[0] >> 32)) { g = x.seg; key = seg_key(x); }
       take = x.k0 <= Ub;
@@ -1239,6 +1182,8 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
   const bool gm = !d.cand_smem;
   uint32_t e = 0, mp = 0, c0 = 0;
   bool staged = false;
+  // live, unpinned blocks per segment (maintained counts minus this round's pins)
+  if (tid < 16) s.segtot[tid] = tid < NSEG ? st.segcnt[tid] - s.pincnt[tid] : 0u;
   for (int attempt = 0; attempt < 3; ++attempt) {
     if (tid < 16) { s.used[tid] = 0; }
     if (tid == 0) {
@@ -1247,7 +1192,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
       if (gm) {
         g->ncand = 0;
         g->now = now;
-        for (int i = 0; i < 16; ++i) { g->segtot[i] = 0; g->cnt[i] = 0; g->thr[i] = st.thr[i]; }
+        for (int i = 0; i < 16; ++i) { g->cnt[i] = 0; g->thr[i] = st.thr[i]; }
         for (int q = 0; q < 3; ++q) for (int t = 0; t < 5; ++t) g->cw[q][t] = s.cw[q][t];
         for (int i = 0; i < 2; ++i) { g->mu[i] = st.par.mu[i]; g->sigma[i] = st.par.sigma[i]; }
         g->gamma = st.par.gamma;
@@ -1258,7 +1203,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
     issue(c, CMD_SCAN);
     if (tid == 0) { const uint64_t t1 = gtimer(); st.tph[1] += t1 - t0; t0 = t1; }
     if (gm) {            // gather the group's counts; bring the candidates into smem
-      if (tid < 16) { s.segtot[tid] = __ldcg(&g->segtot[tid]); s.cnt[tid] = __ldcg(&g->cnt[tid]); }
+      if (tid < 16) s.cnt[tid] = __ldcg(&g->cnt[tid]);
       if (tid == 0) s.ncand = __ldcg(&g->ncand);
       cta_sync();
       const uint32_t e0 = min(m, s.segtot[0]);
@@ -1385,7 +1330,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
       uint32_t g = 0xFFFFFFFFu;
       uint64_t key = ~0ull;
       if (i < nc) {
-        const Cand& x = c.cand[i];
+        const Cand x = c.cand[i];
         // EF grows within its threshold's num_tokens band: min over that band only
         if (x.seg != 0 || (x.k0 >> 32) == (st.thr[0] >> 32)) { g = x.seg; key = seg_key(x); }
       }
@@ -1402,7 +1347,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
     }
     bool take = false;
     if (i < nc) {
-      const Cand& x = c.cand[i];
+      const Cand x = c.cand[i];
       take = x.k0 < Kth || (x.k0 == Kth && (x.k1 < K1th || (x.k1 == K1th && (uint64_t)x.k2 <= K2th)));
     }
     const uint32_t bal = __ballot_sync(~0u, take);
@@ -1573,6 +1518,7 @@ __device__ void apply_chunk(Ctx& c, uint32_t m, uint32_t* vids_out) {
       int32_t pos = tbl_find_pos(tkey, d.tmask, H);
       if (pos >= 0) tkey[pos] = KEY_TOMB;
       d.bmeta[gi] = 0;
+      atomicSub(&st.segcnt[seg_of_tix(meta_tix(meta))], 1u);
       if (tau < 5) atomicAdd((unsigned long long*)&st.ts_ev[tau], 1ull);
       if (q != Q_EF) atomicAdd((unsigned long long*)&st.qe[q - 1], 1ull);
       atomicAdd((unsigned long long*)&st.evict_by_queue[q], 1ull);
@@ -1637,6 +1583,7 @@ __device__ void load_state(Ctx& c) {
   const uint32_t* src = reinterpret_cast<const uint32_t*>(d.st + c.r);
   uint32_t* dst = reinterpret_cast<uint32_t*>(&c.s->st);
   for (int i = threadIdx.x; i < (int)(sizeof(RState) / 4); i += NT) dst[i] = __ldcg(src + i);
+  if (threadIdx.x < 16) c.s->pincnt[threadIdx.x] = 0;
   cta_sync();
   recompute_cw(*c.s);
   cta_sync();
@@ -1687,6 +1634,7 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
     s.npin = 0;
     s.matched = 0;
   }
+  if (threadIdx.x < 16) s.pincnt[threadIdx.x] = 0;
   cta_sync();
   const uint32_t stamp = (uint32_t)st.round;
   uint64_t tA = gtimer();
@@ -1737,8 +1685,12 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
         // O7/O8 touch: last = now, hint overwritten (A9, A10)
         d.blast[gi] = now;
         d.bkey[gi] = scan_key(q, meta_ntok(meta), q == Q_EF ? d.bid[gi] : 0u, now);
+        const uint32_t tix = tix_of(q, tau, j, omax);
         d.bmeta[gi] = meta_pack(q, tau, meta_ntok(meta)) | M_PIN |       // pinned for this round (A11)
-                      (lrq_of(j, omax) << M_LRQ_SHIFT);
+                      (tix << M_TIX_SHIFT);
+        const uint32_t so = seg_of_tix(meta_tix(meta)), sn = seg_of_tix(tix);
+        if (so != sn) { atomicSub(&st.segcnt[so], 1u); atomicAdd(&st.segcnt[sn], 1u); }
+        atomicAdd(&s.pincnt[sn], 1u);
         d.bob[gi] = j;
         d.bomax[gi] = omax;
       } else if (j >= h) {  // O9 miss-after-evict, consumed (A30)
@@ -1813,7 +1765,9 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
     d.bid[gi] = (uint32_t)(st.next_id + rk);
     d.bacc[gi] = 1;
     d.bkey[gi] = scan_key(q, b.ntok[bo + j], (uint32_t)(st.next_id + rk), now);
-    d.bmeta[gi] = meta_pack(q, tau, b.ntok[bo + j]) | (lrq_of(j, omax) << M_LRQ_SHIFT);
+    const uint32_t tix = tix_of(q, tau, j, omax);
+    d.bmeta[gi] = meta_pack(q, tau, b.ntok[bo + j]) | (tix << M_TIX_SHIFT);
+    atomicAdd(&st.segcnt[seg_of_tix(tix)], 1u);
     d.bob[gi] = j;
     d.bomax[gi] = omax;
     tbl_insert(tkey, tval, d.tmask, H, sl, &st.tbl_used);

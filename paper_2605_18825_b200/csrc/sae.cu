@@ -46,9 +46,10 @@ constexpr double INV_SQRT2 = 0.70710678118654757;  // 0x3FE6A09E667F3BCD
 
 enum { Q_EF = 0, Q_CHAT = 1, Q_AGENT = 2, Q_STRUCT = 3 };
 enum { M_LIVE = 1u << 10, M_PIN = 1u << 11 };
-// meta bits 16..31: q16 = floor(-ln(o_b/o_max) * 4096) (0xFFFF for o_b = 0), the STRUCT
-// prefilter's gamma-independent input; -q16/4096 is an upper bound of ln(o_b/o_max).
-constexpr uint32_t M_LRQ_SHIFT = 16;
+// meta bits 12..23: tix, the block's entry in the per-pass candidacy table: its segment
+// (0 EF, 1..8 multi-turn classes) or, for STRUCT, 16 + (tau & 3) * 256 + q8 with
+// q8 = floor(-ln(o_b/o_max) * 32) (255 for o_b = 0): -q8/32 is an upper bound of ln(o_b/o_max).
+constexpr uint32_t M_TIX_SHIFT = 12;
 
 __host__ __device__ inline uint32_t meta_pack(uint32_t q, uint32_t tau, uint32_t ntok) {
   return q | (tau << 2) | (ntok << 5) | M_LIVE;
@@ -77,11 +78,12 @@ struct RState {
   uint64_t select_narrow, select_raw;
   uint64_t tph[16];         // leader phase timers (ns): probe, scan, narrow, select, apply, learn, insert, rebuild,
                             // + issue(): start barrier, own partition, end barrier, (spare)
+  uint32_t segcnt[16];     // live blocks per segment (maintained at insert / touch / evict)
   uint64_t thr[16];        // per-segment candidate thresholds on k0 (heuristic; exactness never depends on them)
   sae_params par;
 };
 
-struct Cand {           // one candidate victim: sort key (tier, k0, k1, k2) + slot + segment
+struct alignas(16) Cand {  // one candidate victim: sort key (tier, k0, k1, k2) + slot + segment
   uint64_t k0, k1;
   uint32_t k2, ss;      // ss = slot | tier << 28
   uint32_t seg, pad;
@@ -216,22 +218,28 @@ __device__ double p_struct(uint32_t ob, uint32_t omax, double gam) {
   double r = __ddiv_rn((double)ob, (double)omax);
   return __dsub_rn(1.0, dm::ex(__dmul_rn(gam, dm::ln(r))));
 }
-// gamma-independent per-block input of the STRUCT prefilter, stored in meta bits 16..31:
-// q16 = floor(-ln(o_b/o_max) * 4096) (an upper bound -q16/4096 of ln(o_b/o_max), so the
-// bound below stays a lower bound of p); 0xFFFF encodes o_b = 0 (ln = -inf, p = 1).
-__device__ __forceinline__ uint32_t lrq_of(uint32_t ob, uint32_t omax) {
-  if (ob == 0) return 0xFFFFu;
-  const double x = -dm::ln(__ddiv_rn((double)ob, (double)omax)) * 4096.0;
+// gamma-independent per-block input of the STRUCT prefilter (meta tix): q8 with
+// -q8/32 >= ln(o_b/o_max), so the bound below stays a lower bound of p; 255 encodes o_b = 0.
+__device__ __forceinline__ uint32_t q8_of(uint32_t ob, uint32_t omax) {
+  if (ob == 0) return 255u;
+  const double x = -dm::ln(__ddiv_rn((double)ob, (double)omax)) * 32.0;
   const double f = floor(x * (1.0 - 0x1p-40));     // never rounds past the true value
-  return (uint32_t)fmin(fmax(f, 0.0), 65534.0);
+  return (uint32_t)fmin(fmax(f, 0.0), 254.0);
 }
-__device__ __forceinline__ uint32_t meta_lrq(uint32_t m) { return m >> M_LRQ_SHIFT; }
+__device__ __forceinline__ uint32_t tix_of(uint32_t q, uint32_t tau, uint32_t ob, uint32_t omax) {
+  if (q == Q_EF) return 0u;
+  if (q != Q_STRUCT) return 1u + (q - 1u) * 4u + (tau & 3u);
+  return 16u + ((tau & 3u) << 8) + q8_of(ob, omax);
+}
+__device__ __forceinline__ uint32_t meta_tix(uint32_t m) { return (m >> M_TIX_SHIFT) & 0xFFFu; }
+// segment of a table index: EF 0, multi-turn classes 1..8, STRUCT classes 9..12
+__device__ __forceinline__ uint32_t seg_of_tix(uint32_t tix) { return tix < 16u ? tix : 9u + ((tix - 16u) >> 8); }
 // A guaranteed lower bound of Eq.(2)'s p = 1 - exp(gamma * ln(o/o_max)) (gamma > 0) from
-// q16: fp32 exp (relative error < 1e-5 over the argument range) inflated by 2^-10.  Used
+// q8: fp32 exp (relative error < 1e-5 over the argument range) inflated by 2^-10.  Used
 // only to decide which STRUCT blocks need their exact score; never to order them.
-__device__ __forceinline__ double p_struct_lo(uint32_t q16, float gam) {
-  if (q16 == 0xFFFFu) return 1.0 - 0x1p-10;
-  const double e = (double)__expf(-gam * ((float)q16 * (1.0f / 4096.0f)));
+__device__ __forceinline__ double p_struct_lo8(uint32_t q8, float gam) {
+  if (q8 == 255u) return 1.0 - 0x1p-10;
+  const double e = (double)__expf(-gam * ((float)q8 * (1.0f / 32.0f)));
   return 1.0 - fmin(1.0, e * (1.0 + 0x1p-10));
 }
 // scan key of a block (see Dev::bkey)
