@@ -151,7 +151,7 @@ struct Smem {
   uint64_t pfx[16], pmask[16];
   uint32_t below[16], target[16], binc[16];
   unsigned long long kmin[16];
-  unsigned long long drefs[16], dors[16];  // radix_select: first key per class; OR of key differences
+  unsigned long long drefs[16], dors[16];  // radix_select: AND / OR of each class's keys
   uint32_t nv, nw;          // nw: this CTA's candidates awaiting finalize_key (global mode)
   uint32_t cseq, wcmd;      // leader: commands posted this launch; worker: command to run
   uint32_t gbase;           // worker: this CTA's reservation in the group candidate buffer
@@ -692,7 +692,7 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
       for (uint64_t sl = lo + tid; sl < hi; sl += NT) {
         const uint64_t gi = c.base + sl;
         if (__ldcg(d.bmeta + gi) & M_LIVE)
-          tbl_insert(keys, vals, d.tmask, __ldcg(d.bhash + gi), (uint32_t)sl, &g->tblcnt);
+          d.btpos[gi] = tbl_insert(keys, vals, d.tmask, __ldcg(d.bhash + gi), (uint32_t)sl, &g->tblcnt);
       }
       break;
     }
@@ -773,7 +773,7 @@ __device__ void worker_loop(Ctx& c) {
     if (threadIdx.x == 0) {
       const unsigned long long want = cmd_tag(c.d->epoch, seq);
       unsigned long long w;
-      while (((w = ld_acquire_u64(&c.ctl->cmdw)) >> 8) != want) __nanosleep(20);
+      while (((w = ld_acquire_u64(&c.ctl->cmdw)) >> 8) != want) __nanosleep(128);
       c.s->wcmd = (unsigned)(w & 0xFFu);
     }
     cta_sync();
@@ -1021,41 +1021,37 @@ __device__ void radix_select(const Cand* a, uint32_t n, bool per_seg, uint32_t a
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid < 16) { s.pfx[tid] = 0; s.pmask[tid] = 0; s.below[tid] = 0; }
   // The digits above the highest bit in which two keys of one class differ are common to
-  // the whole class: start below them (per class: OR of key ^ the class's first key).
-  if (tid < 16) { s.drefs[tid] = ~0ull; s.dors[tid] = 0ull; }
-  cta_sync();
-  for (uint32_t i0 = 0; i0 < n; i0 += NT) {          // a reference key per class
-    const uint32_t i = i0 + tid;
-    if (i < n) {
-      const Cand x = a[i];
-      const uint32_t g = per_seg ? x.seg : 0u;
-      if (g < 16 && ((active >> g) & 1u) && (tie == 0 || (x.k0 == K0 && (tie == 1 || x.k1 == K1)))) {
-        const uint64_t key = per_seg ? seg_key(x) : (tie == 0 ? x.k0 : tie == 1 ? x.k1 : (uint64_t)x.k2);
-        if (s.drefs[g] == ~0ull) atomicCAS(&s.drefs[g], ~0ull, (unsigned long long)key);
-      }
-    }
-  }
+  // the whole class: start below them.  Differing bits = OR(keys) ^ AND(keys) per class
+  // (one pass: lanes of one class reduce together, one smem atomic per group).
+  if (tid < 16) { s.drefs[tid] = ~0ull; s.dors[tid] = 0ull; }   // drefs: AND, dors: OR
   cta_sync();
   for (uint32_t i0 = 0; i0 < n; i0 += NT) {
     const uint32_t i = i0 + tid;
     uint32_t g = 0xFFFFFFFFu;
-    uint64_t dx = 0;
+    uint64_t key = 0;
     if (i < n) {
       const Cand x = a[i];
       const uint32_t gg = per_seg ? x.seg : 0u;
       if (gg < 16 && ((active >> gg) & 1u) && (tie == 0 || (x.k0 == K0 && (tie == 1 || x.k1 == K1)))) {
-        const uint64_t key = per_seg ? seg_key(x) : (tie == 0 ? x.k0 : tie == 1 ? x.k1 : (uint64_t)x.k2);
+        key = per_seg ? seg_key(x) : (tie == 0 ? x.k0 : tie == 1 ? x.k1 : (uint64_t)x.k2);
         g = gg;
-        dx = key ^ s.drefs[gg];
       }
     }
     const uint32_t peers = __match_any_sync(~0u, g);
     if (g != 0xFFFFFFFFu) {
-      const uint32_t ohi = __reduce_or_sync(peers, (uint32_t)(dx >> 32));
-      const uint32_t olo = __reduce_or_sync(peers, (uint32_t)dx);
-      if (lane == __ffs(peers) - 1 && (ohi | olo)) atomicOr(&s.dors[g], ((unsigned long long)ohi << 32) | olo);
+      const uint32_t ohi = __reduce_or_sync(peers, (uint32_t)(key >> 32));
+      const uint32_t olo = __reduce_or_sync(peers, (uint32_t)key);
+      const uint32_t ahi = __reduce_and_sync(peers, (uint32_t)(key >> 32));
+      const uint32_t alo = __reduce_and_sync(peers, (uint32_t)key);
+      if (lane == __ffs(peers) - 1) {
+        atomicOr(&s.dors[g], ((unsigned long long)ohi << 32) | olo);
+        atomicAnd(&s.drefs[g], ((unsigned long long)ahi << 32) | alo);
+      }
     }
   }
+  cta_sync();
+  if (tid < 16)                                   // differing bits (0 for an empty class)
+    s.dors[tid] = (s.dors[tid] == 0ull && s.drefs[tid] == ~0ull) ? 0ull : (s.dors[tid] ^ s.drefs[tid]);
   cta_sync();
   int top = 0;
   for (int g = 0; g < 16; ++g)
@@ -1162,6 +1158,20 @@ __device__ void stage_victims(Ctx& c, uint32_t nc, uint64_t Ub) {
   }
   cta_sync();
   const uint32_t nv = min(s.nv, (uint32_t)VCAP);
+  if (nv <= (uint32_t)NT) {
+    // rank placement: (k0, k1, k2) is a total order without ties (ids are unique), so each
+    // staged record's rank is the number of smaller ones -- no barriers inside the count
+    Cand x;
+    uint32_t rank = 0;
+    if ((uint32_t)tid < nv) {
+      x = c.vbuf[tid];
+      for (uint32_t j = 0; j < nv; ++j) rank += cand_less(c.vbuf[j], x) ? 1u : 0u;
+    }
+    cta_sync();
+    if ((uint32_t)tid < nv) c.vbuf[rank] = x;
+    cta_sync();
+    return;
+  }
   int N = 32;
   while ((uint32_t)N < nv) N <<= 1;
   for (uint32_t i = nv + tid; i < (uint32_t)N; i += NT) {
@@ -1507,42 +1517,43 @@ __device__ void apply_chunk(Ctx& c, uint32_t m, uint32_t* vids_out) {
   const uint64_t gb = (uint64_t)c.r * d.G;
   for (uint32_t v0 = 0; v0 < m; v0 += d.G) {
     const uint32_t mb = min(m - v0, d.G);
-    // phase 1: remove from the resident table, count, expire ghost slots
-    for (uint32_t v = threadIdx.x; v < mb; v += NT) {
-      const uint32_t sl = c.cand[v0 + v].ss & SLOT_MASK;
-      const uint64_t gi = c.base + sl;
-      const uint64_t H = d.bhash[gi];
-      const uint32_t meta = d.bmeta[gi];
-      const uint32_t q = meta_q(meta), tau = meta_tau(meta);
-      if (vids_out) vids_out[v0 + v] = d.bid[gi];
-      int32_t pos = tbl_find_pos(tkey, d.tmask, H);
-      if (pos >= 0) tkey[pos] = KEY_TOMB;
-      d.bmeta[gi] = 0;
-      atomicSub(&st.segcnt[seg_of_tix(meta_tix(meta))], 1u);
-      if (tau < 5) atomicAdd((unsigned long long*)&st.ts_ev[tau], 1ull);
-      if (q != Q_EF) atomicAdd((unsigned long long*)&st.qe[q - 1], 1ull);
-      atomicAdd((unsigned long long*)&st.evict_by_queue[q], 1ull);
-      atomicAdd((unsigned long long*)&st.evict_by_type[tau], 1ull);
-      const uint32_t p = (uint32_t)((st.gseq + v0 + v) % d.G);
-      if (d.glive[gb + p]) {  // FIFO expiry of the oldest ghost (A30)
-        gkey[d.gtslot[gb + p]] = KEY_TOMB;
-        d.glive[gb + p] = 0;
+    // phase 1: remove from the resident table (position kept in the SoA: no probe), count,
+    // expire the ghost slots; all loads of a victim are independent (one round trip)
+    for (uint32_t vb = 0; vb < mb; vb += NT) {
+      const uint32_t v = vb + threadIdx.x;
+      uint64_t H = 0;
+      uint32_t p = 0, sl = 0;
+      if (v < mb) {
+        sl = c.cand[v0 + v].ss & SLOT_MASK;
+        const uint64_t gi = c.base + sl;
+        p = (uint32_t)((st.gseq + v0 + v) % d.G);
+        H = d.bhash[gi];
+        const uint32_t meta = d.bmeta[gi];
+        const uint32_t tp = d.btpos[gi];
+        const uint8_t glv = d.glive[gb + p];
+        const uint32_t gts = d.gtslot[gb + p];
+        const uint32_t q = meta_q(meta), tau = meta_tau(meta);
+        if (vids_out) vids_out[v0 + v] = d.bid[gi];
+        tkey[tp] = KEY_TOMB;
+        d.bmeta[gi] = 0;
+        atomicSub(&st.segcnt[seg_of_tix(meta_tix(meta))], 1u);
+        if (tau < 5) atomicAdd((unsigned long long*)&st.ts_ev[tau], 1ull);
+        if (q != Q_EF) atomicAdd((unsigned long long*)&st.qe[q - 1], 1ull);
+        atomicAdd((unsigned long long*)&st.evict_by_queue[q], 1ull);
+        atomicAdd((unsigned long long*)&st.evict_by_type[tau], 1ull);
+        if (glv) gkey[gts] = KEY_TOMB;   // FIFO expiry of the oldest ghost (A30)
+        d.ghash[gb + p] = H;
+        d.gtau[gb + p] = (uint8_t)tau;
       }
-      d.ghash[gb + p] = H;
-      d.gtau[gb + p] = (uint8_t)tau;
+      cta_sync();
+      // phase 2: ghost push (recently_evicted[hash] = tau), free the slot
+      if (v < mb) {
+        d.glive[gb + p] = 1;
+        d.gtslot[gb + p] = tbl_insert(gkey, gval, d.gmask, H, p, &st.gtbl_used);
+        d.freestk[c.base + st.free_top + v0 + v] = sl;
+      }
+      cta_sync();
     }
-    cta_sync();
-    // phase 2: ghost push (recently_evicted[hash] = tau), free the slot
-    for (uint32_t v = threadIdx.x; v < mb; v += NT) {
-      const uint32_t sl = c.cand[v0 + v].ss & SLOT_MASK;
-      const uint64_t gi = c.base + sl;
-      const uint32_t p = (uint32_t)((st.gseq + v0 + v) % d.G);
-      const uint64_t H = d.ghash[gb + p];
-      d.glive[gb + p] = 1;
-      d.gtslot[gb + p] = tbl_insert(gkey, gval, d.gmask, H, p, &st.gtbl_used);
-      d.freestk[c.base + st.free_top + v0 + v] = sl;
-    }
-    cta_sync();
     if (threadIdx.x == 0) {
       st.free_top += mb;
       st.live -= mb;
@@ -1770,7 +1781,7 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
     atomicAdd(&st.segcnt[seg_of_tix(tix)], 1u);
     d.bob[gi] = j;
     d.bomax[gi] = omax;
-    tbl_insert(tkey, tval, d.tmask, H, sl, &st.tbl_used);
+    d.btpos[gi] = tbl_insert(tkey, tval, d.tmask, H, sl, &st.tbl_used);
   }
   cta_sync();
   if (threadIdx.x == 0) {

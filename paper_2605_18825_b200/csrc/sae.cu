@@ -137,7 +137,7 @@ struct Dev {
   uint32_t* bomax;
   uint64_t* bkey;       // scan key: EF ? (ntok << 32 | id) : obits(last)
   uint32_t* bacc;
-  uint32_t* bpin;
+  uint32_t* btpos;       // the block's position in the resident table (set at insert / rebuild)
   uint32_t* freestk;
   uint64_t* tkey;
   uint32_t* tval;
@@ -441,7 +441,7 @@ __global__ void k_init(Dev d) {
   const uint64_t RC = (uint64_t)d.R * d.C;
   for (uint64_t i = tid; i < RC; i += stride) {
     d.bmeta[i] = 0;
-    d.bpin[i] = 0;
+    d.btpos[i] = 0;
     d.freestk[i] = d.C - 1 - (uint32_t)(i % d.C);
   }
   const uint64_t TBn = (uint64_t)d.R * (d.tmask + 1ull);
@@ -628,7 +628,7 @@ sae_status sae_create(const sae_config* cfg, sae_ctx** out) {
   CK(dalloc(ctx, &d.bomax, RC));
   CK(dalloc(ctx, &d.bkey, RC + 4));   // +4: bulk-copy tail padding
   CK(dalloc(ctx, &d.bacc, RC));
-  CK(dalloc(ctx, &d.bpin, RC));
+  CK(dalloc(ctx, &d.btpos, RC));
   CK(dalloc(ctx, &d.freestk, RC));
   CK(dalloc(ctx, &d.tkey, R * TB));
   CK(dalloc(ctx, &d.tval, R * TB));
