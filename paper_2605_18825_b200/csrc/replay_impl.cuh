@@ -387,10 +387,18 @@ __device__ void scan_range(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P) {
             if (x.seg != 0) note_cand(c, P, gdst, pos);
           }
         }
-      } else if (take) {
-        const Cand x = make_cand(meta, kt[u], (uint32_t)(s0 + u));
-        atomicAdd(&s.cnt[x.seg], 1u);
-        c.cand[atomicAdd(&s.ncand, 1u)] = x;
+      } else {
+        const uint32_t bal = __ballot_sync(~0u, take);
+        if (bal) {
+          uint32_t basep = 0;
+          if (lane == 0) basep = atomicAdd(&s.ncand, (unsigned)__popc(bal));
+          basep = __shfl_sync(~0u, basep, 0);
+          if (take) {
+            const Cand x = make_cand(meta, kt[u], (uint32_t)(s0 + u));
+            atomicAdd(&s.cnt[x.seg], 1u);
+            c.cand[basep + __popc(bal & ((1u << lane) - 1u))] = x;
+          }
+        }
       }
     }
 #pragma unroll
@@ -710,7 +718,8 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
       uint32_t* vals = d.gval + (uint64_t)c.r * gt;
       for (uint64_t p = lo + tid; p < hi; p += NT)
         if (__ldcg(d.glive + gb + p))
-          d.gtslot[gb + p] = tbl_insert(keys, vals, d.gmask, __ldcg(d.ghash + gb + p), (uint32_t)p, &g->gtblcnt);
+          d.gtslot[gb + p] = tbl_insert(keys, vals, d.gmask, __ldcg(d.ghash + gb + p),
+                                        (uint32_t)p | ((uint32_t)__ldcg(d.gtau + gb + p) << 28), &g->gtblcnt);
       break;
     }
     case CMD_COUNTQ: {
@@ -814,10 +823,22 @@ __device__ void rebuild_ghost(Ctx& c) {
 
 // stride-halving tree sum over y[0..P) in smem (SURVEY c.3 TREE)
 __device__ double tree_sum(double* y, int P) {
-  for (int h = P >> 1; h >= 1; h >>= 1) {
+  int h = P >> 1;
+  for (; h >= 32; h >>= 1) {
     for (int i = threadIdx.x; i < h; i += NT) y[i] = __dadd_rn(y[i], y[i + h]);
     cta_sync();
   }
+  // the last levels (h <= 16) inside warp 0 by shuffles: lane i holds y[i]; the same
+  // operands and order as y[i] = y[i] + y[i + h]
+  if (threadIdx.x < 32) {
+    double v = (int)threadIdx.x < P ? y[threadIdx.x] : 0.0;
+    for (; h >= 1; h >>= 1) {
+      const double o = __shfl_down_sync(~0u, v, h);
+      if ((int)threadIdx.x < h) v = __dadd_rn(v, o);
+    }
+    if (threadIdx.x == 0) y[0] = v;
+  }
+  cta_sync();
   double r = y[0];
   cta_sync();
   return r;
@@ -1161,14 +1182,20 @@ __device__ void stage_victims(Ctx& c, uint32_t nc, uint64_t Ub) {
   if (nv <= (uint32_t)NT) {
     // rank placement: (k0, k1, k2) is a total order without ties (ids are unique), so each
     // staged record's rank is the number of smaller ones -- no barriers inside the count
+    // T consecutive lanes share one record and split the count (T = NT / nv rounded down
+    // to a power of two, at most 32), then combine with shuffles
+    uint32_t T = 1;
+    while (T < 32u && T * 2u * max(nv, 1u) <= (uint32_t)NT) T <<= 1;
+    const uint32_t e = (uint32_t)tid / T, r = (uint32_t)tid & (T - 1u);
     Cand x;
     uint32_t rank = 0;
-    if ((uint32_t)tid < nv) {
-      x = c.vbuf[tid];
-      for (uint32_t j = 0; j < nv; ++j) rank += cand_less(c.vbuf[j], x) ? 1u : 0u;
+    if (e < nv) {
+      x = c.vbuf[e];
+      for (uint32_t j = r; j < nv; j += T) rank += cand_less(c.vbuf[j], x) ? 1u : 0u;
     }
+    for (uint32_t o = 1; o < T; o <<= 1) rank += __shfl_xor_sync(~0u, rank, o);
     cta_sync();
-    if ((uint32_t)tid < nv) c.vbuf[rank] = x;
+    if (e < nv && r == 0) c.vbuf[rank] = x;
     cta_sync();
     return;
   }
@@ -1387,11 +1414,11 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
   const uint32_t trim_at = d.trim_at, trim_to = d.trim_to;
   uint32_t shrink = 0;
   for (int g = 0; g < NSEG; ++g) {
-    const uint32_t want = 3 * s.used[g] + SLACK;
+    const uint32_t want = 3 * s.used[g] + d.slack;
     if (s.cnt[g] > trim_at * want) shrink |= 1u << g;
   }
   if (shrink) {
-    if (tid < NSEG) s.target[tid] = trim_to * (3 * s.used[tid] + SLACK);
+    if (tid < NSEG) s.target[tid] = trim_to * (3 * s.used[tid] + d.slack);
     cta_sync();
     radix_select(c.cand, nc, true, shrink, s, 0, 0, 0, 2);   // two digits: a bound, not a rank
     if (tid < NSEG && ((shrink >> tid) & 1u)) st.thr[tid] = min(st.thr[tid], s.pfx[tid] | ~s.pmask[tid]);
@@ -1404,7 +1431,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
     const uint32_t g = tid;
     const uint64_t T = st.thr[g];
     const uint32_t left = s.cnt[g] - min(s.cnt[g], s.used[g]);
-    if (T != ~0ull && s.segtot[g] > s.cnt[g] && left < 2 * s.used[g] + SLACK) {
+    if (T != ~0ull && s.segtot[g] > s.cnt[g] && left < 2 * s.used[g] + d.slack) {
       const uint64_t km = s.kmin[g] == ~0ull ? T : (uint64_t)s.kmin[g];
       uint64_t Tn;
       if (g == 0) {                 // id part only, saturating inside the ntok band
@@ -1522,7 +1549,7 @@ __device__ void apply_chunk(Ctx& c, uint32_t m, uint32_t* vids_out) {
     for (uint32_t vb = 0; vb < mb; vb += NT) {
       const uint32_t v = vb + threadIdx.x;
       uint64_t H = 0;
-      uint32_t p = 0, sl = 0;
+      uint32_t p = 0, sl = 0, tau = 0;
       if (v < mb) {
         sl = c.cand[v0 + v].ss & SLOT_MASK;
         const uint64_t gi = c.base + sl;
@@ -1532,7 +1559,8 @@ __device__ void apply_chunk(Ctx& c, uint32_t m, uint32_t* vids_out) {
         const uint32_t tp = d.btpos[gi];
         const uint8_t glv = d.glive[gb + p];
         const uint32_t gts = d.gtslot[gb + p];
-        const uint32_t q = meta_q(meta), tau = meta_tau(meta);
+        const uint32_t q = meta_q(meta);
+        tau = meta_tau(meta);
         if (vids_out) vids_out[v0 + v] = d.bid[gi];
         tkey[tp] = KEY_TOMB;
         d.bmeta[gi] = 0;
@@ -1549,7 +1577,7 @@ __device__ void apply_chunk(Ctx& c, uint32_t m, uint32_t* vids_out) {
       // phase 2: ghost push (recently_evicted[hash] = tau), free the slot
       if (v < mb) {
         d.glive[gb + p] = 1;
-        d.gtslot[gb + p] = tbl_insert(gkey, gval, d.gmask, H, p, &st.gtbl_used);
+        d.gtslot[gb + p] = tbl_insert(gkey, gval, d.gmask, H, p | (tau << 28), &st.gtbl_used);
         d.freestk[c.base + st.free_top + v0 + v] = sl;
       }
       cta_sync();
@@ -1650,12 +1678,18 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
   const uint32_t stamp = (uint32_t)st.round;
   uint64_t tA = gtimer();
   // ---- O4/O5 classify + probe (Alg.1 Classify P:550-564; strict prefix P:158)
+  // (the first NT blocks' values stay in registers for the next loop: same thread, same j)
+  uint64_t rH = 0;
+  int32_t rsl = -1;
+  uint32_t rq = 0, rtau = 0;
   for (uint32_t j = threadIdx.x; j < n; j += NT) {
     const uint64_t H = b.h[bo + j];
     const uint32_t tau = b.tau[bo + j];
     const int32_t sl = tbl_find(tkey, tval, d.tmask, H);
+    const uint32_t q = classify(tau, mt, ag, cid, j < spb, untempl);
     b.slot[bo + j] = sl;
-    b.q[bo + j] = (uint8_t)classify(tau, mt, ag, cid, j < spb, untempl);
+    b.q[bo + j] = (uint8_t)q;
+    if (j < (uint32_t)NT) { rH = H; rsl = sl; rq = q; rtau = tau; }
     if (sl < 0) atomicMin(&s.h, (int32_t)j);
     else atomicAdd(&s.npin, 1u);
   }
@@ -1669,16 +1703,19 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
     uint32_t fc = 0, fa = 0, fn = 0;
     double lnv = 0.0;
     if (valid) {
-      const int32_t sl = b.slot[bo + j];
-      const uint32_t q = b.q[bo + j], tau = b.tau[bo + j];
+      const bool inreg = j0 == 0;
+      const int32_t sl = inreg ? rsl : b.slot[bo + j];
+      const uint32_t q = inreg ? rq : b.q[bo + j], tau = inreg ? rtau : b.tau[bo + j];
       const uint32_t bin = min(d.nbins - 1, (d.nbins * j) / omax);
       if (tau < 5) atomicAdd((unsigned long long*)&st.ts_acc[tau], 1ull);
       if (q == Q_STRUCT) atomicAdd((unsigned long long*)&st.pb_acc[bin], 1ull);
       if (sl >= 0) {
         const uint64_t gi = c.base + (uint32_t)sl;
         const uint32_t meta = d.bmeta[gi];
+        const double lastv = d.blast[gi];
+        const uint32_t idv = d.bid[gi];
         if (j < h) {  // O7 hit (A9: credited to the old queue before re-routing)
-          double dt = __dsub_rn(now, d.blast[gi]);
+          double dt = __dsub_rn(now, lastv);
           if (dt < d.dt_eps) dt = d.dt_eps;
           const uint32_t qo = meta_q(meta);
           if (qo == Q_CHAT || qo == Q_AGENT) {
@@ -1695,7 +1732,7 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
         }
         // O7/O8 touch: last = now, hint overwritten (A9, A10)
         d.blast[gi] = now;
-        d.bkey[gi] = scan_key(q, meta_ntok(meta), q == Q_EF ? d.bid[gi] : 0u, now);
+        d.bkey[gi] = scan_key(q, meta_ntok(meta), idv, now);
         const uint32_t tix = tix_of(q, tau, j, omax);
         d.bmeta[gi] = meta_pack(q, tau, meta_ntok(meta)) | M_PIN |       // pinned for this round (A11)
                       (tix << M_TIX_SHIFT);
@@ -1705,11 +1742,11 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
         d.bob[gi] = j;
         d.bomax[gi] = omax;
       } else if (j >= h) {  // O9 miss-after-evict, consumed (A30)
-        const uint64_t H = b.h[bo + j];
+        const uint64_t H = inreg ? rH : b.h[bo + j];
         const int32_t gp = tbl_find_pos(gkey, d.gmask, H);
         if (gp >= 0) {
-          const uint32_t rp = gval[gp];
-          const uint32_t gtau = d.gtau[gb + rp];
+          const uint32_t gv = gval[gp];            // ring position | tau << 28
+          const uint32_t rp = gv & SLOT_MASK, gtau = gv >> 28;
           if (gtau < 5) atomicAdd((unsigned long long*)&st.ts_mae[gtau], 1ull);
           atomicAdd((unsigned long long*)&st.mae_by_type[gtau], 1ull);
           gkey[gp] = KEY_TOMB;

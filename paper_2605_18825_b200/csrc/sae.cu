@@ -119,6 +119,7 @@ struct Dev {
   uint32_t epoch;       // launch counter of the ctx (group command words are tagged with it)
   uint32_t cand_smem;   // 1: candidates live in the leader's smem (C <= CAND_MAX, GP == 1)
   uint32_t bulk_ok;     // 1: replica bases are 16-byte aligned (C % 4 == 0): bulk-copy scan
+  uint32_t slack;              // minimum reserve of candidates per segment (env SAE_SLACK; default 32)
   uint32_t trim_at, trim_to;   // threshold trimming: a segment holding > trim_at x its want is
                                // cut to trim_to x want (env SAE_TRIM="at,to"; default 8,4)
   uint32_t scan_l2;     // L2 policy of the streamed scan columns: 1 evict_last (they fit in L2
@@ -671,6 +672,11 @@ sae_status sae_create(const sae_config* cfg, sae_ctx** out) {
   d.bulk_ok = (d.C % 4 == 0) ? 1u : 0u;
   d.trim_at = 8;
   d.trim_to = 4;
+  d.slack = SLACK;
+  if (const char* e = getenv("SAE_SLACK")) {
+    const int v = atoi(e);
+    if (v >= 1 && v <= 1024) d.slack = (uint32_t)v;
+  }
   if (const char* e = getenv("SAE_TRIM")) {
     unsigned a = 0, b = 0;
     if (sscanf(e, "%u,%u", &a, &b) == 2 && a >= 2 && b >= 1 && b < a) { d.trim_at = a; d.trim_to = b; }
