@@ -1033,7 +1033,8 @@ __device__ void narrow(Ctx& c, uint32_t e, uint32_t mp);
 // Global mode: one class (0), key k0.  Per-segment mode: class = segment, key = seg_key.
 __device__ void radix_select(const Cand* a, uint32_t n, bool per_seg, uint32_t active, Smem& s,
                              int tie = 0, uint64_t K0 = 0, uint64_t K1 = 0, int digits = 8,
-                             uint32_t early = 0) {
+                             uint32_t early = 0, int tier = -1) {
+  // tier >= 0 (global mode): only candidates of that tier (0 EF, 1 scored) take part
   // early > 0 (global mode): stop as soon as the chosen bin and everything below it hold at
   // most `early` keys (below[0] + binc[0]); the caller then sorts that prefix set
   // digits < 8: stop after that many 8-bit digits (the rank-target key then lies in
@@ -1053,7 +1054,8 @@ __device__ void radix_select(const Cand* a, uint32_t n, bool per_seg, uint32_t a
     if (i < n) {
       const Cand x = a[i];
       const uint32_t gg = per_seg ? x.seg : 0u;
-      if (gg < 16 && ((active >> gg) & 1u) && (tie == 0 || (x.k0 == K0 && (tie == 1 || x.k1 == K1)))) {
+      if (gg < 16 && ((active >> gg) & 1u) && (tie == 0 || (x.k0 == K0 && (tie == 1 || x.k1 == K1))) &&
+          (tier < 0 || (int)(x.ss >> 28) == tier)) {
         key = per_seg ? seg_key(x) : (tie == 0 ? x.k0 : tie == 1 ? x.k1 : (uint64_t)x.k2);
         g = gg;
       }
@@ -1099,7 +1101,8 @@ __device__ void radix_select(const Cand* a, uint32_t n, bool per_seg, uint32_t a
       if (i < n) {
         const Cand x = a[i];
         const uint32_t g = per_seg ? x.seg : 0u;
-        const bool in_tie = tie == 0 || (x.k0 == K0 && (tie == 1 || x.k1 == K1));
+        const bool in_tie = (tie == 0 || (x.k0 == K0 && (tie == 1 || x.k1 == K1))) &&
+                            (tier < 0 || (int)(x.ss >> 28) == tier);
         if (g < 16 && ((active >> g) & 1u) && in_tie) {
           const uint64_t key = per_seg ? seg_key(x) : (tie == 0 ? x.k0 : tie == 1 ? x.k1 : (uint64_t)x.k2);
           if ((key & s.pmask[g]) == s.pfx[g]) bin = g * 256u + (uint32_t)((key >> shift) & 255u);
@@ -1281,11 +1284,22 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
     staged = false;
     const uint64_t tR = gtimer();
     if (nc >= m) {
-      if (tid == 0) s.target[0] = m;
+      // Stage 1 / Stage 2: if the EF candidates cover all m victims, select
+      // among them only; otherwise every EF candidate is a victim and the rest come from the
+      // scored candidates -- each radix then runs over one tier (narrow key ranges)
+      const uint32_t ef = s.cnt[0];
+      const bool in_ef = ef >= m;
+      if (tid == 0) s.target[0] = in_ef ? m : m - ef;
       cta_sync();
-      radix_select(c.cand, nc, false, 1u, s, 0, 0, 0, 8, VCAP / 2);
+      const uint32_t lim = in_ef ? VCAP / 2 : (ef + 16 < VCAP / 2 ? VCAP / 2 - ef : 16u);
+      radix_select(c.cand, nc, false, 1u, s, 0, 0, 0, 8, lim, in_ef ? 0 : 1);
+      staged = (in_ef ? 0u : ef) + s.below[0] + s.binc[0] <= VCAP;
+      if (!staged) {               // rare: fall back to the exact global rank m
+        if (tid == 0) s.target[0] = m;
+        cta_sync();
+        radix_select(c.cand, nc, false, 1u, s);
+      }
       Kth = s.pfx[0];
-      staged = s.below[0] + s.binc[0] <= VCAP;
     } else {
       staged = true;                     // nc < m <= MSUB < VCAP
     }

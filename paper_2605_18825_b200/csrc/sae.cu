@@ -672,7 +672,7 @@ sae_status sae_create(const sae_config* cfg, sae_ctx** out) {
   d.bulk_ok = (d.C % 4 == 0) ? 1u : 0u;
   d.trim_at = 8;
   d.trim_to = 4;
-  d.slack = SLACK;
+  d.slack = d.cand_smem ? SLACK / 2 : SLACK;   // private pools: rescans are cheap, keep fewer
   if (const char* e = getenv("SAE_SLACK")) {
     const int v = atoi(e);
     if (v >= 1 && v <= 1024) d.slack = (uint32_t)v;
