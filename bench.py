@@ -47,6 +47,10 @@ WORKLOADS = {
                desc="C4 single-turn-dominated templated trace (Table 2 row 10/10/40/25/15), "
                     "4M-block (64 Mi-token) pool, one 148-CTA cooperative replica group per GPU; "
                     "pool pre-filled with the trace's first 100K requests (untimed)"),
+    "c4x": dict(cfg="c4", per_step=2000, ref_step=2, prefill=600_000, capacity=1 << 24,
+                desc="C4 trace on a 2^24-block (256 Mi-token) pool, whose 12-byte scan records "
+                     "(201 MB) exceed L2 (SURVEY 8(d)): one 148-CTA cooperative replica group per "
+                     "GPU; pool pre-filled with the trace's first 600K requests (untimed)"),
     "c5": dict(cfg="c5", per_step=250, ref_step=60,
                desc="C5 parameter-sweep replicas: balanced trace, C=2304, 32 points x seeds, "
                     "replicas per GPU = 1024/N"),
@@ -122,6 +126,8 @@ def make_trace(wl: dict, rank: int, n_requests: int | None = None, seed_shift: i
     if n_requests:
         cfg["n_requests"] = n_requests
     cfg["seed"] = cfg["seed"] + 0x1000 * rank + seed_shift
+    if "capacity" in wl:
+        cfg["capacity"] = wl["capacity"]
     tr = T.generate(cfg)
     T.materialize(tr)
     tr["config"] = cfg

@@ -172,6 +172,8 @@ struct Ctx {               // per-CTA view of one replica (group)
   GroupCtl* ctl;
   uint32_t r, rank, GP;
   uint64_t base;           // r * C
+  const uint64_t* pf_h;    // leader of a group: the next request's block hashes (prefetched
+  uint32_t pf_n;           // into L2 while the workers scan), count
 };
 
 __device__ void recompute_cw(Smem& s) {
@@ -472,6 +474,32 @@ constexpr uint32_t BTILE_BYTES = BTILE * (4 + 8);
 constexpr int BSTAGES = (int)((CAND_MAX * sizeof(Cand)) / BTILE_BYTES) < 6
                             ? (int)((CAND_MAX * sizeof(Cand)) / BTILE_BYTES) : 6;
 static_assert(BSTAGES >= 2, "bulk scan needs two stages");
+__device__ void scan_bulk_begin(Ctx& c, uint64_t lo, uint64_t hi) {
+  const Dev& d = *c.d;
+  Smem& s = *c.s;
+  if (threadIdx.x != 0) return;
+  unsigned char* buf = reinterpret_cast<unsigned char*>(c.cand);
+  const uint64_t ntiles = (hi - lo + BTILE - 1) / BTILE;
+  uint64_t* full = &s.mbar[0];
+  uint64_t* empty = &s.mbar[8];
+  for (int st = 0; st < BSTAGES; ++st) { mbar_init(&full[st], 1); mbar_init(&empty[st], NW); }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  const uint64_t pol = d.scan_l2 ? l2_policy(d.scan_l2) : 0ull;
+  for (uint64_t t = 0; t < ntiles && t < (uint64_t)BSTAGES; ++t) {
+    const uint64_t t0 = lo + t * BTILE;
+    const uint32_t n4 = ((uint32_t)min((uint64_t)BTILE, hi - t0) + 3) & ~3u;
+    unsigned char* b = buf + (size_t)t * BTILE_BYTES;
+    mbar_expect_tx(&full[t], n4 * 12u);
+    if (d.scan_l2) {
+      bulk_g2s_pol(b, d.bmeta + c.base + t0, n4 * 4u, &full[t], pol);
+      bulk_g2s_pol(b + BTILE * 4, d.bkey + c.base + t0, n4 * 8u, &full[t], pol);
+    } else {
+      bulk_g2s(b, d.bmeta + c.base + t0, n4 * 4u, &full[t]);
+      bulk_g2s(b + BTILE * 4, d.bkey + c.base + t0, n4 * 8u, &full[t]);
+    }
+  }
+}
 __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P) {
   const Dev& d = *c.d;
   Smem& s = *c.s;
@@ -497,13 +525,8 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
       bulk_g2s(b + BTILE * 4, d.bkey + c.base + t0, n4 * 8u, &full[st]);
     }
   };
-  if (tid == 0) {
-    for (int st = 0; st < BSTAGES; ++st) { mbar_init(&full[st], 1); mbar_init(&empty[st], NW); }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    for (uint64_t t = 0; t < ntiles && t < (uint64_t)BSTAGES; ++t) issue_tile(t);
-  }
-  cta_sync();
+  // (prologue -- barrier init and the first BSTAGES tiles -- issued by scan_bulk_begin
+  //  before the pass parameters and the candidacy table are staged, so they overlap)
   for (uint64_t t = 0; t < ntiles; ++t) {
     const int st = (int)(t % BSTAGES);
     const uint32_t par = (uint32_t)((t / BSTAGES) & 1);
@@ -587,6 +610,14 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
   uint64_t lo, hi;
   switch (cmd) {
     case CMD_SCAN: {
+      uint64_t wlo = 0, whi = 0;
+      const bool bulk = c.GP > 1 && !leader && d.bulk_ok;
+      if (c.GP > 1 && !leader) {
+        const uint64_t nw = c.GP - 1, w = c.rank - 1;
+        wlo = ((uint64_t)d.C * w / nw) & ~3ull;
+        whi = w + 1 == nw ? d.C : (((uint64_t)d.C * (w + 1) / nw) & ~3ull);
+        if (bulk) scan_bulk_begin(c, wlo, whi);   // first tiles in flight while staging
+      }
       if (tid < 16) s.cnt[tid] = 0;
       if (tid == 0) { s.ncand = 0; s.nw = 0; }
       cta_sync();
@@ -615,12 +646,9 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
         // the leader's smem holds the candidates: workers 1..GP-1 split the pool in
         // 4-slot-aligned slices and stream it through shared memory
         if (!leader) {
-          const uint64_t nw = c.GP - 1, w = c.rank - 1;
-          lo = ((uint64_t)d.C * w / nw) & ~3ull;
-          hi = w + 1 == nw ? d.C : (((uint64_t)d.C * (w + 1) / nw) & ~3ull);
           const uint64_t tw0 = gtimer();
-          if (d.bulk_ok) scan_range_bulk(c, lo, hi, P);
-          else scan_range(c, lo, hi, P);
+          if (bulk) scan_range_bulk(c, wlo, whi, P);
+          else scan_range(c, wlo, whi, P);
           if (c.rank == 1 && tid == 0) g->wscan_ns += gtimer() - tw0;
         }
       } else {
@@ -756,6 +784,21 @@ __device__ void issue(Ctx& c, unsigned cmd) {
   if (cmd == CMD_EXIT) return;
   const uint64_t t1 = gtimer();
   run_cmd(c, cmd, true);
+  if (cmd == CMD_SCAN && c.pf_n) {
+    // idle while the workers stream: pull the next request's resident-table and ghost-table
+    // home lines into L2 (its probes then start from L2; state is not read here)
+    const Dev& d = *c.d;
+    const uint64_t tb = (uint64_t)d.tmask + 1, gt = (uint64_t)d.gmask + 1;
+    for (uint32_t j = threadIdx.x; j < c.pf_n; j += NT) {
+      const uint64_t H = c.pf_h[j];
+      const uint64_t* tk = d.tkey + (uint64_t)c.r * tb + home(H, d.tmask);
+      const uint32_t* tv = d.tval + (uint64_t)c.r * tb + home(H, d.tmask);
+      const uint64_t* gk = d.gkey + (uint64_t)c.r * gt + home(H, d.gmask);
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(tk));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(tv));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(gk));
+    }
+  }
   const uint64_t t2 = gtimer();
   if (threadIdx.x == 0) {
     const unsigned long long target = (unsigned long long)(c.GP - 1) * c.s->cseq;
@@ -1181,6 +1224,7 @@ __device__ void stage_victims(Ctx& c, uint32_t nc, uint64_t Ub) {
     if (take && pos < VCAP) c.vbuf[pos] = c.cand[i];
   }
   cta_sync();
+  const uint64_t tO = gtimer();
   const uint32_t nv = min(s.nv, (uint32_t)VCAP);
   if (nv <= (uint32_t)NT) {
     // rank placement: (k0, k1, k2) is a total order without ties (ids are unique), so each
@@ -1200,6 +1244,7 @@ __device__ void stage_victims(Ctx& c, uint32_t nc, uint64_t Ub) {
     cta_sync();
     if (e < nv && r == 0) c.vbuf[rank] = x;
     cta_sync();
+    if (tid == 0 && !c.d->cand_smem) {} else if (tid == 0) st.tph[13] += gtimer() - tO;
     return;
   }
   int N = 32;
@@ -1801,6 +1846,12 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
   const uint64_t k = s.k, admit = s.admit;
   if (threadIdx.x == 0) st.tph[0] += gtimer() - tA;
   // ---- O11 evictions (Alg.1 Evict x k, chunked at K crossings)
+  if (c.GP > 1 && i + 1 < b.n) {     // next request of this replica's run (prefetch hint)
+    c.pf_h = b.h + b.boff[i + 1];
+    c.pf_n = (uint32_t)min(b.boff[i + 2] - b.boff[i + 1], (uint64_t)512);
+  } else {
+    c.pf_n = 0;
+  }
   if (k > 0) evict_k(c, k, stamp, b.o_vids ? b.o_vids + b.boff[i] : nullptr);
   tA = gtimer();
   // ---- unpin this request's resident blocks
@@ -1872,6 +1923,8 @@ __device__ Ctx make_ctx(const Dev& d, uint32_t r, uint32_t rank) {
   c.rank = rank;
   c.GP = d.GP;
   c.base = (uint64_t)r * d.C;
+  c.pf_h = nullptr;
+  c.pf_n = 0;
   return c;
 }
 
