@@ -155,10 +155,12 @@ struct Smem {
   uint32_t nv, nw;          // nw: this CTA's candidates awaiting finalize_key (global mode)
   uint32_t cseq, wcmd;      // leader: commands posted this launch; worker: command to run
   uint32_t gbase;           // worker: this CTA's reservation in the group candidate buffer
+  uint32_t fin;             // 1: the scored candidates carry their exact keys (finalize_key ran)
   uint32_t pincnt[16];      // leader: this round's pinned blocks per segment
   unsigned long long thr64[16];   // candidacy table of the current scan: keys (EF, multi-turn)
   uint32_t thrS[1024];            // STRUCT: upper 32 bits of a bound on obits(last), per (tau, q8)
-  uint32_t rhist[NSEG * 256];   // radix-select histograms (one 256-bin digit per segment)
+  __align__(16) uint32_t rhist[NSEG * 256];   // radix-select histograms (one 256-bin digit per
+                                // segment); worker scan: its finished candidate records
   __align__(8) uint64_t mbar[16];  // bulk-copy stage barriers (worker scan pipeline): full[8], empty[8]
   uint64_t wthr[16], wpfx[16], wpmask[16];   // worker copies of the leader's command parameters
   double wcw[15], wmu[2], wsg[2];
@@ -275,7 +277,7 @@ __device__ __forceinline__ Cand make_cand(uint32_t meta, uint64_t key, uint32_t 
   Cand x;
   x.ss = sl | ((q == Q_EF ? 0u : 1u) << 28);
   x.seg = seg_of_tix(meta_tix(meta));
-  x.k0 = q == Q_EF ? key : 0ull;
+  x.k0 = q == Q_EF ? key : ~0ull;    // scored: set by finalize_key (until then after every EF key)
   x.k1 = q == Q_EF ? 0ull : key;
   x.k2 = 0;
   x.pad = 0;
@@ -306,6 +308,7 @@ __device__ __forceinline__ void finalize_key(const Dev& d, uint64_t base, const 
 // radix histogram area) and scores them exactly after streaming (no transcendental inside
 // the streaming loop); overflow is scored in place.
 constexpr uint32_t WCAP = NSEG * 256;
+constexpr uint32_t WCAPC = (uint32_t)(NSEG * 256 * 4 / sizeof(Cand));   // records in the same area
 __device__ __forceinline__ void note_cand(Ctx& c, const ScanP& P, Cand* gdst, uint32_t pos) {
   const uint32_t w = atomicAdd(&c.s->nw, 1u);
   if (w < WCAP) {
@@ -411,7 +414,9 @@ __device__ void scan_range(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P) {
   if (gm) {
     finalize_noted(c, P, gdst);
   } else {
-    for (uint32_t i = tid; i < s.ncand; i += NT) finalize_key(d, c.base, P, c.cand[i]);
+    // private pool: exact scores are computed lazily by select_chunk, only when the EF
+    // candidates cannot cover the chunk (Stage 2 needed)
+    if (tid == 0) s.fin = 0;
   }
 }
 
@@ -554,17 +559,14 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
         uint32_t basep = 0;
         if (lane == 0) basep = atomicAdd(&s.nw, (unsigned)__popc(bal));
         basep = __shfl_sync(~0u, basep, 0);
-        if (take) {
-          const uint32_t sl = (uint32_t)(t0 + u * NT + tid);
+        if (take) {                       // exact record now (its loads and fp64 chain
+          const uint32_t sl = (uint32_t)(t0 + u * NT + tid);   // overlap the other warps' stream)
           const uint32_t w = basep + __popc(bal & ((1u << lane) - 1u));
-          if (w < WCAP) {
-            s.rhist[w] = sl;
-          } else {                        // list full (rare): append to the group buffer directly
-            Cand x = make_cand(mv[u], kv[u], sl);
-            finalize_key(d, c.base, P, x);
-            atomicAdd(&s.cnt[x.seg], 1u);
-            gdst[atomicAdd(&c.ctl->ncand, 1u)] = x;
-          }
+          Cand x = make_cand(mv[u], kv[u], sl);
+          finalize_key(d, c.base, P, x);
+          atomicAdd(&s.cnt[x.seg], 1u);
+          if (w < WCAPC) reinterpret_cast<Cand*>(s.rhist)[w] = x;
+          else gdst[atomicAdd(&c.ctl->ncand, 1u)] = x;   // list full (rare): append directly
         }
       }
     }
@@ -585,17 +587,13 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
   }
   // publish the CTA's candidates: one reservation in the group buffer, then the records
   // (meta/key re-read from L2; exact Eq.(1)-(3) scores, ids) written contiguously
-  const uint32_t nl = min(s.nw, WCAP);
+  const uint32_t nl = min(s.nw, WCAPC);
   if (tid == 0) s.gbase = atomicAdd(&c.ctl->ncand, nl);
   cta_sync();
   const uint32_t gb0 = s.gbase;
-  for (uint32_t i = tid; i < nl; i += NT) {
-    const uint32_t sl = s.rhist[i];
-    Cand x = make_cand(__ldcg(d.bmeta + c.base + sl), __ldcg(d.bkey + c.base + sl), sl);
-    finalize_key(d, c.base, P, x);
-    atomicAdd(&s.cnt[x.seg], 1u);
-    gdst[gb0 + i] = x;
-  }
+  const uint4* lsrc = reinterpret_cast<const uint4*>(s.rhist);
+  uint4* ldst = reinterpret_cast<uint4*>(gdst + gb0);
+  for (uint32_t i = tid; i < 2 * nl; i += NT) ldst[i] = lsrc[i];
 }
 
 // stride-halving tree sum over y[0..P) in smem (SURVEY c.3 TREE)
@@ -1203,7 +1201,7 @@ __device__ void stage_victims(Ctx& c, uint32_t nc, uint64_t Ub) {
     if (i < nc) {
       const Cand x = c.cand[i];
       // EF grows within its threshold's num_tokens band: min over that band only
-      if (x.seg != 0 || (x.k0 >> 32) == (st.thr[0] >> 32)) { g = x.seg; key = seg_key(x); }
+      if ((x.seg != 0 || (x.k0 >> 32) == (st.thr[0] >> 32)) && (s.fin || x.seg < 9)) { g = x.seg; key = seg_key(x); }
       take = x.k0 <= Ub;
     }
     const uint32_t peers = __match_any_sync(~0u, g);
@@ -1289,7 +1287,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
     if (tid == 0) { const uint64_t t1 = gtimer(); st.tph[1] += t1 - t0; t0 = t1; }
     if (gm) {            // gather the group's counts; bring the candidates into smem
       if (tid < 16) s.cnt[tid] = __ldcg(&g->cnt[tid]);
-      if (tid == 0) s.ncand = __ldcg(&g->ncand);
+      if (tid == 0) { s.ncand = __ldcg(&g->ncand); s.fin = 1; }
       cta_sync();
       const uint32_t e0 = min(m, s.segtot[0]);
       const bool narrowed = s.ncand > (uint32_t)CAND_MAX;
@@ -1299,10 +1297,11 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
       const uint64_t tL = gtimer();
       const Cand* src = narrowed ? d.gsel + (uint64_t)c.r * CAND_MAX : d.gcand + c.base;
       for (uint32_t i = tid; i < s.ncand; i += NT) {
-        Cand x;
-        x.k0 = __ldcg(&src[i].k0); x.k1 = __ldcg(&src[i].k1); x.k2 = __ldcg(&src[i].k2);
-        x.ss = __ldcg(&src[i].ss); x.seg = __ldcg(&src[i].seg);
-        c.cand[i] = x;
+        const uint4* sp = reinterpret_cast<const uint4*>(src + i);   // 2 x 16 B per record
+        uint4* dp = reinterpret_cast<uint4*>(c.cand + i);
+        const uint4 a0 = __ldcg(sp), a1 = __ldcg(sp + 1);
+        dp[0] = a0;
+        dp[1] = a1;
       }
       cta_sync();
       if (tid == 0) st.tph[13] += gtimer() - tL;
@@ -1320,6 +1319,15 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
       }
     }
     cta_sync();
+    if (!gm && s.cnt[0] < m) {       // Stage 2 needed: exact scores of the scored candidates
+      ScanP P;
+      P.now = now; P.thr = (const unsigned long long*)st.thr; P.cw = &s.cw[0][0];
+      P.mu = st.par.mu; P.sg = st.par.sigma; P.gamma = st.par.gamma;
+      P.dt_eps = d.dt_eps; P.z_cut = d.z_cut; P.stamp = 0;
+      for (uint32_t i = tid; i < nc; i += NT) finalize_key(d, c.base, P, c.cand[i]);
+      if (tid == 0) s.fin = 1;
+      cta_sync();
+    }
     // The victims are the m smallest candidates by (k0, k1, k2): EF keys (ntok, id) are
     // < 2^63 <= obits(P), so Stage 1 precedes Stage 2 by construction.
     c0 = s.cnt[0];
@@ -1337,7 +1345,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
       if (tid == 0) s.target[0] = in_ef ? m : m - ef;
       cta_sync();
       const uint32_t lim = in_ef ? VCAP / 2 : (ef + 16 < VCAP / 2 ? VCAP / 2 - ef : 16u);
-      radix_select(c.cand, nc, false, 1u, s, 0, 0, 0, 8, lim, in_ef ? 0 : 1);
+      radix_select(c.cand, nc, false, 1u, s, 0, 0, 0, 8, lim / 2, in_ef ? 0 : 1);
       staged = (in_ef ? 0u : ef) + s.below[0] + s.binc[0] <= VCAP;
       if (!staged) {               // rare: fall back to the exact global rank m
         if (tid == 0) s.target[0] = m;
@@ -1474,7 +1482,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
   uint32_t shrink = 0;
   for (int g = 0; g < NSEG; ++g) {
     const uint32_t want = 3 * s.used[g] + d.slack;
-    if (s.cnt[g] > trim_at * want) shrink |= 1u << g;
+    if (s.cnt[g] > trim_at * want && (s.fin || g < 9)) shrink |= 1u << g;   // STRUCT keys need scores
   }
   if (shrink) {
     if (tid < NSEG) s.target[tid] = trim_to * (3 * s.used[tid] + d.slack);
@@ -1486,7 +1494,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
   // ---- grow a segment's threshold before its reserve runs dry (avoids refills): double
   //      the key distance from the smallest candidate (keys: EF (ntok,id); class last;
   //      STRUCT P).  Heuristic only -- exactness is re-proved every pass.
-  if (tid < NSEG && !((shrink >> tid) & 1u)) {
+  if (tid < NSEG && !((shrink >> tid) & 1u) && (s.fin || tid < 9)) {
     const uint32_t g = tid;
     const uint64_t T = st.thr[g];
     const uint32_t left = s.cnt[g] - min(s.cnt[g], s.used[g]);
