@@ -559,14 +559,19 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
         uint32_t basep = 0;
         if (lane == 0) basep = atomicAdd(&s.nw, (unsigned)__popc(bal));
         basep = __shfl_sync(~0u, basep, 0);
-        if (take) {                       // exact record now (its loads and fp64 chain
-          const uint32_t sl = (uint32_t)(t0 + u * NT + tid);   // overlap the other warps' stream)
+        if (take) {
+          // only the slot now: the exact score (a dependent fp64 chain) is computed after the
+          // stream -- stalling a warp on it here delays its stage release (measured slower)
+          const uint32_t sl = (uint32_t)(t0 + u * NT + tid);
           const uint32_t w = basep + __popc(bal & ((1u << lane) - 1u));
-          Cand x = make_cand(mv[u], kv[u], sl);
-          finalize_key(d, c.base, P, x);
-          atomicAdd(&s.cnt[x.seg], 1u);
-          if (w < WCAPC) reinterpret_cast<Cand*>(s.rhist)[w] = x;
-          else gdst[atomicAdd(&c.ctl->ncand, 1u)] = x;   // list full (rare): append directly
+          if (w < WCAP) {
+            s.rhist[w] = sl;
+          } else {                        // list full (rare): append to the group buffer directly
+            Cand x = make_cand(mv[u], kv[u], sl);
+            finalize_key(d, c.base, P, x);
+            atomicAdd(&s.cnt[x.seg], 1u);
+            gdst[atomicAdd(&c.ctl->ncand, 1u)] = x;
+          }
         }
       }
     }
@@ -587,13 +592,17 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
   }
   // publish the CTA's candidates: one reservation in the group buffer, then the records
   // (meta/key re-read from L2; exact Eq.(1)-(3) scores, ids) written contiguously
-  const uint32_t nl = min(s.nw, WCAPC);
+  const uint32_t nl = min(s.nw, WCAP);
   if (tid == 0) s.gbase = atomicAdd(&c.ctl->ncand, nl);
   cta_sync();
   const uint32_t gb0 = s.gbase;
-  const uint4* lsrc = reinterpret_cast<const uint4*>(s.rhist);
-  uint4* ldst = reinterpret_cast<uint4*>(gdst + gb0);
-  for (uint32_t i = tid; i < 2 * nl; i += NT) ldst[i] = lsrc[i];
+  for (uint32_t i = tid; i < nl; i += NT) {
+    const uint32_t sl = s.rhist[i];
+    Cand x = make_cand(__ldcg(d.bmeta + c.base + sl), __ldcg(d.bkey + c.base + sl), sl);
+    finalize_key(d, c.base, P, x);
+    atomicAdd(&s.cnt[x.seg], 1u);
+    gdst[gb0 + i] = x;
+  }
 }
 
 // stride-halving tree sum over y[0..P) in smem (SURVEY c.3 TREE)
