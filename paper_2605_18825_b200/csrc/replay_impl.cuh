@@ -161,7 +161,7 @@ struct Smem {
   uint32_t thrS[1024];            // STRUCT: upper 32 bits of a bound on obits(last), per (tau, q8)
   __align__(16) uint32_t rhist[NSEG * 256];   // radix-select histograms (one 256-bin digit per
                                 // segment); worker scan: its finished candidate records
-  __align__(8) uint64_t mbar[16];  // bulk-copy stage barriers (worker scan pipeline): full[8], empty[8]
+  __align__(8) uint64_t mbar[24];  // bulk-copy stage barriers (worker scan pipeline): full[12], empty[12]
   uint64_t wthr[16], wpfx[16], wpmask[16];   // worker copies of the leader's command parameters
   double wcw[15], wmu[2], wsg[2];
 };
@@ -474,10 +474,13 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // "empty" mbarrier (one arrival per warp), so warps never wait for each other: only the
 // producer thread (thread 0) waits for a stage to drain before refilling it.  Same outputs
 // as scan_range.
-constexpr int BTILE = 2048;
+#ifndef SAE_BTILE
+#define SAE_BTILE 2048
+#endif
+constexpr int BTILE = SAE_BTILE;
 constexpr uint32_t BTILE_BYTES = BTILE * (4 + 8);
-constexpr int BSTAGES = (int)((CAND_MAX * sizeof(Cand)) / BTILE_BYTES) < 6
-                            ? (int)((CAND_MAX * sizeof(Cand)) / BTILE_BYTES) : 6;
+constexpr int BSTAGES = (int)((CAND_MAX * sizeof(Cand)) / BTILE_BYTES) < 12
+                            ? (int)((CAND_MAX * sizeof(Cand)) / BTILE_BYTES) : 12;
 static_assert(BSTAGES >= 2, "bulk scan needs two stages");
 __device__ void scan_bulk_begin(Ctx& c, uint64_t lo, uint64_t hi) {
   const Dev& d = *c.d;
@@ -486,7 +489,7 @@ __device__ void scan_bulk_begin(Ctx& c, uint64_t lo, uint64_t hi) {
   unsigned char* buf = reinterpret_cast<unsigned char*>(c.cand);
   const uint64_t ntiles = (hi - lo + BTILE - 1) / BTILE;
   uint64_t* full = &s.mbar[0];
-  uint64_t* empty = &s.mbar[8];
+  uint64_t* empty = &s.mbar[12];
   for (int st = 0; st < BSTAGES; ++st) { mbar_init(&full[st], 1); mbar_init(&empty[st], NW); }
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -513,7 +516,7 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
   unsigned char* buf = reinterpret_cast<unsigned char*>(c.cand);
   const uint64_t ntiles = (hi - lo + BTILE - 1) / BTILE;
   uint64_t* full = &s.mbar[0];
-  uint64_t* empty = &s.mbar[8];
+  uint64_t* empty = &s.mbar[12];
   auto issue_tile = [&](uint64_t t) {
     const int st = (int)(t % BSTAGES);
     const uint64_t t0 = lo + t * BTILE;
