@@ -166,7 +166,9 @@ typedef struct {
   /* device time (ns, globaltimer) spent by the replica leader per phase: probe+touch,
    * scan passes, narrowing, sort+check, apply, learn, insert+outputs, table rebuild, and for
    * multi-CTA groups: command post, leader's own partition, wait for the workers, worker 1's
-   * scan time; [12] victim staging + tie-break + victim sort + threshold carry; [13..15] spare */
+   * scan time; [12] threshold carry (trim / grow) after the select; [13] candidate gather from
+   * the group buffer (groups) or victim rank placement (private pools); [14] the select's radix
+   * passes; [15] victim staging + ordering */
   uint64_t phase_ns[16];
   uint64_t select_narrow, select_raw;   /* narrowings (candidate sets > 4096) and raw candidates */
   sae_params params;
