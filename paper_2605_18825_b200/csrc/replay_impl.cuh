@@ -1255,7 +1255,7 @@ __device__ void stage_victims(Ctx& c, uint32_t nc, uint64_t Ub) {
     cta_sync();
     if (e < nv && r == 0) c.vbuf[rank] = x;
     cta_sync();
-    if (tid == 0 && !c.d->cand_smem) {} else if (tid == 0) st.tph[13] += gtimer() - tO;
+    if (tid == 0 && c.d->cand_smem) st.tph[13] += gtimer() - tO;   // (groups: [13] is the gather)
     return;
   }
   int N = 32;
