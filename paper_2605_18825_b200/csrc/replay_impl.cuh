@@ -911,8 +911,10 @@ __device__ void learn(Ctx& c) {
   const uint32_t f = p.learn_flags;
   const double gamma_old = p.gamma;
   // L1 TokenWeights (A16, A17)
-  if ((f & SAE_L_TOKENS) && threadIdx.x == 0) {
-    for (int t = 0; t < 5; ++t) {
+  // (each type is independent: one thread per type, the same arithmetic)
+  if ((f & SAE_L_TOKENS) && threadIdx.x < 5) {
+    {
+      const int t = threadIdx.x;
       if (st.ts_ev[t] > 10) {
         double rm = __ddiv_rn((double)st.ts_mae[t], (double)st.ts_ev[t]);
         double rr = st.ts_acc[t] > 0 ? __ddiv_rn((double)st.ts_hit[t], (double)st.ts_acc[t]) : 0.0;
@@ -925,7 +927,8 @@ __device__ void learn(Ctx& c) {
         p.w[t] = clampd(p.w[t], 0.1, 5.0);
       }
     }
-    for (int t = 0; t < 5; ++t) {
+    {
+      const int t = threadIdx.x;
       st.ts_ev[t] = (99ull * st.ts_ev[t]) / 100ull;
       st.ts_mae[t] = (99ull * st.ts_mae[t]) / 100ull;
       st.ts_hit[t] = (99ull * st.ts_hit[t]) / 100ull;
@@ -964,16 +967,18 @@ __device__ void learn(Ctx& c) {
         }
         for (int q = 0; q < 3; ++q) { st.qh[q] = 0; st.qe[q] = 0; }
       }
-    } else if (threadIdx.x == 0) {
-      for (int q = 0; q < 3; ++q) {
+    } else if (threadIdx.x < 3) {   // queues are independent: one thread per queue
+      {
+        const int q = threadIdx.x;
         if (st.qe[q] > 5) {
           double eff = __ddiv_rn((double)st.qh[q], (double)st.qe[q]);
           double tgt = __dadd_rn(1.0, __ddiv_rn(eff, p.T));
           p.alpha[q] = __dadd_rn(p.alpha[q], __dmul_rn(p.beta_q, __dsub_rn(tgt, p.alpha[q])));
           p.alpha[q] = clampd(p.alpha[q], 0.1, 3.0);
         }
+        st.qh[q] = 0;
+        st.qe[q] = 0;
       }
-      for (int q = 0; q < 3; ++q) { st.qh[q] = 0; st.qe[q] = 0; }
     }
   }
   cta_sync();
@@ -1010,13 +1015,24 @@ __device__ void learn(Ctx& c) {
     }
   }
   // L4 DecayPower (A27)
+  if (f & SAE_L_DECAY) {
+    // per-bin hit rates in parallel (scratch: the candidate buffer), sums in bin order
+    double* rt = reinterpret_cast<double*>(c.cand);
+    const uint32_t NB = d.nbins;
+    if (threadIdx.x < NB) {
+      const uint32_t i = threadIdx.x;
+      rt[i] = st.pb_acc[i] == 0 ? -1.0 : __ddiv_rn((double)st.pb_hit[i], (double)st.pb_acc[i]);
+    }
+    cta_sync();
+  }
   if ((f & SAE_L_DECAY) && threadIdx.x == 0) {
+    const double* rt = reinterpret_cast<const double*>(c.cand);
     uint32_t NB = d.nbins, half = NB / 2;
     double fs = 0.0, bs = 0.0;
     int fc = 0, bc = 0;
     for (uint32_t i = 0; i < NB; ++i) {
       if (st.pb_acc[i] == 0) continue;
-      double rate = __ddiv_rn((double)st.pb_hit[i], (double)st.pb_acc[i]);
+      const double rate = rt[i];
       if (i < half) { fs = __dadd_rn(fs, rate); fc++; } else { bs = __dadd_rn(bs, rate); bc++; }
     }
     if (fc > 0 && bc > 0) {
@@ -1028,10 +1044,12 @@ __device__ void learn(Ctx& c) {
         p.gamma = clampd(p.gamma, 0.3, 3.0);
       }
     }
-    for (uint32_t i = 0; i < NB; ++i) {
-      st.pb_hit[i] = (99ull * st.pb_hit[i]) / 100ull;
-      st.pb_acc[i] = (99ull * st.pb_acc[i]) / 100ull;
-    }
+  }
+  cta_sync();
+  if ((f & SAE_L_DECAY) && threadIdx.x < d.nbins) {
+    const uint32_t i = threadIdx.x;
+    st.pb_hit[i] = (99ull * st.pb_hit[i]) / 100ull;
+    st.pb_acc[i] = (99ull * st.pb_acc[i]) / 100ull;
   }
   cta_sync();
   double cw_old[4];

@@ -4,9 +4,9 @@
 // silent/conflicting passages: DESIGN.md "Readings".
 //
 // Device layout: per replica r a struct-of-
-// arrays block table of C slots (hash u64, last f64, id u32, meta u32 =
-// q|tau|ntok|live, ob u32, omax u32, p_struct f64 cached per gamma-epoch,
-// acc u32, pin-stamp u32), an open-addressing resident table (u64 key -> slot,
+// arrays block table of C slots (hash u64, last f64, key u64 = the scan key, id u32,
+// meta u32 = q|tau|ntok|live|pin|candidacy-table entry, ob u32, omax u32, acc u32,
+// table position u32), an open-addressing resident table (u64 key -> slot,
 // tombstones + rebuild), a free-slot stack, the ghost ring (recently_evicted,
 // P:535) with its own hash index, the ln(dt) interval rings, and a scalar
 // state record (counters, learned parameters, E, ids).
@@ -458,10 +458,8 @@ __global__ void k_params_gather(Dev d, sae_params* out) {
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < d.R; r += gridDim.x * blockDim.x)
     out[r] = d.st[r].par;
 }
-// replace parameters; the cached p_struct of a replica is refreshed if its gamma changed
-__global__ void k_params_scatter(Dev d, const sae_params* in, uint32_t r0, uint32_t nr) {
-  // parameters only feed the kernels through RState (no cached gamma-dependent state)
-}
+// replace parameters (they feed the kernels only through RState: no cached
+// parameter-dependent block state to refresh)
 __global__ void k_params_commit(Dev d, const sae_params* in, uint32_t r0, uint32_t nr) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += gridDim.x * blockDim.x)
     if (r0 + i < d.R) d.st[r0 + i].par = in[i];
@@ -726,10 +724,8 @@ sae_status sae_destroy(sae_ctx* ctx) {
 
 static sae_status scatter_params(sae_ctx* ctx, const sae_params* dev_in, uint32_t r0, uint32_t nr,
                                  cudaStream_t s) {
-  dim3 grid(8, nr);
-  k_params_scatter<<<grid, 256, 0, s>>>(ctx->d, dev_in, r0, nr);
   k_params_commit<<<(nr + 255) / 256, 256, 0, s>>>(ctx->d, dev_in, r0, nr);
-  ctx->launches += 2;
+  ctx->launches += 1;
   CK(cudaGetLastError());
   return SAE_OK;
 }
