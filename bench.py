@@ -76,6 +76,22 @@ class Clocks:
         self.index = index
         self.proc = None
         self.f = None
+        self.offset = 0
+
+    def mark(self, wait_s: float = 15.0):
+        """Wait until the sampler is producing rows (nvidia-smi's NVML start-up on a fresh
+        box takes seconds and stalls the launching thread if it overlaps the timed steps),
+        then only count rows from here on: the timed region."""
+        if self.proc is None:
+            return
+        t0 = time.time()
+        while time.time() - t0 < wait_s:
+            self.f.flush()
+            if os.path.getsize(self.f.name) > 0:
+                break
+            time.sleep(0.05)
+        time.sleep(0.25)
+        self.offset = os.path.getsize(self.f.name)
 
     def start(self):
         try:
@@ -96,7 +112,11 @@ class Clocks:
         except Exception:
             self.proc.kill()
         self.f.flush()
-        rows = [l.strip().split(",") for l in open(self.f.name) if l.strip()]
+        with open(self.f.name) as fh:
+            fh.seek(self.offset)
+            rows = [l.strip().split(",") for l in fh if l.strip()]
+        if not rows:      # a very short timed region: fall back to the last sample before it
+            rows = [l.strip().split(",") for l in open(self.f.name) if l.strip()][-1:]
         os.unlink(self.f.name)
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -258,7 +278,7 @@ def run_ours(args, wl, ws, rank, local):
     if wl["cfg"] == "c5":
         R = 1024 // ws
         per = wl["per_step"]
-        n_req = per * (W + 2 * K)
+        n_req = per * (W + 2 * K + 1)
         traces = []
         seeds = sorted(set(((rank * R) + r) // 32 for r in range(R)))
         for sd in seeds:
@@ -298,7 +318,7 @@ def run_ours(args, wl, ws, rank, local):
         R = 1
         per = wl["per_step"]
         pre = wl.get("prefill", 0)
-        tr0 = make_trace(wl, rank, n_requests=(pre + per * (W + 2 * K)) if pre else None)
+        tr0 = make_trace(wl, rank, n_requests=(pre + per * (W + 2 * K + 1)) if pre else None)
         pol = CFG.policy_config(tr0["config"]["capacity"])
         cache = S.SaeCache(pol["capacity"], n_replicas=1, policy=pol)
         for lo in range(0, pre, 20000):   # untimed pre-fill of the pool
@@ -331,6 +351,7 @@ def run_ours(args, wl, ws, rank, local):
             dist.barrier()
 
     clk = Clocks(local)
+    clk.start()           # before the warm-up: its start-up must not overlap the timed steps
     # ---- device-resident timed steps
     times = []
     st0 = None
@@ -339,12 +360,12 @@ def run_ours(args, wl, ws, rank, local):
         barrier()
         torch.cuda.synchronize()
         if s == W:
+            clk.mark()
             cache.sync()
             st0 = [cache.stats(r) for r in range(R)]
             l0 = cache.launches()
             cache.profile(True)
             cache.profile_read()
-            clk.start()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         cache.admit_batch(steps_dev[s], out=outs[s])
@@ -368,10 +389,11 @@ def run_ours(args, wl, ws, rank, local):
 
     # ---- end to end through the public API with pinned host inputs (continuing the trace)
     e2e_ms, h2d, d2h, e2e_req = 0.0, 0, 0, 0
-    host_steps = [step_batch(s) for s in range(W + K, W + 2 * K)]
+    # one untimed warm-up call first (staging buffers, pinned output buffers), then K timed
+    host_steps = [step_batch(s) for s in range(W + K, W + 2 * K + 1)]
     tok_h = torch.from_numpy(arena_tok.view(np.int32)).pin_memory()
     typ_h = torch.from_numpy(arena_typ).pin_memory()
-    for hb in host_steps:
+    for si, hb in enumerate(host_steps):
         hp = S.batch_to_torch({**hb, "tokens": np.zeros(1, np.uint32), "types": np.zeros(1, np.uint8)},
                               pin=True)
         a = int(hb["prompt_off"].min())
@@ -385,6 +407,8 @@ def run_ours(args, wl, ws, rank, local):
         e1.record()
         torch.cuda.synchronize()
         barrier()
+        if si == 0:
+            continue
         e2e_ms += e0.elapsed_time(e1)
         h2d += nbytes_in
         d2h += nbytes_out
