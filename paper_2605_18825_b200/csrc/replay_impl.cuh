@@ -1222,29 +1222,11 @@ __device__ void stage_victims(Ctx& c, uint32_t nc, uint64_t Ub) {
   RState& st = s.st;
   const int tid = threadIdx.x, lane = tid & 31;
   if (tid == 0) s.nv = 0;
-  if (tid < 16) s.kmin[tid] = ~0ull;
   cta_sync();
   for (uint32_t i0 = 0; i0 < nc; i0 += NT) {
     const uint32_t i = i0 + tid;
-    uint32_t g = 0xFFFFFFFFu;
-    uint64_t key = ~0ull;
     bool take = false;
-    if (i < nc) {
-      const Cand x = c.cand[i];
-      // EF grows within its threshold's num_tokens band: min over that band only
-      if ((x.seg != 0 || (x.k0 >> 32) == (st.thr[0] >> 32)) && (s.fin || x.seg < 9)) { g = x.seg; key = seg_key(x); }
-      take = x.k0 <= Ub;
-    }
-    const uint32_t peers = __match_any_sync(~0u, g);
-    if (g != 0xFFFFFFFFu) {
-      const uint32_t hi = (uint32_t)(key >> 32), lo = (uint32_t)key;
-      const uint32_t mhi = __reduce_min_sync(peers, hi);
-      const uint32_t p2 = peers & __ballot_sync(peers, hi == mhi);
-      if (hi == mhi) {
-        const uint32_t mlo = __reduce_min_sync(p2, lo);
-        if (lane == __ffs(p2) - 1) atomicMin(&s.kmin[g], ((unsigned long long)mhi << 32) | mlo);
-      }
-    }
+    if (i < nc) take = c.cand[i].k0 <= Ub;
     const uint32_t bal = __ballot_sync(~0u, take);
     uint32_t basep = 0;
     if (lane == 0 && bal) basep = atomicAdd(&s.nv, (uint32_t)__popc(bal));
@@ -1455,31 +1437,9 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
     }
   }
   if (tid == 0) s.nv = 0;
-  if (tid < 16) s.kmin[tid] = ~0ull;
   cta_sync();
   for (uint32_t i0 = 0; i0 < nc; i0 += NT) {
     const uint32_t i = i0 + tid;
-    {
-      // per-segment minimum key (threshold growth below): lanes of one segment reduce
-      // among themselves (64-bit min as two 32-bit reductions), one smem atomic per group
-      uint32_t g = 0xFFFFFFFFu;
-      uint64_t key = ~0ull;
-      if (i < nc) {
-        const Cand x = c.cand[i];
-        // EF grows within its threshold's num_tokens band: min over that band only
-        if (x.seg != 0 || (x.k0 >> 32) == (st.thr[0] >> 32)) { g = x.seg; key = seg_key(x); }
-      }
-      const uint32_t peers = __match_any_sync(~0u, g);
-      if (g != 0xFFFFFFFFu) {
-        const uint32_t hi = (uint32_t)(key >> 32), lo = (uint32_t)key;
-        const uint32_t mhi = __reduce_min_sync(peers, hi);
-        const uint32_t p2 = peers & __ballot_sync(peers, hi == mhi);
-        if (hi == mhi) {
-          const uint32_t mlo = __reduce_min_sync(p2, lo);
-          if (lane == __ffs(p2) - 1) atomicMin(&s.kmin[g], ((unsigned long long)mhi << 32) | mlo);
-        }
-      }
-    }
     bool take = false;
     if (i < nc) {
       const Cand x = c.cand[i];
@@ -1525,11 +1485,47 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
   // ---- grow a segment's threshold before its reserve runs dry (avoids refills): double
   //      the key distance from the smallest candidate (keys: EF (ntok,id); class last;
   //      STRUCT P).  Heuristic only -- exactness is re-proved every pass.
+  //      (the per-segment minimum keys are computed only for the segments that grow)
+  if (tid == 0) s.nv = 0;                      // reused: mask of growing segments
+  if (tid < 16) s.kmin[tid] = ~0ull;
+  cta_sync();
   if (tid < NSEG && !((shrink >> tid) & 1u) && (s.fin || tid < 9)) {
+    const uint32_t left = s.cnt[tid] - min(s.cnt[tid], s.used[tid]);
+    if (st.thr[tid] != ~0ull && s.segtot[tid] > s.cnt[tid] && left < 2 * s.used[tid] + d.slack)
+      atomicOr(&s.nv, 1u << tid);
+  }
+  cta_sync();
+  const uint32_t growm = s.nv;
+  if (growm) {
+    for (uint32_t i0 = 0; i0 < nc; i0 += NT) {
+      const uint32_t i = i0 + tid;
+      uint32_t g = 0xFFFFFFFFu;
+      uint64_t key = ~0ull;
+      if (i < nc) {
+        const Cand x = c.cand[i];
+        // EF grows within its threshold's num_tokens band: min over that band only
+        if (((growm >> x.seg) & 1u) && (x.seg != 0 || (x.k0 >> 32) == (st.thr[0] >> 32))) {
+          g = x.seg;
+          key = seg_key(x);
+        }
+      }
+      const uint32_t peers = __match_any_sync(~0u, g);
+      if (g != 0xFFFFFFFFu) {
+        const uint32_t hi = (uint32_t)(key >> 32), lo = (uint32_t)key;
+        const uint32_t mhi = __reduce_min_sync(peers, hi);
+        const uint32_t p2 = peers & __ballot_sync(peers, hi == mhi);
+        if (hi == mhi) {
+          const uint32_t mlo = __reduce_min_sync(p2, lo);
+          if (lane == __ffs(p2) - 1) atomicMin(&s.kmin[g], ((unsigned long long)mhi << 32) | mlo);
+        }
+      }
+    }
+    cta_sync();
+  }
+  if (tid < NSEG && ((growm >> tid) & 1u)) {
     const uint32_t g = tid;
     const uint64_t T = st.thr[g];
-    const uint32_t left = s.cnt[g] - min(s.cnt[g], s.used[g]);
-    if (T != ~0ull && s.segtot[g] > s.cnt[g] && left < 2 * s.used[g] + d.slack) {
+    {
       const uint64_t km = s.kmin[g] == ~0ull ? T : (uint64_t)s.kmin[g];
       uint64_t Tn;
       if (g == 0) {                 // id part only, saturating inside the ntok band
