@@ -74,7 +74,9 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        L = C.CDLL(build())
+        # ORACLE_LIB: load a prebuilt copy instead (tests/test_oracle_mutations.py points it at
+        # deliberately mutated builds to show that the pins catch one-line mistakes)
+        L = C.CDLL(os.environ.get("ORACLE_LIB") or build())
         d, u32, u64, i32, vp = C.c_double, C.c_uint32, C.c_uint64, C.c_int, C.c_void_p
         P = C.POINTER
         sig = {

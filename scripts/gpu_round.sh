@@ -1,0 +1,61 @@
+#!/usr/bin/env bash
+# One documented entry point for the GPU-box work of a round (run under gpurun):
+#
+#   gpurun --timeout 1800 -- 'bash scripts/gpu_round.sh <step> [<step> ...]'
+#
+# Steps (each writes under gpurun_out/, which gpurun copies back):
+#   info        host cores / GPU / clocks of the box
+#   tests       pytest -m gpu (parity through the C ABI) + smoke()
+#   bench       default bench line (C5, cpu_baseline) -> gpurun_out/bench_c5.json
+#   bench_all   bench lines of c2, c3, c4, c4x (no cpu baseline)
+#   ncu_c5      launch list + ncu --set full --import-source on of the timed C5 k_replay
+#   ncu_c4      launch list + full capture of a C4 200-request k_replay launch
+#   ncu_c4x     full capture of a C4x 200-request k_replay launch
+#   sanitize    compute-sanitizer memcheck / racecheck / synccheck on small replays
+#   sass        cuobjdump -sass of libsae.so (k_replay) -> gpurun_out/sass_k_replay.txt
+# Summaries worth keeping are copied into profiles/ by hand (scripts/profile_summary.py).
+set -u
+cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
+mkdir -p gpurun_out
+O=gpurun_out
+for step in "$@"; do
+  echo "== $step"
+  case "$step" in
+    info)
+      (nproc; lscpu | grep -E 'Model name|Socket|Thread|Core' ; nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv) > $O/box_info.txt 2>&1
+      cat $O/box_info.txt ;;
+    tests)
+      timeout 1500 python -m pytest tests -q -m gpu -x 2>&1 | tail -15 | tee $O/gpu_tests.log
+      timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2 | tee $O/smoke.log ;;
+    bench)
+      timeout 900 python bench.py > $O/bench_c5.json 2> $O/bench_c5.err; tail -1 $O/bench_c5.json ;;
+    bench_all)
+      for w in c2 c3 c4 c4x; do
+        timeout 1200 python bench.py --workload $w --steps 3 --warmup 3 --no-cpu-baseline > $O/bench_$w.json 2> $O/bench_$w.err
+        tail -1 $O/bench_$w.json
+      done ;;
+    ncu_c5)
+      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c5.csv \
+        python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+      timeout 1200 ncu --set full --import-source on --clock-control none -k regex:k_replay -s 3 -c 1 -f -o $O/full_c5 \
+        python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+      ls -la $O/full_c5.ncu-rep ;;
+    ncu_c4)
+      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c4.csv \
+        python bench.py --workload c4 --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+      timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_replay -s 5 -c 1 -f -o $O/full_c4 \
+        python scripts/prof_c4.py > $O/prof_c4.log 2>&1 ;;
+    ncu_c4x)
+      timeout 1500 ncu --set full --import-source on --clock-control none -k regex:k_replay -s 30 -c 1 -f -o $O/full_c4x \
+        python scripts/prof_c4x.py > $O/prof_c4x.log 2>&1 ;;
+    sanitize)
+      for tool in memcheck racecheck synccheck; do
+        timeout 900 compute-sanitizer --tool $tool python scripts/sanitize.py > $O/sanitize_$tool.log 2>&1
+        tail -3 $O/sanitize_$tool.log
+      done ;;
+    sass)
+      cuobjdump -sass paper_2605_18825_b200/libsae.so > $O/sass_all.txt 2>&1
+      grep -cE 'UBLKCP|SYNCS' $O/sass_all.txt ;;
+    *) echo "unknown step $step" ;;
+  esac
+done
