@@ -14,8 +14,11 @@ A "step" is one sae_admit_batch over one batch of requests of the workload's
 synthetic trace (all of §8(a): hash, lookup+touch, classify, score, select,
 evict, learn); the replay state carries across steps, as in a serving trace.
 Inputs are resident in HBM before the timed region; L2 is flushed (256 MiB
-write) between timed steps.  Under torchrun every rank replays its own seed of
-the workload (weak scaling, no data-path collective: the traces are independent).
+write) between timed steps.  With --gpus N (torchrun, or re-launched under torchrun
+when WORLD_SIZE is unset) rank g owns the contiguous C5 replicas shard(1024, N, g):
+strong scaling, no data-path collective unless --sync mean_w@E; the job's hit /
+eviction / miss-after-evict counters are summed with an int64 NCCL all-reduce.  C2-C4
+are single traces: N GPUs replay N independent seeds (weak scaling, "replicas only").
 
 --impl reference times the CPU oracle (oracle/, the deliberately slow checker) on
 the same workload on the host cores; it is the reference arm of this tier.
@@ -51,7 +54,7 @@ WORKLOADS = {
                 desc="C4 trace on a 2^24-block (256 Mi-token) pool, whose 12-byte scan records "
                      "(201 MB) exceed L2 (SURVEY 8(d)): one 148-CTA cooperative replica group per "
                      "GPU; pool pre-filled with the trace's first 600K requests (untimed)"),
-    "c5": dict(cfg="c5", per_step=250, ref_step=60,
+    "c5": dict(cfg="c5", per_step=250, ref_step=100,
                desc="C5 parameter-sweep replicas: balanced trace, C=2304, 32 points x seeds, "
                     "replicas per GPU = 1024/N"),
 }
@@ -182,54 +185,144 @@ def oracle_fill(R, tr, cap: int, limit: int) -> int:
     return pos
 
 
+_REF = {}
+
+
+def _ref_init(point, n_req):
+    """Pool worker initialiser (reference arm, C5): one oracle replica per host core, replica
+    `point` of the rank-0 seed's trace."""
+    import oracle
+    cfg = CFG.get("c5", n_requests=n_req)
+    tr = T.generate(cfg, seed=0x5AEC1000)
+    T.materialize(tr)
+    p = CFG.policy_config(2304)
+    p["params"] = CFG.c5_point_params(point.value if hasattr(point, "value") else point)
+    _REF.update(tr=tr, R=oracle.Replica(p), pos=0)
+
+
+def _ref_step(n):
+    tr, R, pos = _REF["tr"], _REF["R"], _REF["pos"]
+    hi = min(pos + n, tr["n"])
+    R.replay(tr, pos, hi, want_hashes=False)
+    _REF["pos"] = hi
+    return hi - pos, int(R.stats().blocks_scored)
+
+
 def run_reference(args, wl, ws, rank):
-    """The oracle (as it stands) on the host cores: the reference arm."""
+    """The oracle (as it stands) on the host cores: the reference arm.  C5: one replica per
+    host core (a process pool), every step each core replays ref_step requests of
+    its replica; other workloads: the oracle single-threaded (C4: its rescans threaded)."""
     if rank != 0:
         return
     import oracle
     n_need = wl["ref_step"] * (args.warmup + args.steps)
     pre = wl.get("prefill", 0)
+    ncpu = os.cpu_count() or 1
+    times, reqs = [], 0
     if wl["cfg"] == "c5":
-        tr = make_trace(wl, 0, n_requests=max(n_need, 1000))
+        import multiprocessing as mp
+        ctx = mp.get_context("spawn")
+        n_req = max(n_need + 10, 1000)
+        pools = [ctx.Pool(1, initializer=_ref_init, initargs=(i % 32, n_req)) for i in range(ncpu)]
+        for pl in pools:
+            pl.apply(_ref_step, (0,))               # initialised before the timed steps
+        scored = 0
+        for step in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            res = [pl.apply_async(_ref_step, (wl["ref_step"],)) for pl in pools]
+            got = [r.get() for r in res]
+            dt = time.perf_counter() - t0
+            if step >= args.warmup:
+                times.append(dt)
+                reqs += sum(g[0] for g in got)
+            scored = sum(g[1] for g in got)
+        for pl in pools:
+            pl.terminate()
+        cores = ncpu
+        per_step = wl["ref_step"] * ncpu
+        sample = ("%d processes (one per host core), each the oracle replaying one C5 replica (parameter "
+                  "points 0..%d of the rank-0 seed's trace); %d steps x %d requests per core after %d "
+                  "warm-up steps; wall clock per step" % (ncpu, min(ncpu, 32) - 1, args.steps,
+                                                          wl["ref_step"], args.warmup))
     else:
         tr = make_trace(wl, 0, n_requests=(pre + n_need) if pre else None)
-    pol = CFG.policy_config(tr["config"]["capacity"])
-    R = oracle.Replica(pol)
-    pos = oracle_fill(R, tr, pol["capacity"], pre) if pre else 0   # untimed pre-fill
-    times, reqs = [], 0
-    for step in range(args.warmup + args.steps):
-        lo, hi = pos, min(pos + wl["ref_step"], tr["n"])
-        t0 = time.perf_counter()
-        res = R.replay(tr, lo, hi, want_hashes=False)
-        dt = time.perf_counter() - t0
-        pos = hi
-        if step >= args.warmup:
-            times.append(dt)
-            reqs += hi - lo
+        pol = CFG.policy_config(tr["config"]["capacity"])
+        R = oracle.Replica(pol)
+        pos = oracle_fill(R, tr, pol["capacity"], pre) if pre else 0   # untimed pre-fill
+        for step in range(args.warmup + args.steps):
+            lo, hi = pos, min(pos + wl["ref_step"], tr["n"])
+            t0 = time.perf_counter()
+            R.replay(tr, lo, hi, want_hashes=False)
+            dt = time.perf_counter() - t0
+            pos = hi
+            if step >= args.warmup:
+                times.append(dt)
+                reqs += hi - lo
+        scored = int(R.stats().blocks_scored)
+        cores = ncpu if pre else 1
+        per_step = wl["ref_step"]
+        sample = "%d steps x %d requests of the %s trace after %d warm-up steps, %s" % (
+            args.steps, wl["ref_step"], wl["cfg"], args.warmup,
+            "rescans threaded over %d cores" % ncpu if pre else "single thread")
     val = reqs / sum(times)
-    st = R.stats()
     line = {
         "impl": "reference", "metric": "requests replayed/s", "value": val, "unit": "req/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl["desc"], "requests_per_step": wl["ref_step"]},
-        "cpu_baseline": {"value": val, "unit": "req/s", "cores": 1, "kind": "oracle",
-                         "sample": "%d steps x %d requests of the %s trace after %d warm-up steps, "
-                                   "single thread" % (args.steps, wl["ref_step"], wl["cfg"],
-                                                      args.warmup)},
+        "scaling": "strong" if wl["cfg"] == "c5" else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": wl["desc"], "requests_per_step": per_step},
+        "cpu_baseline": {"value": val, "unit": "req/s", "cores": cores, "kind": "oracle",
+                         "host_cpu_count": ncpu, "sample": sample},
         "e2e": {"value": val, "unit": "req/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "blocks_scored": int(st.blocks_scored),
+        "blocks_scored": scored,
     }
     print(json.dumps(line), flush=True)
 
 
+def _c5_oracle_worker(args):
+    """One host core: the oracle replays one C5 replica (parameter point `point`, the rank-0
+    seed's trace) for `seconds` of wall clock; returns the requests replayed."""
+    point, seconds, n_req = args
+    import oracle
+    cfg = CFG.get("c5", n_requests=n_req)
+    tr = T.generate(cfg, seed=0x5AEC1000)
+    T.materialize(tr)
+    p = CFG.policy_config(2304)
+    p["params"] = CFG.c5_point_params(point)
+    R = oracle.Replica(p)
+    t0 = time.perf_counter()
+    pos = 0
+    while time.perf_counter() - t0 < seconds and pos < tr["n"]:
+        R.replay(tr, pos, min(pos + 100, tr["n"]), want_hashes=False)
+        pos = min(pos + 100, tr["n"])
+    return pos, time.perf_counter() - t0
+
+
 def cpu_baseline(wl, tr, seconds: float = 15.0):
-    """The oracle as it stands, single thread, on a bounded sample of the workload."""
+    """The oracle as it stands on a bounded sample of the workload, on the box's host cores:
+    C5 as a process pool (one replica per core); C4 / C4x with the oracle's
+    threaded key computation over all cores; C2 / C3 single-threaded."""
     import oracle
     pol = CFG.policy_config(tr["config"]["capacity"])
     pre = wl.get("prefill", 0)
-    if pre:   # C4: pre-fill the 4M-block pool up to its first eviction (untimed), then time rounds
+    ncpu = os.cpu_count() or 1
+    if wl["cfg"] == "c5":
+        import multiprocessing as mp
+        n = ncpu
+        with mp.get_context("spawn").Pool(n) as pool:
+            t0 = time.perf_counter()
+            res = pool.map(_c5_oracle_worker, [(i % 32, seconds, 10_000) for i in range(n)])
+            wall = time.perf_counter() - t0
+        done = sum(r[0] for r in res)
+        busy = max(r[1] for r in res)
+        return {"value": done / busy, "unit": "req/s", "cores": n, "kind": "oracle",
+                "host_cpu_count": ncpu,
+                "sample": "%d processes (one per host core), each the oracle replaying one C5 replica "
+                          "(parameter points 0..%d, the rank-0 seed's trace, C=2304) for %.0f s: %d "
+                          "requests in total (pool wall %.1f s incl. trace generation)"
+                          % (n, min(n, 32) - 1, seconds, done, wall)}
+    if pre:   # C4: pre-fill the pool up to its first eviction (untimed), then time rounds
         R = oracle.Replica(pol)
         pre = oracle_fill(R, tr, pol["capacity"], pre)
         t0 = time.perf_counter()
@@ -238,30 +331,21 @@ def cpu_baseline(wl, tr, seconds: float = 15.0):
             R.replay(tr, pos, pos + 1, want_hashes=False)
             pos += 1
         dt = time.perf_counter() - t0
-        return {"value": (pos - pre) / dt, "unit": "req/s", "cores": 1, "kind": "oracle",
-                "sample": "requests %d..%d of the rank-0 c4 trace (the first eviction rounds) after "
-                          "an untimed pre-fill of the 4M-block pool (%.1f s, single thread)" % (pre, pos, dt)}
+        return {"value": (pos - pre) / dt, "unit": "req/s", "cores": ncpu, "kind": "oracle",
+                "host_cpu_count": ncpu,
+                "sample": "requests %d..%d of the rank-0 %s trace (the first eviction rounds) after "
+                          "an untimed pre-fill of the %d-block pool (%.1f s; each rescan's keys "
+                          "computed by %d threads)" % (pre, pos, wl["cfg"], pol["capacity"], dt, ncpu)}
     t0 = time.perf_counter()
-    done, reps = 0, 0
-    while time.perf_counter() - t0 < seconds:
-        p = dict(pol)
-        if wl["cfg"] == "c5":
-            p["params"] = CFG.c5_point_params(reps % 32)
-        R = oracle.Replica(p)
-        pos, chunk = 0, 500
-        while time.perf_counter() - t0 < seconds and pos < tr["n"]:
-            R.replay(tr, pos, min(pos + chunk, tr["n"]), want_hashes=False)
-            pos = min(pos + chunk, tr["n"])
-        done += pos
-        reps += 1
-        if wl["cfg"] != "c5":
-            break
+    R = oracle.Replica(pol)
+    pos, chunk = 0, 500
+    while time.perf_counter() - t0 < seconds and pos < tr["n"]:
+        R.replay(tr, pos, min(pos + chunk, tr["n"]), want_hashes=False)
+        pos = min(pos + chunk, tr["n"])
     dt = time.perf_counter() - t0
-    what = ("%d replicas (parameter points 0..%d) x up to %d requests of the rank-0 seed" %
-            (reps, reps - 1, tr["n"])) if wl["cfg"] == "c5" else "first %d requests" % done
-    return {"value": done / dt, "unit": "req/s", "cores": 1, "kind": "oracle",
-            "sample": "%s of the %s trace: %d requests in %.1f s, single thread"
-                      % (what, wl["cfg"], done, dt)}
+    return {"value": pos / dt, "unit": "req/s", "cores": 1, "kind": "oracle",
+            "host_cpu_count": ncpu,
+            "sample": "first %d requests of the %s trace: %.1f s, single thread" % (pos, wl["cfg"], dt)}
 
 
 def run_ours(args, wl, ws, rank, local):
@@ -275,23 +359,27 @@ def run_ours(args, wl, ws, rank, local):
     from paper_2605_18825_b200 import sae as S
 
     W, K = args.warmup, args.steps
+    from paper_2605_18825_b200 import replicas as RP
     if wl["cfg"] == "c5":
-        R = 1024 // ws
+        # contiguous shard of the 1024 global replicas (sizes differ by at most one when N does
+        # not divide 1024); replica g = seed (g // 32) at parameter point (g % 32)
+        g0, g1 = RP.shard(1024, ws, rank)
+        R = g1 - g0
         per = wl["per_step"]
         n_req = per * (W + 2 * K + 1)
         traces = []
-        seeds = sorted(set(((rank * R) + r) // 32 for r in range(R)))
+        seeds = sorted(set(RP.layout(g)[0] for g in range(g0, g1)))
         for sd in seeds:
             cfg = CFG.get("c5", n_requests=n_req)
             t = T.generate(cfg, seed=0x5AEC1000 + sd)
             T.materialize(t)
             t["config"] = cfg
             traces.append(t)
-        rep_of = [seeds.index(((rank * R) + r) // 32) for r in range(R)]
+        rep_of = [seeds.index(RP.layout(g)[0]) for g in range(g0, g1)]
         pol = CFG.policy_config(2304)
         cache = S.SaeCache(2304, n_replicas=R, policy=pol)
         for r in range(R):
-            cache.set_params(r, CFG.c5_point_params(((rank * R) + r) % 32))
+            cache.set_params(r, CFG.c5_point_params(RP.layout(g0 + r)[1]))
 
         def step_batch(step):
             subs = [slice_batch(traces[rep_of[r]], step * per, (step + 1) * per, replica=r)
@@ -350,6 +438,12 @@ def run_ours(args, wl, ws, rank, local):
         if dist is not None:
             dist.barrier()
 
+    sync_every = 0
+    if args.sync != "none":
+        assert wl["cfg"] == "c5" and args.sync.startswith("mean_w@"), "--sync mean_w@E is a C5 mode"
+        sync_every = int(args.sync.split("@")[1])
+        assert sync_every % per == 0, "the sync period must be a multiple of the %d-request step" % per
+    n_syncs = 0
     clk = Clocks(local)
     clk.start()           # before the warm-up: its start-up must not overlap the timed steps
     # ---- device-resident timed steps
@@ -369,6 +463,9 @@ def run_ours(args, wl, ws, rank, local):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         cache.admit_batch(steps_dev[s], out=outs[s])
+        if sync_every and ((s + 1) * per) % sync_every == 0:
+            RP.sync_mean_w(cache)      # NCCL all-gather + fixed-order mean
+            n_syncs += s >= W
         e1.record()
         torch.cuda.synchronize()
         barrier()
@@ -429,6 +526,9 @@ def run_ours(args, wl, ws, rank, local):
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
+    # job-wide hit / eviction / miss-after-evict totals: device sum over this rank's replicas,
+    # then an int64 SUM all-reduce over the ranks (NCCL over NVLink)
+    tot_end = RP.allreduce_counters(cache)
     tmax = allmax(tot_ms)
     req_all = allsum(req)
     e2e_tmax = allmax(e2e_ms)
@@ -477,14 +577,29 @@ def run_ours(args, wl, ws, rank, local):
                    "l2": "flushed between timed steps (256 MiB device write)",
                    "parallelism": "replicas%d" % ws},
         "blocks_scored_per_s": scored_all / (tmax * 1e-3),
-        "hit_rate_tokens": hit_tok / max(prm_tok, 1),
-        "hit_rate_blocks": hit_blk / max(look, 1),
+        # hit rates of the whole job (all ranks, all steps so far) from the int64 all-reduced
+        # counters; the timed-window rates of rank 0 alongside
+        "hit_rate_tokens": tot_end["hit_tokens"] / max(tot_end["prompt_tokens"], 1),
+        "hit_rate_blocks": tot_end["hit_blocks"] / max(tot_end["blocks_looked_up"], 1),
+        "hit_rate_tokens_timed_rank0": hit_tok / max(prm_tok, 1),
+        "job_counters": {k: tot_end[k] for k in ("requests", "hit_blocks", "hit_tokens",
+                                                 "prompt_tokens", "evictions", "learner_firings",
+                                                 "eviction_rounds")} | {
+            "mae_by_type": [tot_end["mae_by_type%d" % i] for i in range(6)],
+            "evict_by_queue": [tot_end["evict_by_queue%d" % i] for i in range(4)],
+            "reduced_over": "%d rank(s), int64 SUM all-reduce" % ws},
+        "sync": {"mode": args.sync, "syncs_in_timed_region": n_syncs},
         "gpu_launches": int(launches),
         "clocks": clocks,
         "score_select_phase": phase_info,
         "roofline": {"bound": "hbm", "kernel": "k_replay", "achieved": achieved, "peak": hbm,
                      "peak_source": src, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic,
+                     "traffic_source": "profiles/ncu_traffic.json (archived ncu --set full capture of "
+                                       "this workload's k_replay; not measured in this run)",
+                     "limiter": ("per-round latency of one CTA per replica (state L1/L2-resident); "
+                                 "the HBM roofline does not bind") if wl["cfg"] in ("c2", "c5") else
+                                "scan pass HBM/L2 bandwidth + the leader CTA's serial phases",
                      "algorithmic_bytes_per_launch": alg_bytes / max(rep_n, 1),
                      "avg_launch_ms": avg_ms, "kernel_share_of_step": rep_ms / max(tot_ms, 1e-9)},
         "e2e": {"value": e2e_all / (e2e_tmax * 1e-3), "unit": "req/s",
@@ -507,9 +622,26 @@ def main():
     ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--sync", default="none",
+                    help="C5 parameter sync: none | mean_w@E (every E requests per replica: NCCL "
+                         "all-gather of the learned weights + fixed-order mean over seeds)")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference" or os.environ.get("BENCH_ALLOW_FEW_WARMUP")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun (the driver does this
+        # itself; a plain `python bench.py --gpus N` gets the same launch)
+        import socket
+        so = socket.socket()
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+        so.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               "--nproc-per-node", str(args.gpus), "--master-addr", "127.0.0.1",
+               "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     ws, rank, local = dist_setup()
+    if ws != args.gpus:
+        print("bench.py: --gpus %d but WORLD_SIZE=%d; using WORLD_SIZE" % (args.gpus, ws), file=sys.stderr)
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
         run_reference(args, wl, ws, rank)

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define SAE_ABI_VERSION 2u
+#define SAE_ABI_VERSION 3u
 
 typedef struct sae_ctx sae_ctx;
 typedef int sae_status;
@@ -56,7 +56,9 @@ enum {
   SAE_E_OVERFLOW = -6,       /* victim buffer too small / 2^32 block ids exhausted  */
   SAE_E_OOM = -7,
   SAE_E_CUDA = -8,
-  SAE_E_ABI = -9
+  SAE_E_ABI = -9,
+  SAE_E_INTERNAL = -10       /* an exactness check still failed after a full rescan
+                                (select); never expected -- raised, not hidden */
 };
 
 /* queues and token types */
@@ -174,23 +176,39 @@ typedef struct {
   sae_params params;
 } sae_replica_stats;
 
+/* Whole-ctx totals of the additive counters (every replica summed), u64, for the multi-GPU
+ * int64 all-reduce of hit / eviction / miss-after-evict statistics. */
+typedef struct {
+  uint64_t requests, blocks_looked_up, hit_blocks, hit_tokens, prompt_tokens, evictions;
+  uint64_t evict_by_queue[4], evict_by_type[6], mae_by_type[6];
+  uint64_t learner_firings, eviction_rounds, blocks_scored, blocks_scored_struct;
+} sae_counters;
+
 /* Trajectory snapshot taken at each learner firing. */
 typedef struct {
   uint64_t E, request;
   double w[5], alpha[3], mu[2], sigma[2], gamma;
 } sae_traj;
 
-/* Allocate a ctx with all device state on cfg->device.  SAE_E_ABI on version
- * mismatch, SAE_E_CAPACITY_ZERO if capacity_blocks == 0, SAE_E_INVAL on other
- * bad sizes, SAE_E_OOM / SAE_E_CUDA on allocation failure. */
+/* Allocate a ctx with all device state on cfg->device: n_replicas independent caches of
+ * capacity_blocks blocks each (the paper's block pool, "cache of capacity C";
+ * S:19-30 CacheStore), with the learners' state initialised from cfg->init (P:910-912,
+ * DESIGN.md A29).  cfg is a HOST pointer, read once.  *out receives the ctx (owned by the
+ * caller until sae_destroy).  Errors: SAE_E_ABI on version mismatch, SAE_E_CAPACITY_ZERO if
+ * capacity_blocks == 0, SAE_E_INVAL on other bad sizes or sigma <= 0, SAE_E_OOM /
+ * SAE_E_CUDA on allocation failure.  On any error nothing is leaked, *out is untouched and
+ * sae_last_error(NULL) gives the text. */
 sae_status sae_create(const sae_config* cfg, sae_ctx** out);
+/* Free every device allocation of the ctx (synchronises the device first). */
 sae_status sae_destroy(sae_ctx* ctx);
 
-/* Replace one replica's parameters (sweeps, C5); p is a HOST pointer (synchronous).
- * The cached structural priorities are refreshed if gamma changes. */
+/* Replace one replica's learned values and meta-parameters (Appendix C parameter sweep,
+ * P:842-853; C5).  p is a HOST pointer, copied before the call returns (synchronous on s).
+ * Every score reads the parameters from the replica state, so nothing cached needs a
+ * refresh.  SAE_E_INVAL if replica >= n_replicas or a sigma <= 0. */
 sae_status sae_set_params(sae_ctx* ctx, uint32_t replica, const sae_params* p, sae_stream s);
-/* Copy every replica's parameters into dev_out[n_replicas] (device), stream-ordered,
- * e.g. for an NCCL all-gather of the learned token-type weights. */
+/* Copy every replica's parameters into dev_out[n_replicas] (device), stream-ordered, for
+ * the multi-GPU all-gather of the learned token-type weights. */
 sae_status sae_params_gather(sae_ctx* ctx, sae_params* dev_out, sae_stream s);
 /* Replace every replica's parameters from dev_in[n_replicas] (device), stream-ordered. */
 sae_status sae_params_scatter(sae_ctx* ctx, const sae_params* dev_in, sae_stream s);
@@ -201,37 +219,85 @@ sae_status sae_params_scatter(sae_ctx* ctx, const sae_params* dev_in, sae_stream
 sae_status sae_params_point_mean(const sae_params* all_dev, uint32_t n_total, uint32_t n_points,
                                  sae_params* out_dev, sae_stream s);
 
-/* Synchronously compute batch->total_blocks (reads prompt/decode lengths on the device). */
+/* Synchronously compute batch->total_blocks = sum_i ceil(prompt_len/B) + ceil(decode_len/B)
+ * (P:319 16-token blocks; A34 decode blocks) from the DEVICE length arrays of batch. */
 sae_status sae_batch_blocks(sae_ctx* ctx, const sae_batch* batch, uint64_t* total_blocks, sae_stream s);
 
-/* Replay a batch: for every request, steps a1..a7 (hash, lookup+touch, classify,
- * score, select, evict, learn) exactly as Alg.1 Add/Evict/Classify + the learners,
- * replicas in parallel, requests of a replica in order. */
+/* Replay a batch: for every request, steps a1..a7 -- chained hashing,
+ * strict-prefix lookup + touch, Classify, Eq.(1)-(3)
+ * scores, Alg.1 Evict, the learners every K evictions (P:540-545,
+ * P:689-823) -- replicas in parallel, the requests of a replica in array order (S:56-64
+ * insert_request).  batch and out hold DEVICE pointers (caller-owned, valid until the
+ * stream passes the call).  batch->total_blocks must equal sum_i ceil(prompt_len/B) +
+ * ceil(decode_len/B) (sae_batch_blocks): the device recomputes it and raises the sticky
+ * SAE_E_INVAL (nothing written) if it is smaller.  A replica whose requests are not
+ * contiguous raises SAE_E_INVAL and is skipped (its state is untouched).  Device errors
+ * (SAE_E_TIME, SAE_E_INVAL for an empty prompt, SAE_E_OVERFLOW) stop that replica at the
+ * failing request and are reported by the next sae_stats / sae_sync. */
 sae_status sae_admit_batch(sae_ctx* ctx, const sae_batch* batch, sae_admit_out* out, sae_stream s);
 
-/* Read-only probe: hit_blocks[i] = resident chained-prefix length of request i
- * against the CURRENT state of its replica.  No touch, no counters. */
+/* sae_admit_batch with HOST buffers (the end-to-end call): every array of host_batch is a
+ * HOST pointer (pinned for asynchronous copies); the request arrays are copied into
+ * ctx-owned device staging, and the token/type arena range [tok_lo, tok_hi) of
+ * host_batch->tokens / ->types into the caller's DEVICE arena tokens_dev / types_dev at the
+ * same offsets (prompt_off / decode_off index that arena).  host_out holds HOST pointers:
+ * per-request outputs [n], victim_off [n+1] and victim_ids [victim_cap >= total_blocks] are
+ * copied back device->host on s (read them after synchronising s); block_hash / block_tau
+ * may be NULL.  *h2d_bytes / *d2h_bytes (optional, host) receive the bytes copied each way.
+ * Errors as sae_admit_batch. */
+sae_status sae_admit_batch_host(sae_ctx* ctx, const sae_batch* host_batch, uint64_t tok_lo,
+                                uint64_t tok_hi, uint32_t* tokens_dev, uint8_t* types_dev,
+                                sae_admit_out* host_out, uint64_t* h2d_bytes, uint64_t* d2h_bytes,
+                                sae_stream s);
+
+/* Read-only probe (S:56-64 prefix match without the insert; P:158 strict prefix):
+ * hit_blocks[i] (device u32 [n]) = resident chained-prefix length of request i against the
+ * CURRENT state of its replica.  No touch, no counters, no hint update.  batch as in
+ * sae_admit_batch (device pointers; total_blocks checked on the device). */
 sae_status sae_lookup(sae_ctx* ctx, const sae_batch* batch, uint32_t* hit_blocks, sae_stream s);
 
-/* Alg.1 Evict() x k on one replica at time `now` (>= the replica's time; advances
- * it) with an empty pin set and full accounting (ghost push, counters, K trigger).
+/* Alg.1 Evict() x k on one replica at time `now` (>= the replica's time;
+ * advances it) with an empty pin set and full accounting: ghost push, ts.ev / qe /
+ * E (A35) and the learners at every multiple of K (A14).
  * victim_ids (device, >= k) receive the ids, *n_out (device u32) the count.  If
  * fewer than k blocks are resident the sticky error SAE_E_EMPTY is raised. */
 sae_status sae_evict(sae_ctx* ctx, uint32_t replica, uint32_t k, double now,
                      uint32_t* victim_ids, uint32_t* n_out, sae_stream s);
 
-/* Run the learners now (UINT32_MAX = all replicas); E is unchanged. */
+/* Run the learners now -- TokenWeights, QueueWeights, LognormalParams, DecayPower
+ * with the replica's learn_flags -- on one replica or on all
+ * (UINT32_MAX); E is unchanged; one trajectory snapshot is appended.  Stream-ordered. */
 sae_status sae_update(sae_ctx* ctx, uint32_t replica, sae_stream s);
 
-/* Synchronous: copy one replica's counters/parameters to host_out; returns and
- * clears the sticky device error if one was raised. */
+/* Synchronous: copy one replica's counters (token_stats P:720-730, queue counters P:581-593,
+ * positional bins P:793, hit/eviction totals), parameters and diagnostics to host_out (HOST
+ * pointer); returns and clears the sticky device error if one was raised. */
 sae_status sae_stats(sae_ctx* ctx, uint32_t replica, sae_replica_stats* host_out, sae_stream s);
-/* Synchronous: copy up to cap trajectory snapshots of a replica (oldest first). */
+/* Stream-ordered: dev_out (DEVICE pointer to one sae_counters) = the sum over every replica
+ * of this ctx of its additive counters (hit accounting A41, evictions by queue / type A35,
+ * miss-after-evict by type P:535-538).  Exact (integer) in any order, so the per-GPU totals
+ * can be all-reduced with NCCL (int64 SUM) into the job's totals. */
+sae_status sae_counters_device(sae_ctx* ctx, sae_counters* dev_out, sae_stream s);
+/* Synchronous: copy up to cap trajectory snapshots (one per learner firing: E, request,
+ * w, alpha, mu, sigma, gamma) of a replica, oldest first, to host_out (HOST);
+ * host_out == NULL only returns the count in *n_out. */
 sae_status sae_get_traj(sae_ctx* ctx, uint32_t replica, sae_traj* host_out, uint64_t cap,
                         uint64_t* n_out, sae_stream s);
 /* Synchronize the stream and return (and clear) the sticky device error. */
 sae_status sae_sync(sae_ctx* ctx, sae_stream s);
+/* Text of the last error of ctx; of the last failed sae_create when ctx is NULL. */
 const char* sae_last_error(const sae_ctx* ctx);
+
+/* Eq.(1)-(3) evaluated on the device with the same arithmetic, operation order
+ * and fdlibm-algorithm ln/exp/erfc as the replay's select uses for a candidate:
+ * out[i] = ((alpha[q-1] * w[tau]) * p) / dt with dt = max(dt_in[i], dt_eps) (A7), p = Eq.(1)
+ * survival for q in {1 chat, 2 agent} (0 when z > z_cut, A36) or Eq.(2) for q = 3 struct from
+ * (ob[i], omax[i]).  q = 0 (EF, not scored) gives NaN.  params: HOST pointer; q, tau, dt_in,
+ * ob, omax, out: DEVICE arrays of n.  For property tests (class monotonicity) and parity of
+ * the score function itself. */
+sae_status sae_priority(const sae_params* params, double dt_eps, double z_cut, uint64_t n,
+                        const uint8_t* q, const uint8_t* tau, const double* dt_in, const uint32_t* ob,
+                        const uint32_t* omax, double* out, sae_stream s);
 
 /* Synthetic-trace token materialisation (input generator, not the method):
  * tokens[dst[p] + i] = SM(SM(seed ^ SM(stream[p])) ^ (start[p] + i)) mod 2^17 and

@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "sae_oracle.cpp")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-CXXFLAGS = ["-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC"]
+CXXFLAGS = ["-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC", "-pthread"]
 
 
 def build(force: bool = False) -> str:
@@ -88,6 +88,7 @@ def lib():
             "orc_classify": (i32, [i32] * 6),
             "orc_tree_sum": (d, [vp, u64]),
             "orc_score": (d, [d, d, d, d]),
+            "orc_priority": (d, [P(OrcParams), d, d, i32, i32, d, u32, u32]),
             "orc_create": (vp, [P(OrcConfig)]),
             "orc_destroy": (None, [vp]),
             "orc_set_params": (None, [vp, P(OrcParams)]),
@@ -125,6 +126,12 @@ def erfc(x): return lib().orc_erfc(float(x))
 def survival(dt, mu, sg, z_cut=30.0): return lib().orc_survival(dt, mu, sg, z_cut)
 def p_struct(ob, omax, gam): return lib().orc_p_struct(int(ob), int(omax), float(gam))
 def score(alpha, w, p, dt): return lib().orc_score(alpha, w, p, dt)
+def priority(params: dict, q, tau, dt, ob=0, omax=1, dt_eps=1e-3, z_cut=30.0):
+    """Eq.(1)-(3) of one block at elapsed time dt through the oracle's score()."""
+    return lib().orc_priority(C.byref(make_params(params)), dt_eps, z_cut, int(q), int(tau),
+                              float(dt), int(ob), int(omax))
+
+
 def classify(tau, mt, ag, cid, is_struct, untempl):
     return lib().orc_classify(int(tau), int(mt), int(ag), int(cid), int(is_struct), int(untempl))
 

@@ -23,6 +23,8 @@
 #include <unordered_map>
 #include <algorithm>
 #include <tuple>
+#include <thread>
+#include <cstdlib>
 
 namespace orc {
 
@@ -635,6 +637,16 @@ void ghost_push(Replica& R, uint64_t hash, uint8_t tau) {
   R.gmap[hash] = {tau, s};
 }
 
+// Threads for the key computation of large pools: ORACLE_THREADS, else every host core.
+static size_t oracle_threads() {
+  if (const char* e = std::getenv("ORACLE_THREADS")) {
+    const long v = std::atol(e);
+    if (v >= 1) return (size_t)v;
+  }
+  const unsigned h = std::thread::hardware_concurrency();
+  return h ? h : 1;
+}
+
 // Remove one victim (SURVEY c.2 O11 steps 1-4), with Alg.1 K trigger (A14).
 void evict_one(Replica& R, uint64_t hash, std::vector<uint32_t>& out) {
   auto it = R.res.find(hash);
@@ -670,10 +682,9 @@ void evict_k(Replica& R, uint64_t k, const std::unordered_map<uint64_t, int>* pi
       uint32_t id;
       uint64_t hash;
     };
-    std::vector<Key> keys;
-    keys.reserve(R.res.size());
-    for (auto& kv : R.res) {
-      if (pin && pin->count(kv.first)) continue;
+    // every unpinned resident block's key (Alg.1 scans every block)
+    auto pinned = [&](const std::pair<const uint64_t, Block>* kv) { return pin && pin->count(kv->first); };
+    auto key_of = [&](const std::pair<const uint64_t, Block>& kv) {
       const Block& b = kv.second;
       Key key;
       key.hash = kv.first;
@@ -687,17 +698,53 @@ void evict_k(Replica& R, uint64_t k, const std::unordered_map<uint64_t, int>* pi
         key.tier = 1;
         key.p = score(R, b, R.now);
       }
-      keys.push_back(key);
-    }
-    R.st.blocks_scored += keys.size();
+      return key;
+    };
     auto less = [](const Key& a, const Key& b) {
       return std::tie(a.tier, a.p, a.last, a.id) < std::tie(b.tier, b.p, b.last, b.id);
     };
-    if (m > keys.size()) m = keys.size();
+    const size_t NB = R.res.size();
+    std::vector<Key> keys;
+    // Large pools: the same keys computed by T threads over contiguous
+    // slices, each keeping its slice's m smallest; the union is then ordered.  The m smallest
+    // under a total order do not depend on the partition, so this equals the serial rescan.
+    const size_t T = NB >= 16384 ? oracle_threads() : 1;
+    size_t N = 0;         // unpinned blocks scored
+    if (T <= 1) {
+      keys.reserve(NB);
+      for (auto& kv : R.res)
+        if (!pinned(&kv)) keys.push_back(key_of(kv));
+      N = keys.size();
+      if (m > N) m = N;
+    } else {
+      std::vector<size_t> cnt(T, 0);
+      std::vector<std::vector<Key>> part(T);
+      std::vector<std::thread> th;
+      for (size_t t = 0; t < T; ++t)
+        th.emplace_back([&, t]() {
+          // thread t walks its share of the hash map's buckets (read-only)
+          const size_t nb = R.res.bucket_count();
+          const size_t lo = nb * t / T, hi = nb * (t + 1) / T;
+          std::vector<Key>& v = part[t];
+          v.reserve(NB / T + 16);
+          for (size_t bk = lo; bk < hi; ++bk)
+            for (auto it = R.res.begin(bk); it != R.res.end(bk); ++it)
+              if (!pinned(&*it)) v.push_back(key_of(*it));
+          cnt[t] = v.size();
+          const size_t mm = std::min<size_t>(m, v.size());
+          std::partial_sort(v.begin(), v.begin() + (ptrdiff_t)mm, v.end(), less);
+          v.resize(mm);
+        });
+      for (auto& x : th) x.join();
+      for (size_t t = 0; t < T; ++t) N += cnt[t];
+      for (auto& v : part) keys.insert(keys.end(), v.begin(), v.end());
+      if (m > N) m = N;
+    }
+    R.st.blocks_scored += N;
     std::partial_sort(keys.begin(), keys.begin() + (ptrdiff_t)m, keys.end(), less);
     for (uint64_t i = 0; i < m; ++i) evict_one(R, keys[i].hash, out);
     remaining -= m;
-    if (keys.empty()) break;
+    if (N == 0) break;
   }
 }
 
@@ -723,6 +770,20 @@ int orc_classify(int tau, int mt, int ag, int cid, int is_struct, int untempl) {
 }
 double orc_tree_sum(const double* y, uint64_t n) { return tree_sum(std::vector<double>(y, y + n)); }
 double orc_score(double alpha, double w, double p, double dt) { return ((alpha * w) * p) / dt; }
+
+// Eq.(1)-(3) of one block at elapsed time dt through score() itself (a throwaway replica
+// holding only the parameters; last = 0, now = dt): for property tests of the priority.
+double orc_priority(const orc_params* p, double dt_eps, double z_cut, int q, int tau, double dt,
+                    uint32_t ob, uint32_t omax) {
+  Replica R;
+  R.cfg.dt_eps = dt_eps;
+  R.cfg.z_cut = z_cut;
+  R.par = *p;
+  Block b;
+  b.id = 0; b.last = 0.0; b.acc = 1; b.ntok = 16;
+  b.q = (uint8_t)q; b.tau = (uint8_t)tau; b.ob = ob; b.omax = omax;
+  return score(R, b, dt);
+}
 
 // --- replica handle -----------------------------------------------------------------
 void* orc_create(const orc_config* cfg) {

@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -92,7 +93,7 @@ struct alignas(16) Cand {  // one candidate victim: sort key (tier, k0, k1, k2) 
 // Control block of a multi-CTA replica group (global memory, one per replica).  The
 // leader CTA publishes a command + its parameters; all CTAs of the group execute their
 // partition of it between two group barriers.
-enum { CMD_SCAN = 1, CMD_HIST, CMD_COMPACT, CMD_REFRESH, CMD_CLEAR_T, CMD_FILL_T, CMD_CLEAR_G,
+enum { CMD_SCAN = 1, CMD_HIST, CMD_COMPACT, CMD_CLEAR_T, CMD_FILL_T, CMD_CLEAR_G,
        CMD_FILL_G, CMD_COUNTQ, CMD_EXIT };
 struct GroupCtl {          // hot words on separate 128-byte lines (polled / atomically updated)
   alignas(128) unsigned long long cmdw;   // posted command word (epoch:24 | seq:32 | cmd:8)
@@ -166,6 +167,7 @@ struct BatchDev {
   const uint8_t* flags;
   const uint32_t* spb;
   uint64_t* boff;         // [n+1]
+  uint64_t tb;            // the caller's total_blocks (workspace size); checked against boff[n]
   uint64_t* h;            // [TB]
   uint8_t* tau;
   uint8_t* ntok;
@@ -363,13 +365,25 @@ __global__ void k_scan_apply(const uint64_t* in, uint64_t n, const uint64_t* par
   if (blockIdx.x == np - 1 && threadIdx.x == 0) out[n] = part[np];
 }
 
+constexpr uint32_t RUN_INVALID = 0xFFFFFFFEu;   // run_start of a replica whose requests are split
+
+// The caller's total_blocks sizes the per-batch workspace: a batch whose real block count
+// (boff[n], computed on the device) exceeds it would write past the workspace.  Every kernel
+// that indexes by block offset checks this first and does nothing on a mismatch.
+__device__ __forceinline__ bool batch_size_ok(const BatchDev& b) { return b.boff[b.n] <= b.tb; }
+
 __global__ void k_runs(BatchDev b, Dev d) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= b.n) return;
   uint32_t r = b.replica[i];
   if (r >= d.R) { raise_err(d, SAE_E_INVAL); return; }
   if (i == 0 || b.replica[i - 1] != r) {
-    if (atomicCAS(&b.run_start[r], 0xFFFFFFFFu, i) != 0xFFFFFFFFu) raise_err(d, SAE_E_INVAL);
+    // a second run of the same replica: its requests are not contiguous.  Mark the replica
+    // invalid (k_replay skips it, its state stays untouched) and raise the sticky error.
+    if (atomicCAS(&b.run_start[r], 0xFFFFFFFFu, i) != 0xFFFFFFFFu) {
+      atomicExch(&b.run_start[r], RUN_INVALID);
+      raise_err(d, SAE_E_INVAL);
+    }
   }
   if (i == b.n - 1 || b.replica[i + 1] != r) b.run_end[r] = i + 1;
 }
@@ -378,6 +392,10 @@ __global__ void k_runs(BatchDev b, Dev d) {
 __global__ void __launch_bounds__(128) k_hash(BatchDev b, Dev d) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= b.n) return;
+  if (!batch_size_ok(b)) {
+    if (i == 0) raise_err(d, SAE_E_INVAL);
+    return;
+  }
   const uint32_t B = d.B;
   uint32_t L = b.plen[i], O = b.dlen[i];
   uint32_t np = (L + B - 1) / B, nd = (O + B - 1) / B;
@@ -418,7 +436,7 @@ constexpr int CAND_MAX = 2560;
 // read-only probe, one warp per request
 __global__ void k_lookup(Dev d, BatchDev b, uint32_t* out) {
   const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (wid >= b.n) return;
+  if (wid >= b.n || !batch_size_ok(b)) return;
   const uint32_t r = b.replica[wid];
   if (r >= d.R) return;
   const uint32_t B = d.B;
@@ -481,12 +499,45 @@ __global__ void k_point_mean(const sae_params* all, uint32_t n_total, uint32_t n
   out[r] = o;
 }
 
+// sae_counters_device: thread f sums additive counter f over the replicas (fixed layout of
+// sae_counters = the leading fields of RState's statistics block, in the same order)
+static_assert(offsetof(RState, blocks_scored_struct) - offsetof(RState, requests) + 8 == sizeof(sae_counters),
+              "sae_counters mirrors the leading statistics of RState");
+__global__ void k_counters(Dev d, sae_counters* out) {
+  constexpr int NF = (int)(sizeof(sae_counters) / 8);
+  const int f = threadIdx.x;
+  if (f >= NF) return;
+  unsigned long long acc = 0;
+  for (uint32_t r = 0; r < d.R; ++r) {
+    const RState& st = d.st[r];
+    const uint64_t* base = &st.requests;    // requests .. blocks_scored_struct are contiguous
+    acc += base[f];
+  }
+  reinterpret_cast<uint64_t*>(out)[f] = acc;
+}
+
 __global__ void k_count_queues(Dev d, uint32_t r, unsigned long long* out5) {
   const uint64_t base = (uint64_t)r * d.C;
   for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < d.C; s += gridDim.x * blockDim.x) {
     uint32_t m = d.bmeta[base + s];
     if (m & M_LIVE) { atomicAdd(&out5[meta_q(m)], 1ull); atomicAdd(&out5[4], 1ull); }
   }
+}
+
+// sae_priority: Eq.(1)-(3) exactly as finalize_key scores a candidate (cw = alpha * w first)
+__global__ void k_priority(sae_params p, double dt_eps, double z_cut, uint64_t n, const uint8_t* q,
+                           const uint8_t* tau, const double* dt_in, const uint32_t* ob,
+                           const uint32_t* omax, double* out) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t qq = q[i], t = tau[i] & 3u;
+  if (qq == 0 || qq > 3) { out[i] = __longlong_as_double(0x7ff8000000000000ll); return; }
+  double dt = dt_in[i];
+  if (dt < dt_eps) dt = dt_eps;
+  const double cw = __dmul_rn(p.alpha[qq - 1], p.w[t]);
+  const double pp = qq == 3 ? p_struct(ob[i], omax[i], p.gamma)
+                            : survival(dt, p.mu[qq - 1], p.sigma[qq - 1], z_cut);
+  out[i] = __ddiv_rn(__dmul_rn(cw, pp), dt);
 }
 
 __device__ __forceinline__ uint64_t sm64(uint64_t x) {
@@ -552,6 +603,9 @@ struct sae_ctx {
   // per-batch workspace (stream-ordered allocations)
   void* ws = nullptr;
   size_t ws_cap = 0;
+  // device staging of sae_admit_batch_host (request arrays + outputs)
+  void* stage = nullptr;
+  size_t stage_cap = 0;
   std::vector<void*> allocs;
   // optional profiling: CUDA events around every k_replay launch (bench roofline)
   uint64_t coresident = 0;
@@ -584,18 +638,7 @@ static cudaError_t dalloc(sae_ctx* ctx, T** p, uint64_t n) {
 
 extern "C" {
 
-sae_status sae_create(const sae_config* cfg, sae_ctx** out) {
-  sae_ctx* ctx = nullptr;
-  if (!cfg || !out) return SAE_E_INVAL;
-  if (cfg->abi_version != SAE_ABI_VERSION) return SAE_E_ABI;
-  if (cfg->capacity_blocks == 0) return SAE_E_CAPACITY_ZERO;
-  if (cfg->n_replicas == 0 || cfg->block_tokens == 0 || cfg->block_tokens > 16 || cfg->K == 0 ||
-      cfg->ghost_capacity == 0 || cfg->interval_ring == 0 || cfg->interval_ring > RMAX ||
-      cfg->n_pos_bins == 0 || cfg->n_pos_bins > 16 || cfg->capacity_blocks > SLOT_MASK)
-    return SAE_E_INVAL;
-  for (int q = 0; q < 2; ++q)
-    if (!(cfg->init.sigma[q] > 0.0)) return SAE_E_INVAL;
-  ctx = new sae_ctx();
+static sae_status create_impl(const sae_config* cfg, sae_ctx* ctx) {
   ctx->cfg = *cfg;
   ctx->device = cfg->device;
   CK(cudaSetDevice(cfg->device));
@@ -708,6 +751,33 @@ sae_status sae_create(const sae_config* cfg, sae_ctx** out) {
   ctx->launches++;
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
+  return SAE_OK;
+}
+
+// text of the last failed sae_create (sae_last_error(NULL))
+static thread_local std::string g_create_error;
+
+sae_status sae_create(const sae_config* cfg, sae_ctx** out) {
+  g_create_error.clear();
+  if (!cfg || !out) { g_create_error = "null argument"; return SAE_E_INVAL; }
+  if (cfg->abi_version != SAE_ABI_VERSION) { g_create_error = "ABI version mismatch"; return SAE_E_ABI; }
+  if (cfg->capacity_blocks == 0) { g_create_error = "capacity_blocks == 0"; return SAE_E_CAPACITY_ZERO; }
+  if (cfg->n_replicas == 0 || cfg->block_tokens == 0 || cfg->block_tokens > 16 || cfg->K == 0 ||
+      cfg->ghost_capacity == 0 || cfg->interval_ring == 0 || cfg->interval_ring > RMAX ||
+      cfg->n_pos_bins == 0 || cfg->n_pos_bins > 16 || cfg->capacity_blocks > SLOT_MASK ||
+      !(cfg->init.sigma[0] > 0.0) || !(cfg->init.sigma[1] > 0.0)) {
+    g_create_error = "invalid configuration";
+    return SAE_E_INVAL;
+  }
+  sae_ctx* ctx = new sae_ctx();
+  const sae_status rc = create_impl(cfg, ctx);
+  if (rc != SAE_OK) {               // free everything allocated so far; keep the message
+    g_create_error = ctx->last_error.empty() ? "sae_create failed" : ctx->last_error;
+    cudaDeviceSynchronize();
+    for (void* p : ctx->allocs) cudaFree(p);
+    delete ctx;
+    return rc;
+  }
   *out = ctx;
   return SAE_OK;
 }
@@ -718,6 +788,7 @@ sae_status sae_destroy(sae_ctx* ctx) {
   cudaDeviceSynchronize();
   for (void* p : ctx->allocs) cudaFree(p);
   if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->stage) cudaFree(ctx->stage);
   delete ctx;
   return SAE_OK;
 }
@@ -790,6 +861,7 @@ static sae_status prepare(sae_ctx* ctx, const sae_batch* b, BatchDev& x, cudaStr
   }
   char* p = (char*)ctx->ws;
   auto take = [&](size_t bytes) { char* q = p; p += al(bytes); return (void*)q; };
+  x.tb = total_blocks;
   uint64_t* cnt = (uint64_t*)take((n + 1) * 8);
   x.boff = (uint64_t*)take((n + 1) * 8);
   uint64_t* part = (uint64_t*)take((ntile + 1) * 8);
@@ -870,6 +942,90 @@ sae_status sae_admit_batch(sae_ctx* ctx, const sae_batch* b, sae_admit_out* o, s
   CK(cudaGetLastError());
   if (o->block_hash) CK(cudaMemcpyAsync(o->block_hash, x.h, b->total_blocks * 8, cudaMemcpyDeviceToDevice, s));
   if (o->block_tau) CK(cudaMemcpyAsync(o->block_tau, x.tau, b->total_blocks, cudaMemcpyDeviceToDevice, s));
+  return SAE_OK;
+}
+
+// End-to-end call with HOST buffers: H2D of the request arrays and of the token arena range,
+// the replay, D2H of the outputs -- all stream-ordered on s (include/sae.h).
+sae_status sae_admit_batch_host(sae_ctx* ctx, const sae_batch* hb, uint64_t tok_lo, uint64_t tok_hi,
+                                uint32_t* tokens_dev, uint8_t* types_dev, sae_admit_out* ho,
+                                uint64_t* h2d_bytes, uint64_t* d2h_bytes, sae_stream st) {
+  if (!ctx || !hb || !ho || tok_hi < tok_lo) return SAE_E_INVAL;
+  const uint64_t n = hb->n, tb = hb->total_blocks;
+  if (n && (!tokens_dev || !types_dev || !hb->replica || !hb->arrival || !hb->prompt_off ||
+            !hb->prompt_len || !hb->decode_off || !hb->decode_len || !hb->tokens || !hb->types ||
+            !hb->flags || !hb->shared_prefix_blocks))
+    return SAE_E_INVAL;
+  if (n && ho->victim_ids && ho->victim_cap < tb) return SAE_E_INVAL;
+  cudaStream_t s = (cudaStream_t)st;
+  CK(cudaSetDevice(ctx->device));
+  auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
+  const uint64_t tbx = tb ? tb : 1;
+  size_t need = al(n * 4) * 4 + al(n * 8) * 3 + al(n) + al(n * 4) * 4 + al((n + 1) * 8) + al(tbx * 4) +
+                (ho->block_hash ? al(tbx * 8) : 0) + (ho->block_tau ? al(tbx) : 0) + 256;
+  if (need > ctx->stage_cap) {
+    if (ctx->stage) CK(cudaFreeAsync(ctx->stage, s));
+    ctx->stage = nullptr;
+    const size_t cap = need + need / 4;
+    CK(cudaMallocAsync(&ctx->stage, cap, s));
+    ctx->stage_cap = cap;
+  }
+  char* p = (char*)ctx->stage;
+  auto take = [&](size_t bytes) { char* q = p; p += al(bytes); return (void*)q; };
+  uint64_t hin = 0, hout = 0;
+  auto h2d = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+    hin += bytes;
+    return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s) : cudaSuccess;
+  };
+  sae_batch db = *hb;
+  db.replica = (const uint32_t*)take(n * 4);
+  db.arrival = (const double*)take(n * 8);
+  db.prompt_off = (const uint64_t*)take(n * 8);
+  db.prompt_len = (const uint32_t*)take(n * 4);
+  db.decode_off = (const uint64_t*)take(n * 8);
+  db.decode_len = (const uint32_t*)take(n * 4);
+  db.flags = (const uint8_t*)take(n);
+  db.shared_prefix_blocks = (const uint32_t*)take(n * 4);
+  CK(h2d((void*)db.replica, hb->replica, n * 4));
+  CK(h2d((void*)db.arrival, hb->arrival, n * 8));
+  CK(h2d((void*)db.prompt_off, hb->prompt_off, n * 8));
+  CK(h2d((void*)db.prompt_len, hb->prompt_len, n * 4));
+  CK(h2d((void*)db.decode_off, hb->decode_off, n * 8));
+  CK(h2d((void*)db.decode_len, hb->decode_len, n * 4));
+  CK(h2d((void*)db.flags, hb->flags, n));
+  CK(h2d((void*)db.shared_prefix_blocks, hb->shared_prefix_blocks, n * 4));
+  CK(h2d(tokens_dev + tok_lo, hb->tokens + tok_lo, (tok_hi - tok_lo) * 4));
+  CK(h2d(types_dev + tok_lo, hb->types + tok_lo, tok_hi - tok_lo));
+  db.tokens = tokens_dev;
+  db.types = types_dev;
+  sae_admit_out dout;
+  std::memset(&dout, 0, sizeof dout);
+  dout.hit_blocks = (uint32_t*)take(n * 4);
+  dout.miss_blocks = (uint32_t*)take(n * 4);
+  dout.matched_tokens = (uint32_t*)take(n * 4);
+  dout.n_victims = (uint32_t*)take(n * 4);
+  dout.victim_off = (uint64_t*)take((n + 1) * 8);
+  dout.victim_ids = (uint32_t*)take(tbx * 4);
+  dout.victim_cap = tbx;
+  dout.block_hash = ho->block_hash ? (uint64_t*)take(tbx * 8) : nullptr;
+  dout.block_tau = ho->block_tau ? (uint8_t*)take(tbx) : nullptr;
+  sae_status rc = sae_admit_batch(ctx, &db, &dout, st);
+  if (rc != SAE_OK) return rc;
+  auto d2h = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+    if (!dst || !bytes) return cudaSuccess;
+    hout += bytes;
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s);
+  };
+  CK(d2h(ho->hit_blocks, dout.hit_blocks, n * 4));
+  CK(d2h(ho->miss_blocks, dout.miss_blocks, n * 4));
+  CK(d2h(ho->matched_tokens, dout.matched_tokens, n * 4));
+  CK(d2h(ho->n_victims, dout.n_victims, n * 4));
+  CK(d2h(ho->victim_off, dout.victim_off, n ? (n + 1) * 8 : 0));
+  CK(d2h(ho->victim_ids, dout.victim_ids, tb * 4));
+  CK(d2h(ho->block_hash, dout.block_hash, tb * 8));
+  CK(d2h(ho->block_tau, dout.block_tau, tb));
+  if (h2d_bytes) *h2d_bytes = hin;
+  if (d2h_bytes) *d2h_bytes = hout;
   return SAE_OK;
 }
 
@@ -997,6 +1153,14 @@ sae_status sae_stats(sae_ctx* ctx, uint32_t replica, sae_replica_stats* out, sae
   return take_sticky(ctx, s);
 }
 
+sae_status sae_counters_device(sae_ctx* ctx, sae_counters* dev_out, sae_stream st) {
+  if (!ctx || !dev_out) return SAE_E_INVAL;
+  k_counters<<<1, 32, 0, (cudaStream_t)st>>>(ctx->d, dev_out);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  return SAE_OK;
+}
+
 sae_status sae_get_traj(sae_ctx* ctx, uint32_t replica, sae_traj* out, uint64_t cap, uint64_t* n_out,
                         sae_stream st) {
   if (!ctx || replica >= ctx->d.R) return SAE_E_INVAL;
@@ -1022,7 +1186,7 @@ sae_status sae_get_traj(sae_ctx* ctx, uint32_t replica, sae_traj* out, uint64_t 
   return SAE_OK;
 }
 
-const char* sae_last_error(const sae_ctx* ctx) { return ctx ? ctx->last_error.c_str() : "null ctx"; }
+const char* sae_last_error(const sae_ctx* ctx) { return ctx ? ctx->last_error.c_str() : g_create_error.c_str(); }
 
 sae_status sae_gen_tokens(uint64_t seed, uint64_t n_pieces, const uint64_t* stream, const uint64_t* start,
                           const uint32_t* len, const uint64_t* dst, const uint8_t* type, uint32_t* tokens,
@@ -1031,6 +1195,18 @@ sae_status sae_gen_tokens(uint64_t seed, uint64_t n_pieces, const uint64_t* stre
   if (n_pieces == 0) return SAE_OK;
   unsigned grid = (unsigned)(n_pieces < 65535ull * 8 ? n_pieces : 65535ull * 8);
   k_gen_tokens<<<grid, 128, 0, (cudaStream_t)st>>>(seed, n_pieces, stream, start, len, dst, type, tokens, types);
+  CK(cudaGetLastError());
+  return SAE_OK;
+}
+
+sae_status sae_priority(const sae_params* params, double dt_eps, double z_cut, uint64_t n,
+                        const uint8_t* q, const uint8_t* tau, const double* dt_in, const uint32_t* ob,
+                        const uint32_t* omax, double* out, sae_stream st) {
+  sae_ctx* ctx = nullptr;
+  if (!params || (n && (!q || !tau || !dt_in || !ob || !omax || !out))) return SAE_E_INVAL;
+  if (n == 0) return SAE_OK;
+  k_priority<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)st>>>(*params, dt_eps, z_cut, n, q, tau,
+                                                                        dt_in, ob, omax, out);
   CK(cudaGetLastError());
   return SAE_OK;
 }

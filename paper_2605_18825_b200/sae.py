@@ -18,10 +18,10 @@ from . import configs as CFG
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsae.so")
 
-SAE_ABI_VERSION = 2
+SAE_ABI_VERSION = 3
 ERRORS = {0: "SAE_OK", -1: "SAE_E_INVAL", -2: "SAE_E_CAPACITY_ZERO", -3: "SAE_E_EMPTY",
           -4: "SAE_E_NOT_RESIDENT", -5: "SAE_E_TIME", -6: "SAE_E_OVERFLOW", -7: "SAE_E_OOM",
-          -8: "SAE_E_CUDA", -9: "SAE_E_ABI"}
+          -8: "SAE_E_CUDA", -9: "SAE_E_ABI", -10: "SAE_E_INTERNAL"}
 
 
 class SaeError(RuntimeError):
@@ -90,9 +90,16 @@ class sae_traj(C.Structure):
 
 
 EXPORTS = ["sae_create", "sae_destroy", "sae_set_params", "sae_params_gather", "sae_params_scatter",
-           "sae_batch_blocks", "sae_admit_batch", "sae_lookup", "sae_evict", "sae_update",
+           "sae_batch_blocks", "sae_admit_batch", "sae_admit_batch_host", "sae_lookup", "sae_evict", "sae_update",
            "sae_stats", "sae_get_traj", "sae_sync", "sae_last_error", "sae_gen_tokens",
-           "sae_launch_count", "sae_profile", "sae_profile_read", "sae_params_point_mean"]
+           "sae_launch_count", "sae_profile", "sae_profile_read", "sae_params_point_mean",
+           "sae_counters_device", "sae_priority"]
+
+# sae_counters (include/sae.h): field order of the whole-ctx counter totals
+COUNTER_FIELDS = (["requests", "blocks_looked_up", "hit_blocks", "hit_tokens", "prompt_tokens",
+                   "evictions"] + ["evict_by_queue%d" % i for i in range(4)] +
+                  ["evict_by_type%d" % i for i in range(6)] + ["mae_by_type%d" % i for i in range(6)] +
+                  ["learner_firings", "eviction_rounds", "blocks_scored", "blocks_scored_struct"])
 
 _lib = None
 
@@ -113,6 +120,8 @@ def lib():
             "sae_params_scatter": (i32, [vp, vp, vp]),
             "sae_batch_blocks": (i32, [vp, P(sae_batch), P(u64), vp]),
             "sae_admit_batch": (i32, [vp, P(sae_batch), P(sae_admit_out), vp]),
+            "sae_admit_batch_host": (i32, [vp, P(sae_batch), u64, u64, vp, vp, P(sae_admit_out),
+                                           P(u64), P(u64), vp]),
             "sae_lookup": (i32, [vp, P(sae_batch), vp, vp]),
             "sae_evict": (i32, [vp, u32, u32, C.c_double, vp, vp, vp]),
             "sae_update": (i32, [vp, u32, vp]),
@@ -125,6 +134,8 @@ def lib():
             "sae_profile": (i32, [vp, i32]),
             "sae_params_point_mean": (i32, [vp, u32, u32, vp, vp]),
             "sae_profile_read": (i32, [vp, P(C.c_double), P(u64)]),
+            "sae_counters_device": (i32, [vp, vp, vp]),
+            "sae_priority": (i32, [P(sae_params), C.c_double, C.c_double, u64] + [vp] * 7),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -171,8 +182,9 @@ _NPD = {"replica": np.uint32, "arrival": np.float64, "prompt_off": np.uint64,
         "tokens": np.uint32, "types": np.uint8, "flags": np.uint8, "spb": np.uint32}
 
 
-def batch_to_torch(b: dict, device="cuda", pin: bool = False) -> dict:
-    """numpy sae_batch arrays (tracegen layout) -> torch tensors (device or pinned host)."""
+def batch_to_torch(b: dict, device="cuda", pin: bool = False, block_tokens: int = 16) -> dict:
+    """numpy sae_batch arrays (tracegen layout) -> torch tensors (device or pinned host);
+    total_blocks is counted with the ctx's block size (the device re-checks it)."""
     out = {}
     for k, td in _TD.items():
         a = np.ascontiguousarray(b[k], dtype=_NPD[k])
@@ -182,7 +194,7 @@ def batch_to_torch(b: dict, device="cuda", pin: bool = False) -> dict:
         else:
             out[k] = t.to(device, non_blocking=False)
     out["n"] = int(b["n"])
-    B = 16
+    out["block_tokens"] = B = int(block_tokens)
     pl = np.asarray(b["prompt_len"], np.int64)
     dl = np.asarray(b["decode_len"], np.int64)
     out["total_blocks"] = int((-(-pl // B) - (-dl // B)).sum())
@@ -242,6 +254,9 @@ class SaeCache:
 
     # ---- calls ---------------------------------------------------------------------
     def _batch(self, b: dict) -> sae_batch:
+        if b.get("block_tokens", 16) != self.policy["block_tokens"]:
+            raise SaeError(-1, "batch counted with %d-token blocks, ctx uses %d (batch_to_torch("
+                           "block_tokens=...))" % (b.get("block_tokens", 16), self.policy["block_tokens"]))
         sb = sae_batch()
         sb.n = b["n"]
         sb.total_blocks = b["total_blocks"]
@@ -277,47 +292,41 @@ class SaeCache:
         return out
 
     def admit_batch_host(self, hb: dict, tok_h, typ_h, tok_d, typ_d, a: int, z: int, stream=None):
-        """End-to-end call with HOST (pinned) inputs: copy the step's request arrays and
-        its token range [a, z) host->device, replay, copy the results device->host.
-        Returns (host outputs, h2d bytes, d2h bytes)."""
-        dev = tok_d.device
+        """End-to-end call through the C ABI's sae_admit_batch_host: the step's request arrays
+        (pinned host tensors in hb) and the token arena range [a, z) (pinned tok_h / typ_h)
+        are copied host->device by the library, the batch is replayed, and the per-request
+        outputs and victim ids come back into pinned host buffers (valid after the stream
+        synchronises).  Returns (host outputs, h2d bytes, d2h bytes)."""
+        n, tb = hb["n"], hb["total_blocks"]
         st = self._staging = getattr(self, "_staging", {})
-        n = hb["n"]
-        db = {"n": n, "total_blocks": hb["total_blocks"], "tokens": tok_d, "types": typ_d}
-        h2d = 0
-        for k in ("replica", "arrival", "prompt_off", "prompt_len", "decode_off", "decode_len",
-                  "flags", "spb"):
-            t = hb[k]
-            buf = st.get(k)
-            if buf is None or buf.numel() < t.numel():
-                buf = st[k] = torch.empty(max(t.numel(), 1) * 2, dtype=t.dtype, device=dev)
-            buf[: t.numel()].copy_(t, non_blocking=True)
-            db[k] = buf[: t.numel()]
-            h2d += t.numel() * t.element_size()
-        tok_d[a:z].copy_(tok_h[a:z], non_blocking=True)
-        typ_d[a:z].copy_(typ_h[a:z], non_blocking=True)
-        h2d += (z - a) * 5
-        outd = st.get("out")
-        if outd is None or outd["victim_ids"].numel() < max(hb["total_blocks"], 1) or \
-                outd["hit_blocks"].numel() < n:
-            outd = st["out"] = self.alloc_out({"n": 2 * n, "total_blocks": 2 * hb["total_blocks"],
-                                               "arrival": db["arrival"]})
-        o = {k: v[: n] for k, v in outd.items() if k in ("hit_blocks", "miss_blocks",
-                                                          "matched_tokens", "n_victims")}
-        o["victim_off"] = outd["victim_off"][: n + 1]
-        o["victim_ids"] = outd["victim_ids"][: max(hb["total_blocks"], 1)]
-        self.admit_batch(db, out=o, stream=stream)
         hout = st.get("hout")
-        if hout is None or hout["victim_ids"].numel() < outd["victim_ids"].numel():
-            hout = st["hout"] = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
-                                 for k, v in outd.items()}
-        res, d2h = {}, 0
-        for k, v in o.items():
-            hbuf = hout[k][: v.numel()]
-            hbuf.copy_(v, non_blocking=True)
-            res[k] = hbuf
-            d2h += v.numel() * v.element_size()
-        return res, h2d, d2h
+        if hout is None or hout["victim_ids"].numel() < max(tb, 1) or hout["hit_blocks"].numel() < n:
+            hout = st["hout"] = {k: torch.empty(max(2 * n, 1), dtype=torch.int32, pin_memory=True)
+                                 for k in ("hit_blocks", "miss_blocks", "matched_tokens", "n_victims")}
+            hout["victim_off"] = torch.empty(2 * n + 1, dtype=torch.int64, pin_memory=True)
+            hout["victim_ids"] = torch.empty(max(2 * tb, 1), dtype=torch.int32, pin_memory=True)
+        sb = sae_batch()
+        sb.n = n
+        sb.total_blocks = tb
+        for k, f in (("replica", "replica"), ("arrival", "arrival"), ("prompt_off", "prompt_off"),
+                     ("prompt_len", "prompt_len"), ("decode_off", "decode_off"),
+                     ("decode_len", "decode_len"), ("flags", "flags"), ("spb", "shared_prefix_blocks")):
+            setattr(sb, f, hb[k].data_ptr())
+        sb.tokens = tok_h.data_ptr()
+        sb.types = typ_h.data_ptr()
+        ao = sae_admit_out()
+        for k in ("hit_blocks", "miss_blocks", "matched_tokens", "n_victims", "victim_off", "victim_ids"):
+            setattr(ao, k, hout[k].data_ptr())
+        ao.victim_cap = hout["victim_ids"].numel()
+        h2d, d2h = C.c_uint64(), C.c_uint64()
+        self._keep = (hb, hout)
+        self._check(lib().sae_admit_batch_host(self.h, C.byref(sb), a, z, tok_d.data_ptr(),
+                                               typ_d.data_ptr(), C.byref(ao), C.byref(h2d),
+                                               C.byref(d2h), _stream(stream)))
+        res = {k: v[: n] for k, v in hout.items() if k not in ("victim_off", "victim_ids")}
+        res["victim_off"] = hout["victim_off"][: n + 1]
+        res["victim_ids"] = hout["victim_ids"][: max(tb, 1)]
+        return res, h2d.value, d2h.value
 
     def lookup(self, b: dict, stream=None) -> torch.Tensor:
         hit = torch.empty(b["n"], dtype=torch.int32, device=b["arrival"].device)
@@ -361,6 +370,14 @@ class SaeCache:
         self._check(lib().sae_get_traj(self.h, replica, arr, n.value, C.byref(n), _stream(stream)))
         return [arr[i] for i in range(n.value)]
 
+    def counters_device(self, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """[len(COUNTER_FIELDS)] int64 device tensor: every replica's additive counters summed
+        on the device (for an NCCL int64 all-reduce across ranks)."""
+        if out is None:
+            out = torch.empty(len(COUNTER_FIELDS), dtype=torch.int64, device="cuda")
+        self._check(lib().sae_counters_device(self.h, out.data_ptr(), _stream(stream)))
+        return out
+
     def sync(self, stream=None):
         self._check(lib().sae_sync(self.h, _stream(stream)))
 
@@ -385,6 +402,19 @@ def params_point_mean(all_params: torch.Tensor, n_points: int, stream=None) -> t
                                      out.data_ptr(), _stream(stream))
     if rc != 0:
         raise SaeError(rc, "sae_params_point_mean")
+    return out
+
+
+def priority(params: dict, q, tau, dt, ob, omax, dt_eps: float = 1e-3, z_cut: float = 30.0,
+             stream=None) -> torch.Tensor:
+    """Eq.(1)-(3) on the device (sae_priority): device tensors q u8, tau u8, dt f64, ob / omax
+    i32 of one length -> P f64 (NaN for EF), the select's arithmetic exactly."""
+    out = torch.empty_like(dt)
+    rc = lib().sae_priority(C.byref(make_params(params)), float(dt_eps), float(z_cut), dt.numel(),
+                            q.data_ptr(), tau.data_ptr(), dt.data_ptr(), ob.data_ptr(), omax.data_ptr(),
+                            out.data_ptr(), _stream(stream))
+    if rc != 0:
+        raise SaeError(rc, "sae_priority")
     return out
 
 
