@@ -76,13 +76,26 @@ enum {
   SAE_L_QUEUE_RELATIVE = 32  /* relative queue rule P:814-817 instead of Alg. P:583-593 */
 };
 
+/* Eviction policy of a replica (sae_params.mode).  SAE_MODE_SAE is the paper's method; the
+ * others are its baselines and its ablation variant, replayed by the
+ * same kernels for side-by-side sweeps.  In the baselines every block sits in one queue
+ * (CHAT) -- no EF stage, no structural queue -- and the victim is the argmin of:
+ *   SAE_MODE_LRU  (last, id)                       least recently used
+ *   SAE_MODE_LFU  (accesses, last, id)             least frequently used
+ *   SAE_MODE_TWO  (w_tau / dt, last, id)           Token-Weight-Only: the learned token-type
+ *                                                  weights without the multi-queue
+ *                                                  architecture (decode blocks weigh as CoT)
+ * Counters and learners run as configured.  Fixed-Param MQ and the learner ladder
+ * are SAE_MODE_SAE with learn_flags / (mu, sigma) settings. */
+enum { SAE_MODE_SAE = 0, SAE_MODE_LRU = 1, SAE_MODE_LFU = 2, SAE_MODE_TWO = 3 };
+
 /* Learned values and meta-parameters, fp64.  Index order: w[sys,user,tool,resp,cot],
  * alpha[chat,agent,struct], mu/sigma[chat,agent].  beta_* weight the NEW value. */
 typedef struct {
   double w[5], alpha[3], mu[2], sigma[2], gamma;
   double eta, a_miss, b_reuse, T, beta_q, beta_ln, beta_gamma;
   uint32_t learn_flags;
-  uint32_t _pad;
+  uint32_t mode;              /* SAE_MODE_* */
 } sae_params;
 
 typedef struct {

@@ -33,7 +33,7 @@ class OrcParams(C.Structure):
                 ("sigma", C.c_double * 2), ("gamma", C.c_double),
                 ("eta", C.c_double), ("a_miss", C.c_double), ("b_reuse", C.c_double),
                 ("T", C.c_double), ("beta_q", C.c_double), ("beta_ln", C.c_double),
-                ("beta_gamma", C.c_double), ("learn_flags", C.c_uint32)]
+                ("beta_gamma", C.c_double), ("learn_flags", C.c_uint32), ("mode", C.c_uint32)]
 
 
 class OrcConfig(C.Structure):
@@ -161,6 +161,7 @@ def make_params(p: dict) -> OrcParams:
     for k in ("gamma", "eta", "a_miss", "b_reuse", "T", "beta_q", "beta_ln", "beta_gamma"):
         setattr(o, k, float(p[k]))
     o.learn_flags = int(p["learn_flags"])
+    o.mode = int(p.get("mode", 0))
     return o
 
 
@@ -168,7 +169,7 @@ def params_dict(o: OrcParams) -> dict:
     return {"w": list(o.w), "alpha": list(o.alpha), "mu": list(o.mu), "sigma": list(o.sigma),
             "gamma": o.gamma, "eta": o.eta, "a_miss": o.a_miss, "b_reuse": o.b_reuse,
             "T": o.T, "beta_q": o.beta_q, "beta_ln": o.beta_ln, "beta_gamma": o.beta_gamma,
-            "learn_flags": o.learn_flags}
+            "learn_flags": o.learn_flags, "mode": o.mode}
 
 
 def make_config(cfg: dict) -> OrcConfig:

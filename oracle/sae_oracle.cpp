@@ -355,6 +355,13 @@ uint64_t block_hash(uint64_t prev, const uint32_t* tok, uint32_t n) {
 enum { Q_EF = 0, Q_CHAT = 1, Q_AGENT = 2, Q_STRUCT = 3 };
 enum { T_SYS = 0, T_USER = 1, T_TOOL = 2, T_RESP = 3, T_COT = 4, T_DECODE = 5 };
 enum { L_TOKENS = 1, L_QUEUES = 2, L_LOGNORMAL = 4, L_DECAY = 8, L_TOKEN_MULT = 16, L_QUEUE_RELATIVE = 32 };
+// Baselines of the paper's comparison and ablation, on the same replay:
+//  MODE_LRU   victim = least recently used: argmin (last, id)
+//  MODE_LFU   victim = least frequently used: argmin (accesses, last, id)
+//  MODE_TWO   Token-Weight-Only: the token-type weights without the multi-queue
+//             architecture: argmin (w_tau / dt, last, id); decode blocks weigh as CoT
+// In the baselines every block sits in one queue (CHAT); counters and learners run as usual.
+enum { MODE_SAE = 0, MODE_LRU = 1, MODE_LFU = 2, MODE_TWO = 3 };
 static const double INV_SQRT2 = 0.70710678118654757;  // 0x3FE6A09E667F3BCD
 
 }  // namespace orc
@@ -366,6 +373,7 @@ typedef struct {
   double w[5], alpha[3], mu[2], sigma[2], gamma;
   double eta, a_miss, b_reuse, T, beta_q, beta_ln, beta_gamma;
   uint32_t learn_flags;
+  uint32_t mode;        // eviction policy: 0 SAECache, 1 LRU, 2 LFU, 3 Token-Weight-Only
 } orc_params;
 
 typedef struct {
@@ -690,7 +698,18 @@ void evict_k(Replica& R, uint64_t k, const std::unordered_map<uint64_t, int>* pi
       key.hash = kv.first;
       key.id = b.id;
       key.last = b.last;
-      if (b.q == Q_EF) {
+      if (R.par.mode == MODE_LRU) {
+        key.tier = 1;
+        key.p = b.last;
+      } else if (R.par.mode == MODE_LFU) {
+        key.tier = 1;
+        key.p = (double)b.acc;
+      } else if (R.par.mode == MODE_TWO) {
+        double dt = R.now - b.last;
+        if (dt < R.cfg.dt_eps) dt = R.cfg.dt_eps;
+        key.tier = 1;
+        key.p = R.par.w[b.tau < 4 ? b.tau : 4] / dt;
+      } else if (b.q == Q_EF) {
         key.tier = 0;
         key.p = (double)b.ntok;
         key.last = 0.0;  // EF ordered by (ntok, id) only
@@ -856,7 +875,9 @@ int orc_admit(void* h, double now, const uint32_t* ptok, const uint8_t* ptyp, ui
   bool untempl = !mt && spb == 0;
   uint32_t omax = std::max<uint32_t>(np - 1, 1);
   std::vector<uint8_t> q(n);
-  for (uint32_t j = 0; j < n; ++j) q[j] = (uint8_t)classify(tau[j], mt, ag, cid, j < spb, untempl);
+  for (uint32_t j = 0; j < n; ++j)
+    q[j] = R.par.mode == MODE_SAE ? (uint8_t)classify(tau[j], mt, ag, cid, j < spb, untempl)
+                                  : (uint8_t)Q_CHAT;   // baselines: one queue
   auto bin = [&](uint32_t j) { return std::min<uint32_t>(cfg.n_bins - 1, (cfg.n_bins * j) / omax); };
 
   // O5 lookup: h = first miss (strict prefix); Pin = resident blocks of the request

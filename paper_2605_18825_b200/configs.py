@@ -16,6 +16,8 @@ Q_EF, Q_CHAT, Q_AGENT, Q_STRUCT = range(4)
 # learner flags
 L_TOKENS, L_QUEUES, L_LOGNORMAL, L_DECAY, L_TOKEN_MULT, L_QUEUE_RELATIVE = 1, 2, 4, 8, 16, 32
 L_DEFAULT = L_TOKENS | L_QUEUES | L_LOGNORMAL | L_DECAY
+# eviction policy modes (include/sae.h SAE_MODE_*): the method and its baselines
+MODE_SAE, MODE_LRU, MODE_LFU, MODE_TWO = 0, 1, 2, 3
 
 HASH_SEED = 0x5AEC0000C0FFEE01
 
@@ -31,6 +33,7 @@ DEFAULT_PARAMS = {
     "eta": 0.1, "a_miss": 5.0, "b_reuse": 2.0, "T": 2.0,
     "beta_q": 0.3, "beta_ln": 0.3, "beta_gamma": 0.3,
     "learn_flags": L_DEFAULT,
+    "mode": MODE_SAE,
 }
 
 

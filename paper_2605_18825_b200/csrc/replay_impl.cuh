@@ -163,7 +163,7 @@ struct Smem {
                                 // segment); worker scan: its finished candidate records
   __align__(8) uint64_t mbar[24];  // bulk-copy stage barriers (worker scan pipeline): full[12], empty[12]
   uint64_t wthr[16], wpfx[16], wpmask[16];   // worker copies of the leader's command parameters
-  double wcw[15], wmu[2], wsg[2];
+  double wcw[15], wmu[2], wsg[2], ww[5];
 };
 
 struct Ctx {               // per-CTA view of one replica (group)
@@ -221,6 +221,8 @@ __device__ __forceinline__ unsigned long long cmd_tag(uint32_t epoch, uint32_t s
 struct ScanP {
   double now, dt_eps, z_cut, gamma;
   uint32_t stamp;
+  uint32_t mode;           // SAE_MODE_* (baselines key every block differently, see sae.h)
+  const double* w;         // [5] token-type weights (Token-Weight-Only)
   const unsigned long long* thr;
   const double* cw;        // [3][5]
   const double* mu;
@@ -292,6 +294,17 @@ __device__ __forceinline__ void finalize_key(const Dev& d, uint64_t base, const 
   const double last = from_obits(x.k1);
   double dt = __dsub_rn(P.now, last);
   if (dt < P.dt_eps) dt = P.dt_eps;
+  if (P.mode != SAE_MODE_SAE) {        // baselines (sae.h): (key, last, id) with key =
+    if (P.mode == SAE_MODE_LRU) {      //   last                       (LRU)
+      x.k0 = x.k1;
+    } else if (P.mode == SAE_MODE_LFU) {   // accesses               (LFU)
+      x.k0 = (uint64_t)__ldcg(d.bacc + base + (x.ss & SLOT_MASK));
+    } else {                           //   w_tau / dt, decode as CoT  (Token-Weight-Only)
+      const uint32_t tau = meta_tau(__ldcg(d.bmeta + base + (x.ss & SLOT_MASK)));
+      x.k0 = obits(__ddiv_rn(P.w[tau < 4 ? tau : 4], dt));
+    }
+    return;
+  }
   if (x.seg <= 8) {
     const uint32_t q = 1 + (x.seg - 1) / 4, tau = (x.seg - 1) & 3;
     const double p = survival(dt, P.mu[q - 1], P.sg[q - 1], P.z_cut);
@@ -637,13 +650,16 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
         P.now = s.st.now;
         P.thr = (const unsigned long long*)s.st.thr; P.cw = &s.cw[0][0];
         P.mu = s.st.par.mu; P.sg = s.st.par.sigma;
+        P.mode = s.st.par.mode; P.w = s.st.par.w;
       } else {        // published by the leader before the command: stage into smem
         if (tid < 16) s.wthr[tid] = __ldcg(&g->thr[tid]);
         if (tid < 15) s.wcw[tid] = __ldcg(&g->cw[0][0] + tid);
+        if (tid < 5) s.ww[tid] = __ldcg(&g->w[tid]);
         if (tid < 2) { s.wmu[tid] = __ldcg(&g->mu[tid]); s.wsg[tid] = __ldcg(&g->sigma[tid]); }
         cta_sync();
         P.now = __ldcg(&g->now);
         P.thr = (const unsigned long long*)s.wthr; P.cw = s.wcw; P.mu = s.wmu; P.sg = s.wsg;
+        P.mode = __ldcg(&g->mode); P.w = s.ww;
       }
       P.stamp = __ldcg(&g->stamp);
       P.gamma = leader ? s.st.par.gamma : __ldcg(&g->gamma);
@@ -1272,6 +1288,10 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
   // live, unpinned blocks per segment (maintained counts minus this round's pins)
   if (tid < 16) s.segtot[tid] = tid < NSEG ? st.segcnt[tid] - s.pincnt[tid] : 0u;
   bool proved = false;
+  // The baselines (sae.h SAE_MODE_*) key every block by a value without the class
+  // monotonicity the thresholds rely on: each of their passes takes every unpinned block as a
+  // candidate (Alg.1's full rescan), so their selection is exact by construction.
+  const bool baseline = st.par.mode != SAE_MODE_SAE;
   for (int attempt = 0; attempt < 3; ++attempt) {
     if (tid < 16) { s.used[tid] = 0; }
     if (tid == 0) {
@@ -1283,9 +1303,14 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
         for (int i = 0; i < 16; ++i) { g->cnt[i] = 0; g->thr[i] = st.thr[i]; }
         for (int q = 0; q < 3; ++q) for (int t = 0; t < 5; ++t) g->cw[q][t] = s.cw[q][t];
         for (int i = 0; i < 2; ++i) { g->mu[i] = st.par.mu[i]; g->sigma[i] = st.par.sigma[i]; }
+        for (int i = 0; i < 5; ++i) g->w[i] = st.par.w[i];
         g->gamma = st.par.gamma;
+        g->mode = st.par.mode;
       }
     }
+    if (baseline && tid < 16) st.thr[tid] = ~0ull;   // baselines: every block is a candidate
+    cta_sync();
+    if (gm && baseline && tid < 16) g->thr[tid] = ~0ull;
     cta_sync();
     uint64_t t0 = gtimer();
     issue(c, CMD_SCAN);
@@ -1329,6 +1354,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
       P.now = now; P.thr = (const unsigned long long*)st.thr; P.cw = &s.cw[0][0];
       P.mu = st.par.mu; P.sg = st.par.sigma; P.gamma = st.par.gamma;
       P.dt_eps = d.dt_eps; P.z_cut = d.z_cut; P.stamp = 0;
+      P.mode = st.par.mode; P.w = st.par.w;
       for (uint32_t i = tid; i < nc; i += NT) finalize_key(d, c.base, P, c.cand[i]);
       if (tid == 0) s.fin = 1;
       cta_sync();
@@ -1338,7 +1364,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
     c0 = s.cnt[0];
     e = min(m, s.segtot[0]);
     mp = m - e;
-    uint64_t Kth = ~0ull;
+    uint64_t Kth = ~0ull, Kth1 = ~0ull;   // the m-th victim's (P, last) when staged
     staged = false;
     const uint64_t tR = gtimer();
     if (nc >= m) {
@@ -1369,13 +1395,17 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
       // growth, then sort the staged set: its first m are the victims, in order
       const uint64_t Ub = nc >= m ? (s.pfx[0] | ~s.pmask[0]) : ~0ull;
       stage_victims(c, nc, Ub);
-      if (nc >= m) Kth = c.vbuf[m - 1].k0;
+      if (nc >= m) { Kth = c.vbuf[m - 1].k0; Kth1 = c.vbuf[m - 1].k1; }
       if (tid == 0) st.tph[15] += gtimer() - tV;
     }
     // ---- exactness check: every block a threshold left out must lose to the mp-th
     //      scored candidate.  EF: enough heads.  Class c: a non-candidate has last > T_c,
-    //      so dt < now - T_c and, P being strictly decreasing in dt within a class,
-    //      P > P_c(now - T_c).  STRUCT class: a non-candidate has P > T_S.
+    //      so dt < now - T_c and, P being non-increasing in dt within a class (tests/
+    //      test_prop_monotone.py), P >= P_c(now - T_c) =: PT; it loses to the m-th victim
+    //      (Pth, last_m, id_m) if Pth < PT, or if Pth == PT and last_m <= T_c (the tie on P is
+    //      broken by last: every non-candidate is younger) -- the case of a tie group of equal
+    //      last (one request's blocks) straddling the threshold.  STRUCT: a non-candidate has
+    //      P > T_S.
     if (tid == 0 && c0 < e) atomicOr(&s.fail, 1u);
     if (mp > 0 && tid >= 1 && tid < NSEG && s.segtot[tid] > s.cnt[tid]) {
       const uint32_t gsg = tid;
@@ -1392,7 +1422,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
         // P(dt) (fdlibm ln/erfc: a few ulp, amplified by at most |z| <= z_cut in the erfc
         // tail); a segment that misses the margin is only rescanned, never decided wrongly
         const double PT = __ddiv_rn(__dmul_rn(s.cw[q - 1][tau], p), dt);
-        ok = Pth < PT - PT * 0x1p-30;
+        ok = Pth < PT - PT * 0x1p-30 || (Pth <= PT && Kth1 <= st.thr[gsg]);
       }
       if (!ok) atomicOr(&s.fail, 1u << gsg);
     }
@@ -1465,6 +1495,12 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
     sort_cands(c.vbuf, N);       // small: the m victims in (k0, last, id) order
   }
   }                        // !staged
+  if (baseline) {                    // no thresholds to carry: copy the victims out
+    for (uint32_t v = tid; v < m; v += NT) c.cand[v] = c.vbuf[v];
+    if (tid == 0) st.tph[12] += gtimer() - tS;
+    cta_sync();
+    return;
+  }
   // ---- carry thresholds: trim segments holding far more candidates than they use
   for (uint32_t v = tid; v < m; v += NT) atomicAdd(&s.used[c.vbuf[v].seg], 1u);
   cta_sync();
@@ -1780,7 +1816,8 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
     const uint64_t H = b.h[bo + j];
     const uint32_t tau = b.tau[bo + j];
     const int32_t sl = tbl_find(tkey, tval, d.tmask, H);
-    const uint32_t q = classify(tau, mt, ag, cid, j < spb, untempl);
+    const uint32_t q = st.par.mode == SAE_MODE_SAE ? classify(tau, mt, ag, cid, j < spb, untempl)
+                                                   : (uint32_t)Q_CHAT;   // baselines: one queue
     b.slot[bo + j] = sl;
     b.q[bo + j] = (uint8_t)q;
     if (j < (uint32_t)NT) { rH = H; rsl = sl; rq = q; rtau = tau; }

@@ -110,7 +110,8 @@ struct GroupCtl {          // hot words on separate 128-byte lines (polled / ato
   alignas(128) unsigned cmd, stamp, shift, active;   // read-only while a command runs
   unsigned long long thr[16], pfx[16], pmask[16];
   double now, gamma, dt_eps, z_cut;
-  double cw[3][5], mu[2], sigma[2];
+  double cw[3][5], mu[2], sigma[2], w[5];
+  unsigned mode;
   alignas(128) unsigned hist[NSEG * 256];
 };
 
@@ -710,6 +711,10 @@ static sae_status create_impl(const sae_config* cfg, sae_ctx* ctx) {
   }
   d.GP = (uint32_t)gp;
   d.cand_smem = (d.C <= ctx->var.cand_max && d.GP == 1) ? 1u : 0u;
+  if (cfg->init.mode > SAE_MODE_TWO || (cfg->init.mode != SAE_MODE_SAE && !d.cand_smem)) {
+    ctx->last_error = "baseline modes need a pool that fits one CTA's candidate buffer";
+    return SAE_E_INVAL;
+  }
   d.bulk_ok = (d.C % 4 == 0) ? 1u : 0u;
   d.trim_at = 8;
   d.trim_to = 4;
@@ -804,6 +809,10 @@ static sae_status scatter_params(sae_ctx* ctx, const sae_params* dev_in, uint32_
 sae_status sae_set_params(sae_ctx* ctx, uint32_t replica, const sae_params* p, sae_stream st) {
   if (!ctx || !p || replica >= ctx->d.R) return SAE_E_INVAL;
   if (!(p->sigma[0] > 0.0) || !(p->sigma[1] > 0.0)) return SAE_E_INVAL;
+  if (p->mode > SAE_MODE_TWO || (p->mode != SAE_MODE_SAE && !ctx->d.cand_smem)) {
+    ctx->last_error = "baseline modes need a pool that fits one CTA's candidate buffer";
+    return SAE_E_INVAL;
+  }
   cudaStream_t s = (cudaStream_t)st;
   sae_params* tmp;
   CK(cudaMallocAsync(&tmp, sizeof(sae_params), s));

@@ -35,7 +35,7 @@ class sae_params(C.Structure):
                 ("sigma", C.c_double * 2), ("gamma", C.c_double), ("eta", C.c_double),
                 ("a_miss", C.c_double), ("b_reuse", C.c_double), ("T", C.c_double),
                 ("beta_q", C.c_double), ("beta_ln", C.c_double), ("beta_gamma", C.c_double),
-                ("learn_flags", C.c_uint32), ("_pad", C.c_uint32)]
+                ("learn_flags", C.c_uint32), ("mode", C.c_uint32)]
 
 
 class sae_config(C.Structure):
@@ -163,6 +163,7 @@ def make_params(p: dict) -> sae_params:
     for k in ("gamma", "eta", "a_miss", "b_reuse", "T", "beta_q", "beta_ln", "beta_gamma"):
         setattr(o, k, float(p[k]))
     o.learn_flags = int(p["learn_flags"])
+    o.mode = int(p.get("mode", 0))
     return o
 
 
@@ -170,7 +171,7 @@ def params_dict(o: sae_params) -> dict:
     return {"w": list(o.w), "alpha": list(o.alpha), "mu": list(o.mu), "sigma": list(o.sigma),
             "gamma": o.gamma, "eta": o.eta, "a_miss": o.a_miss, "b_reuse": o.b_reuse, "T": o.T,
             "beta_q": o.beta_q, "beta_ln": o.beta_ln, "beta_gamma": o.beta_gamma,
-            "learn_flags": o.learn_flags}
+            "learn_flags": o.learn_flags, "mode": o.mode}
 
 
 # torch dtypes carrying the C unsigned layouts bit for bit

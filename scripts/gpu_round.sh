@@ -13,6 +13,8 @@
 #   ncu_c4x     full capture of a C4x 200-request k_replay launch
 #   sanitize    compute-sanitizer memcheck / racecheck / synccheck on small replays
 #   sass        cuobjdump -sass of libsae.so (k_replay) -> gpurun_out/sass_k_replay.txt
+#   ablation    scripts/ablation.py on the balanced, multi-turn- and single-turn-dominant mixes
+#   sweep       C5 bench lines over the select's SAE_SLACK / SAE_TRIM knobs
 # Summaries worth keeping are copied into profiles/ by hand (scripts/profile_summary.py).
 set -u
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
@@ -56,6 +58,16 @@ for step in "$@"; do
     sass)
       cuobjdump -sass paper_2605_18825_b200/libsae.so > $O/sass_all.txt 2>&1
       grep -cE 'UBLKCP|SYNCS' $O/sass_all.txt ;;
+    ablation)
+      for w in c5 c2 c4s; do
+        timeout 900 python scripts/ablation.py --workload $w --out $O/ablation_$w > $O/ablation_$w.log 2>&1
+        tail -14 $O/ablation_$w.log
+      done ;;
+    sweep)
+      for sl in 16 8 4; do for tr in 8,4 4,2 3,2; do
+        SAE_SLACK=$sl SAE_TRIM=$tr timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/sweep_${sl}_${tr}.json 2>/dev/null
+        python -c "import json,sys; d=json.loads(open('$O/sweep_${sl}_${tr}.json').read().strip().splitlines()[-1]); print('slack $sl trim $tr', round(d['value']), d['score_select_phase']['passes_per_request'], round(d['score_select_phase']['cands_per_pass']))"
+      done; done ;;
     *) echo "unknown step $step" ;;
   esac
 done
