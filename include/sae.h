@@ -73,7 +73,10 @@ enum {
   SAE_L_LOGNORMAL = 4,       /* LognormalParams */
   SAE_L_DECAY = 8,           /* decay power */
   SAE_L_TOKEN_MULT = 16,     /* multiplicative token rule (Alg. P:725) instead of P:703-707 */
-  SAE_L_QUEUE_RELATIVE = 32  /* relative queue rule P:814-817 instead of Alg. P:583-593 */
+  SAE_L_QUEUE_RELATIVE = 32, /* relative queue rule P:814-817 instead of Alg. P:583-593 */
+  SAE_L_ADAPTIVE_BETA = 64   /* LognormalParams' EMA factor adapts (A28):
+                                rho = mean (x - mu)^2 / sigma^2 over the ln-intervals x;
+                                beta_ln doubled (at most 1) if rho > 1, else halved */
 };
 
 /* Eviction policy of a replica (sae_params.mode).  SAE_MODE_SAE is the paper's method; the

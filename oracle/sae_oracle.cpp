@@ -354,7 +354,8 @@ uint64_t block_hash(uint64_t prev, const uint32_t* tok, uint32_t n) {
 // ---------------------------------------------------------------------------
 enum { Q_EF = 0, Q_CHAT = 1, Q_AGENT = 2, Q_STRUCT = 3 };
 enum { T_SYS = 0, T_USER = 1, T_TOOL = 2, T_RESP = 3, T_COT = 4, T_DECODE = 5 };
-enum { L_TOKENS = 1, L_QUEUES = 2, L_LOGNORMAL = 4, L_DECAY = 8, L_TOKEN_MULT = 16, L_QUEUE_RELATIVE = 32 };
+enum { L_TOKENS = 1, L_QUEUES = 2, L_LOGNORMAL = 4, L_DECAY = 8, L_TOKEN_MULT = 16, L_QUEUE_RELATIVE = 32,
+       L_ADAPTIVE_BETA = 64 };
 // Baselines of the paper's comparison and ablation, on the same replay:
 //  MODE_LRU   victim = least recently used: argmin (last, id)
 //  MODE_LFU   victim = least frequently used: argmin (accesses, last, id)
@@ -564,7 +565,8 @@ void learn_queues(Replica& R) {
   for (int q = 0; q < 3; ++q) { R.qh[q] = 0; R.qe[q] = 0; }
 }
 
-// LognormalParams: Alg. P:762-784 (threshold > 20 per A23; population std A24).
+// LognormalParams: Alg. P:762-784 (threshold > 20 per A23; population std A24); with
+// L_ADAPTIVE_BETA the EMA factor adapts to the observation variance (A28).
 void learn_lognormal(Replica& R) {
   orc_params& p = R.par;
   for (int s = 0; s < 2; ++s) {
@@ -577,8 +579,18 @@ void learn_lognormal(Replica& R) {
       for (size_t i = 0; i < n; ++i) d[i] = (x[i] - m) * (x[i] - m);
       double v = tree_sum(d) / (double)n;
       double sd = std::sqrt(v);
-      p.mu[s] = p.mu[s] + p.beta_ln * (m - p.mu[s]);
-      p.sigma[s] = p.sigma[s] + p.beta_ln * (sd - p.sigma[s]);
+      double b = p.beta_ln;
+      if (p.learn_flags & L_ADAPTIVE_BETA) {
+        // adaptive EMA factor (reading A28): the observations' variance around the
+        // CURRENT model, v_obs = mean (x - mu)^2, against the model's sigma^2: high (rho > 1)
+        // -> track faster (beta doubled, at most 1), low -> steadier (beta halved)
+        for (size_t i = 0; i < n; ++i) d[i] = (x[i] - p.mu[s]) * (x[i] - p.mu[s]);
+        double vobs = tree_sum(d) / (double)n;
+        double rho = vobs / (p.sigma[s] * p.sigma[s]);
+        b = rho > 1.0 ? std::min(2.0 * p.beta_ln, 1.0) : 0.5 * p.beta_ln;
+      }
+      p.mu[s] = p.mu[s] + b * (m - p.mu[s]);
+      p.sigma[s] = p.sigma[s] + b * (sd - p.sigma[s]);
       if (p.sigma[s] < 0.1) p.sigma[s] = 0.1;
       while (iv.size() > R.cfg.interval_keep) iv.pop_front();
     }

@@ -39,4 +39,5 @@ def variants() -> dict:
     for name, fl in ladder:
         out["FixedParamMQ" + name] = dict(copy.deepcopy(fixed), learn_flags=fl)
     out["SAECache(relative-queue)"] = dict(copy.deepcopy(base), learn_flags=C.L_DEFAULT | C.L_QUEUE_RELATIVE)
+    out["SAECache(adaptive-beta)"] = dict(copy.deepcopy(base), learn_flags=C.L_DEFAULT | C.L_ADAPTIVE_BETA)
     return out

@@ -15,6 +15,7 @@ SYS, USER, TOOL, RESP, COT, DECODE = range(6)
 Q_EF, Q_CHAT, Q_AGENT, Q_STRUCT = range(4)
 # learner flags
 L_TOKENS, L_QUEUES, L_LOGNORMAL, L_DECAY, L_TOKEN_MULT, L_QUEUE_RELATIVE = 1, 2, 4, 8, 16, 32
+L_ADAPTIVE_BETA = 64   # LognormalParams' EMA factor adapts to the observation variance
 L_DEFAULT = L_TOKENS | L_QUEUES | L_LOGNORMAL | L_DECAY
 # eviction policy modes (include/sae.h SAE_MODE_*): the method and its baselines
 MODE_SAE, MODE_LRU, MODE_LFU, MODE_TWO = 0, 1, 2, 3

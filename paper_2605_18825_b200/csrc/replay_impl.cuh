@@ -1010,10 +1010,23 @@ __device__ void learn(Ctx& c) {
         }
         cta_sync();
         double v = __ddiv_rn(tree_sum(y, P), (double)n);
+        double b = p.beta_ln;
+        if (f & SAE_L_ADAPTIVE_BETA) {   // P:758-760 (A28): observation variance around the model
+          const double mu0 = p.mu[sidx];
+          for (int i = threadIdx.x; i < P; i += NT) {
+            double x = (uint32_t)i < n ? ring[(first + i) % RMAX] : 0.0;
+            double dd = __dsub_rn(x, mu0);
+            y[i] = (uint32_t)i < n ? __dmul_rn(dd, dd) : 0.0;
+          }
+          cta_sync();
+          const double vobs = __ddiv_rn(tree_sum(y, P), (double)n);
+          const double rho = __ddiv_rn(vobs, __dmul_rn(p.sigma[sidx], p.sigma[sidx]));
+          b = rho > 1.0 ? fmin(__dmul_rn(2.0, p.beta_ln), 1.0) : __dmul_rn(0.5, p.beta_ln);
+        }
         if (threadIdx.x == 0) {
           double sd = __dsqrt_rn(v);
-          p.mu[sidx] = __dadd_rn(p.mu[sidx], __dmul_rn(p.beta_ln, __dsub_rn(m, p.mu[sidx])));
-          p.sigma[sidx] = __dadd_rn(p.sigma[sidx], __dmul_rn(p.beta_ln, __dsub_rn(sd, p.sigma[sidx])));
+          p.mu[sidx] = __dadd_rn(p.mu[sidx], __dmul_rn(b, __dsub_rn(m, p.mu[sidx])));
+          p.sigma[sidx] = __dadd_rn(p.sigma[sidx], __dmul_rn(b, __dsub_rn(sd, p.sigma[sidx])));
           if (p.sigma[sidx] < 0.1) p.sigma[sidx] = 0.1;
           if (n > d.iv_keep) st.iv_len[sidx] = d.iv_keep;
         }

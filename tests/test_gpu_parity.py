@@ -27,7 +27,7 @@ def test_c1_replay_bit_exact(c1, K):
 
 
 @pytest.mark.parametrize("flags", [0, C.L_TOKENS, C.L_DEFAULT | C.L_TOKEN_MULT,
-                                   C.L_DEFAULT | C.L_QUEUE_RELATIVE])
+                                   C.L_DEFAULT | C.L_QUEUE_RELATIVE, C.L_DEFAULT | C.L_ADAPTIVE_BETA])
 def test_c1_learner_variants(c1, flags):
     p = dict(C.DEFAULT_PARAMS)
     p["learn_flags"] = flags
@@ -226,3 +226,10 @@ def test_c5_mean_w_sync_matches_oracle():
             refs[r].set_params(newp[r])
     for r in range(R):
         assert_params_equal(S.params_dict(cache.stats(r).params), refs[r].params())
+
+
+def test_c2_prefix_adaptive_beta():
+    """The adaptive EMA factor of LognormalParams (A28) over a C2 prefix."""
+    p = dict(C.DEFAULT_PARAMS)
+    p["learn_flags"] = C.L_DEFAULT | C.L_ADAPTIVE_BETA
+    compare_replay(T.make("c2", n_requests=6000), C.policy_config(2304, params=p))

@@ -90,6 +90,39 @@ def test_lognormal_closed_forms():
     assert len(R.intervals(1)) == 200                    # truncate to last 200
 
 
+def test_adaptive_beta_closed_forms():
+    """Adaptive EMA factor (reading A28): rho = mean (x - mu)^2 / sigma^2 over the
+    ln-intervals; rho > 1 -> beta doubled (at most 1), else halved."""
+    F = C.L_LOGNORMAL | C.L_ADAPTIVE_BETA
+    # observations exactly at the model mean: rho = 0 -> beta 0.15: mu stays, sigma 1 -> 0.85
+    R = replica(mu=[2.0, 2.0], sigma=[1.0, 1.0], beta_ln=0.3, learn_flags=F)
+    for _ in range(21):
+        R.push_interval(0, 2.0)
+    R.update()
+    p = R.params()
+    assert p["mu"][0] == 2.0 and abs(p["sigma"][0] - 0.85) < 1e-15
+    # without the flag the same update uses beta 0.3: sigma -> 0.7
+    R = replica(mu=[2.0, 2.0], sigma=[1.0, 1.0], beta_ln=0.3, learn_flags=C.L_LOGNORMAL)
+    for _ in range(21):
+        R.push_interval(0, 2.0)
+    R.update()
+    assert abs(R.params()["sigma"][0] - 0.7) < 1e-15
+    # observations 3 sigma away: rho = 9 -> beta 0.6: mu 2 -> 2 + 0.6 x 3 = 3.8, sigma -> 0.4
+    R = replica(mu=[2.0, 2.0], sigma=[1.0, 1.0], beta_ln=0.3, learn_flags=F)
+    for _ in range(21):
+        R.push_interval(1, 5.0)
+    R.update()
+    p = R.params()
+    assert abs(p["mu"][1] - 3.8) < 1e-15 and abs(p["sigma"][1] - 0.4) < 1e-15
+    # beta 0.7 doubled is capped at 1: jump to the sample statistics (sigma floor 0.1)
+    R = replica(mu=[2.0, 2.0], sigma=[1.0, 1.0], beta_ln=0.7, learn_flags=F)
+    for _ in range(21):
+        R.push_interval(0, 6.0)
+    R.update()
+    p = R.params()
+    assert p["mu"][0] == 6.0 and p["sigma"][0] == 0.1
+
+
 def test_lognormal_statistics_vs_numpy():
     rng = np.random.default_rng(4)
     x = rng.normal(4.82, 1.25, 1000)
