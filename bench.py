@@ -46,6 +46,10 @@ WORKLOADS = {
     "c2": dict(cfg="c2", per_step=5000, ref_step=1500,
                desc="C2 multi-turn-dominated trace (Table 2 row 50/30/10/5/5), 100K requests, "
                     "C=2304 blocks (36K tokens), 1 replica per GPU"),
+    "c3": dict(cfg="c3", per_step=2000, ref_step=100, prefill=2000,
+               desc="C3 balanced trace (Table 2 row 30/20/25/15/10, P:887), C=16,384 blocks "
+                    "(256 Ki tokens), one cooperative replica group per GPU; pool pre-filled with the "
+                    "trace's first 2K requests (untimed; it fills after ~300)"),
     "c4": dict(cfg="c4", per_step=2000, ref_step=2, prefill=100_000,
                desc="C4 single-turn-dominated templated trace (Table 2 row 10/10/40/25/15), "
                     "4M-block (64 Mi-token) pool, one 148-CTA cooperative replica group per GPU; "
@@ -409,10 +413,15 @@ def run_ours(args, wl, ws, rank, local):
         tr0 = make_trace(wl, rank, n_requests=(pre + per * (W + 2 * K + 1)) if pre else None)
         pol = CFG.policy_config(tr0["config"]["capacity"])
         cache = S.SaeCache(pol["capacity"], n_replicas=1, policy=pol)
+        fill_at = None                    # first request of the trace that had to evict
         for lo in range(0, pre, 20000):   # untimed pre-fill of the pool
-            cache.admit_batch(S.batch_to_torch(slice_batch(tr0, lo, min(lo + 20000, pre)),
-                                               device=torch.device("cuda", local)))
+            o = cache.admit_batch(S.batch_to_torch(slice_batch(tr0, lo, min(lo + 20000, pre)),
+                                                   device=torch.device("cuda", local)))
             torch.cuda.synchronize()
+            if fill_at is None:
+                nz = torch.nonzero(o["n_victims"] > 0)
+                if nz.numel():
+                    fill_at = lo + int(nz[0].item())
 
         def step_batch(step):
             return slice_batch(tr0, pre + step * per, pre + (step + 1) * per)
@@ -430,7 +439,14 @@ def run_ours(args, wl, ws, rank, local):
         x["tokens"], x["types"] = tok_d, typ_d
         return x
 
-    steps_dev = [to_dev(step_batch(s)) for s in range(W + K)]
+    host_batches = [step_batch(s) for s in range(W + K)]
+    steps_dev = [to_dev(hb) for hb in host_batches]
+    # K1 algorithmic bytes of the timed steps: 5 B per token read (u32 id + u8 type), 10 B per
+    # block written (u64 hash, u8 tau, u8 ntok)
+    tok_timed = sum(int(hb["prompt_len"].astype(np.int64).sum() + hb["decode_len"].astype(np.int64).sum())
+                    for hb in host_batches[W:])
+    blk_timed = sum(int((-(-hb["prompt_len"].astype(np.int64) // 16) - (-hb["decode_len"].astype(np.int64) // 16)).sum())
+                    for hb in host_batches[W:])
     outs = [cache.alloc_out(b) for b in steps_dev]
     torch.cuda.synchronize()
 
@@ -474,6 +490,7 @@ def run_ours(args, wl, ws, rank, local):
     clocks = clk.stop()
     launches = cache.launches() - l0
     rep_ms, rep_n = cache.profile_read()
+    hash_ms, hash_n = cache.profile_read_hash()
     cache.profile(False)
     cache.sync()
     st1 = [cache.stats(r) for r in range(R)]
@@ -557,6 +574,15 @@ def run_ours(args, wl, ws, rank, local):
                                         zip(st0[0].phase_ns, st1[0].phase_ns)]}
     if ph11 > 0:
         phase_info["streamed_GBps"] = phase_info["bytes_streamed_per_pass"] / phase_info["scan_ns_per_pass"]
+    phase_info["stage2_share_of_chunks"] = d("stage2_chunks") / max(d("eviction_rounds") + d("learner_firings"), 1)
+    if wl.get("prefill"):
+        phase_info["pool_full_at_request"] = fill_at
+        phase_info["pool_full_at_fraction_of_1M_trace"] = None if fill_at is None else fill_at / 1e6
+    k1 = {"kernel": "k_hash", "launches": int(hash_n), "ms_per_step": hash_ms / max(K, 1),
+          "blocks_hashed_per_s": blk_timed / max(hash_ms * 1e-3, 1e-12),
+          "tokens_per_s": tok_timed / max(hash_ms * 1e-3, 1e-12),
+          "algorithmic_GBps": (5.0 * tok_timed + 10.0 * blk_timed) / max(hash_ms * 1e-3, 1e-12) / 1e9,
+          "bytes_model": "5 B per token read + 10 B per block written"}
     avg_ms = rep_ms / max(rep_n, 1)
     achieved = (alg_bytes / max(rep_n, 1)) / (avg_ms * 1e-3) / 1e9 if rep_n else 0.0
     traffic = None
@@ -592,6 +618,7 @@ def run_ours(args, wl, ws, rank, local):
         "gpu_launches": int(launches),
         "clocks": clocks,
         "score_select_phase": phase_info,
+        "k1_hash_phase": k1,
         "roofline": {"bound": "hbm", "kernel": "k_replay", "achieved": achieved, "peak": hbm,
                      "peak_source": src, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic,

@@ -190,6 +190,7 @@ typedef struct {
   uint64_t phase_ns[16];
   uint64_t select_narrow, select_raw;   /* narrowings (candidate sets > 4096) and raw candidates */
   sae_params params;
+  uint64_t stage2_chunks;   /* victim chunks that reached Alg.1 Stage 2: EF could not cover them */
 } sae_replica_stats;
 
 /* Whole-ctx totals of the additive counters (every replica summed), u64, for the multi-GPU
@@ -330,6 +331,9 @@ uint64_t sae_launch_count(const sae_ctx* ctx);
  * elapsed milliseconds and the number of launches since the last read, and resets. */
 sae_status sae_profile(sae_ctx* ctx, int enable);
 sae_status sae_profile_read(sae_ctx* ctx, double* ms_total, uint64_t* n_launches);
+/* Same for the K1 hashing kernel (chained XXH64 + tau of every block of a batch, P:158-159,
+ * P:318-320) launched by sae_admit_batch / sae_lookup while profiling is enabled. */
+sae_status sae_profile_read_hash(sae_ctx* ctx, double* ms_total, uint64_t* n_launches);
 
 #ifdef __cplusplus
 }

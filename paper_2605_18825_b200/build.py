@@ -36,11 +36,13 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Compile csrc/ into libsae.so (or `out`, with extra -D`defines`, e.g. a debug build)."""
+    if out is None and not force and not stale():
         return OUT
-    tmp = OUT + ".tmp%d" % os.getpid()
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp,
+    dst = out or OUT
+    tmp = dst + ".tmp%d" % os.getpid()
+    cmd = [nvcc(), *NVCC_FLAGS, *["-D" + d for d in defines], "-I", os.path.join(ROOT, "include"), "-o", tmp,
            *[os.path.join(CSRC, s) for s in SOURCES]]
     r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     if r.returncode != 0:
@@ -48,8 +50,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, dst)
+    return dst
 
 
 if __name__ == "__main__":

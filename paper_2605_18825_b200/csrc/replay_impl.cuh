@@ -1377,6 +1377,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
     c0 = s.cnt[0];
     e = min(m, s.segtot[0]);
     mp = m - e;
+    if (tid == 0 && attempt == 0 && count_pass && mp > 0) st.stage2_chunks++;
     uint64_t Kth = ~0ull, Kth1 = ~0ull;   // the m-th victim's (P, last) when staged
     staged = false;
     const uint64_t tR = gtimer();
@@ -1395,6 +1396,18 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
         if (tid == 0) s.target[0] = m;
         cta_sync();
         radix_select(c.cand, nc, false, 1u, s);
+        // the m-th victim's last (for the exactness check's tie rule): rank m - nless by k1
+        // inside the k0 tie group (a large tie group is one request's blocks in one class)
+        const uint64_t K0 = s.pfx[0];
+        const uint32_t nless = s.below[0];
+        cta_sync();
+        if (tid == 0) s.target[0] = m - nless;
+        cta_sync();
+        radix_select(c.cand, nc, false, 1u, s, 1, K0);
+        Kth1 = s.pfx[0];
+        cta_sync();
+        if (tid == 0) { s.pfx[0] = K0; s.below[0] = nless; }   // restore for the unstaged path
+        cta_sync();
       }
       Kth = s.pfx[0];
     } else {
@@ -1443,6 +1456,15 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
     const uint32_t fail = s.fail;
     if (tid == 0) st.tph[3] += gtimer() - t0;
     if (fail == 0) { proved = true; break; }
+#ifdef SAE_DEBUG_SELECT
+    if (tid == 0)
+      printf("select fail r=%u req=%llu attempt=%d m=%u e=%u mp=%u nc=%u c0=%u staged=%d Kth=%.17g Kth1=%.17g fail=%x\n",
+             c.r, (unsigned long long)st.requests, attempt, m, e, mp, nc, c0, (int)staged, from_obits(Kth),
+             from_obits(Kth1), fail);
+    if (tid < NSEG && ((fail >> tid) & 1u))
+      printf("   seg %d segtot=%u cnt=%u thr=%.17g (raw %llx)\n", tid, s.segtot[tid], s.cnt[tid],
+             from_obits(st.thr[tid]), (unsigned long long)st.thr[tid]);
+#endif
     if (tid < 10 && ((fail >> tid) & 1u)) st.select_fail_seg[tid]++;
     if (tid < NSEG && (((fail >> tid) & 1u) || attempt >= 1)) st.thr[tid] = ~0ull;
     cta_sync();

@@ -77,6 +77,7 @@ struct RState {
   uint64_t learner_firings, eviction_rounds, blocks_scored, blocks_scored_struct;
   uint64_t select_passes, select_cands, select_big, select_fail_seg[10];
   uint64_t select_narrow, select_raw;
+  uint64_t stage2_chunks;  // chunks whose victims reach Alg.1 Stage 2 (EF cannot cover them)
   uint64_t tph[16];         // leader phase timers (ns): probe, scan, narrow, select, apply, learn, insert, rebuild,
                             // + issue(): start barrier, own partition, end barrier, (spare)
   uint32_t segcnt[16];     // live blocks per segment (maintained at insert / touch / evict)
@@ -613,6 +614,7 @@ struct sae_ctx {
   Variant var;
   bool prof = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_hash;   // K1 (k_hash) launches
 };
 
 static uint32_t pow2_at_least(uint64_t x) {
@@ -890,7 +892,17 @@ static sae_status prepare(sae_ctx* ctx, const sae_batch* b, BatchDev& x, cudaStr
   CK(cudaMemsetAsync(x.run_start, 0xFF, R * 4, s));
   CK(cudaMemsetAsync(x.run_end, 0, R * 4, s));
   k_runs<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, ctx->d);
+  cudaEvent_t h0 = nullptr, h1 = nullptr;
+  if (ctx->prof) {
+    CK(cudaEventCreate(&h0));
+    CK(cudaEventCreate(&h1));
+    CK(cudaEventRecord(h0, s));
+  }
   k_hash<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(x, ctx->d);
+  if (ctx->prof) {
+    CK(cudaEventRecord(h1, s));
+    ctx->prof_hash.push_back({h0, h1});
+  }
   ctx->launches += 6;
   CK(cudaGetLastError());
   return SAE_OK;
@@ -1138,6 +1150,7 @@ sae_status sae_stats(sae_ctx* ctx, uint32_t replica, sae_replica_stats* out, sae
   for (int g = 0; g < 16; ++g) out->phase_ns[g] = rs.tph[g];
   out->select_narrow = rs.select_narrow;
   out->select_raw = rs.select_raw;
+  out->stage2_chunks = rs.stage2_chunks;
   {
     unsigned long long w = 0;
     CK(cudaMemcpy(&w, &ctx->d.ctl[replica].wscan_ns, 8, cudaMemcpyDeviceToHost));
@@ -1235,6 +1248,30 @@ sae_status sae_profile(sae_ctx* ctx, int enable) {
   if (!ctx) return SAE_E_INVAL;
   ctx->prof = enable != 0;
   return SAE_OK;
+}
+
+static sae_status read_events(sae_ctx* ctx, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& ev,
+                              double* ms_total, uint64_t* n_launches) {
+  double tot = 0.0;
+  uint64_t n = 0;
+  for (auto& pr : ev) {
+    CK(cudaEventSynchronize(pr.second));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, pr.first, pr.second));
+    tot += ms;
+    ++n;
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  ev.clear();
+  if (ms_total) *ms_total = tot;
+  if (n_launches) *n_launches = n;
+  return SAE_OK;
+}
+
+sae_status sae_profile_read_hash(sae_ctx* ctx, double* ms_total, uint64_t* n_launches) {
+  if (!ctx) return SAE_E_INVAL;
+  return read_events(ctx, ctx->prof_hash, ms_total, n_launches);
 }
 
 sae_status sae_profile_read(sae_ctx* ctx, double* ms_total, uint64_t* n_launches) {

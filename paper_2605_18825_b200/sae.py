@@ -16,7 +16,7 @@ import torch
 from . import configs as CFG
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsae.so")
+LIB_PATH = os.environ.get("SAE_LIB_PATH") or os.path.join(_HERE, "libsae.so")   # override: debug builds
 
 SAE_ABI_VERSION = 3
 ERRORS = {0: "SAE_OK", -1: "SAE_E_INVAL", -2: "SAE_E_CAPACITY_ZERO", -3: "SAE_E_EMPTY",
@@ -80,7 +80,7 @@ class sae_replica_stats(C.Structure):
                 ("select_big", C.c_uint64), ("select_fail_seg", C.c_uint64 * 10),
                 ("phase_ns", C.c_uint64 * 16),
                 ("select_narrow", C.c_uint64), ("select_raw", C.c_uint64),
-                ("params", sae_params)]
+                ("params", sae_params), ("stage2_chunks", C.c_uint64)]
 
 
 class sae_traj(C.Structure):
@@ -93,7 +93,7 @@ EXPORTS = ["sae_create", "sae_destroy", "sae_set_params", "sae_params_gather", "
            "sae_batch_blocks", "sae_admit_batch", "sae_admit_batch_host", "sae_lookup", "sae_evict", "sae_update",
            "sae_stats", "sae_get_traj", "sae_sync", "sae_last_error", "sae_gen_tokens",
            "sae_launch_count", "sae_profile", "sae_profile_read", "sae_params_point_mean",
-           "sae_counters_device", "sae_priority"]
+           "sae_counters_device", "sae_priority", "sae_profile_read_hash"]
 
 # sae_counters (include/sae.h): field order of the whole-ctx counter totals
 COUNTER_FIELDS = (["requests", "blocks_looked_up", "hit_blocks", "hit_tokens", "prompt_tokens",
@@ -134,6 +134,7 @@ def lib():
             "sae_profile": (i32, [vp, i32]),
             "sae_params_point_mean": (i32, [vp, u32, u32, vp, vp]),
             "sae_profile_read": (i32, [vp, P(C.c_double), P(u64)]),
+            "sae_profile_read_hash": (i32, [vp, P(C.c_double), P(u64)]),
             "sae_counters_device": (i32, [vp, vp, vp]),
             "sae_priority": (i32, [P(sae_params), C.c_double, C.c_double, u64] + [vp] * 7),
         }
@@ -387,6 +388,13 @@ class SaeCache:
 
     def profile(self, enable: bool = True):
         self._check(lib().sae_profile(self.h, 1 if enable else 0))
+
+    def profile_read_hash(self):
+        """(summed K1 hashing-kernel ms, number of its launches) since the last read."""
+        ms = C.c_double()
+        n = C.c_uint64()
+        self._check(lib().sae_profile_read_hash(self.h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
 
     def profile_read(self):
         """(summed replay-kernel ms, number of replay launches) since the last read."""
