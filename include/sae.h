@@ -316,6 +316,33 @@ sae_status sae_priority(const sae_params* params, double dt_eps, double z_cut, u
                         const uint8_t* q, const uint8_t* tau, const double* dt_in, const uint32_t* ob,
                         const uint32_t* omax, double* out, sae_stream s);
 
+/* Characterisation pass (A42): an unbounded cache (C = infinity,
+ * nothing evicted) over one trace in arrival order.  A block is reused if its chained hash
+ * occurred in an earlier request, intra-session if an earlier occurrence was in the
+ * same session, else inter-session.  Counters by token type tau (0..5):
+ *   blocks / reused                      every block            (Table 1 "combined")
+ *   later_blocks / later_intra           blocks of turn > 0     (Table 1 "intra-conv.")
+ *   first_blocks / first_inter           blocks of turn 0       (Table 1 "inter-conv.")
+ * pos_blocks / pos_reused by bin min(9, 10 j / np) over the prompt blocks of single-turn
+ * sessions (positional reuse), and reuses_intra / reuses_inter (session locality). */
+typedef struct {
+  uint64_t blocks[6], reused[6];
+  uint64_t later_blocks[6], later_intra[6];
+  uint64_t first_blocks[6], first_inter[6];
+  uint64_t pos_blocks[10], pos_reused[10];
+  uint64_t reuses_intra, reuses_inter;
+} sae_char_stats;
+
+/* Run the characterisation pass on the device (K1 hashing + two insert-or-find tables) and
+ * copy the counters to host_out (HOST).  batch: DEVICE arrays as for sae_admit_batch (the
+ * replica array is not read); session, turn (u32 [n]) and single_turn (u8 [n], 1 = the
+ * request's session has one turn) are DEVICE arrays.  The (hash, session) key is a 64-bit
+ * mix of both (a collision is possible with probability ~ blocks^2 / 2^64).  Synchronous;
+ * the ctx supplies block_tokens, hash_seed and scratch only -- its cache state is untouched. */
+sae_status sae_characterize(sae_ctx* ctx, const sae_batch* batch, const uint32_t* session,
+                            const uint32_t* turn, const uint8_t* single_turn,
+                            sae_char_stats* host_out, sae_stream s);
+
 /* Synthetic-trace token materialisation (input generator, not the method):
  * tokens[dst[p] + i] = SM(SM(seed ^ SM(stream[p])) ^ (start[p] + i)) mod 2^17 and
  * types[dst[p] + i] = type[p] for every piece p, i < len[p]. Device pointers. */

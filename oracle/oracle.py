@@ -68,6 +68,13 @@ class OrcStats(C.Structure):
                 ("iv_len", C.c_uint64 * 2)]
 
 
+class OrcCharStats(C.Structure):
+    _fields_ = [(k, C.c_uint64 * 6) for k in ("blocks", "reused", "later_blocks", "later_intra",
+                                               "first_blocks", "first_inter")] + \
+               [("pos_blocks", C.c_uint64 * 10), ("pos_reused", C.c_uint64 * 10),
+                ("reuses_intra", C.c_uint64), ("reuses_inter", C.c_uint64)]
+
+
 _lib = None
 
 
@@ -106,6 +113,7 @@ def lib():
             "orc_set_counters": (None, [vp, vp, vp, vp, vp, vp]),
             "orc_push_interval": (None, [vp, i32, d]),
             "orc_replay": (i32, [vp, u64] + [vp] * 9 + [vp, vp, u64, vp, vp, vp, vp]),
+            "orc_characterize": (i32, [P(OrcConfig), u64] + [vp] * 10),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -322,6 +330,25 @@ class Replica:
         nv = int(voff[n])
         return ReplayResult(out4, vout[:nv].copy(), voff, None if hashes is None else hashes[:tot],
                             None if taus is None else taus[:tot], boff, self.traj(), self.stats())
+
+
+def characterize(tr: dict, cfg: dict, single_turn=None) -> dict:
+    """Characterisation pass (unbounded cache) of a single-replica trace: counters by token type,
+    position bin and session locality (sae_oracle.cpp orc_characterize)."""
+    c = make_config(cfg)
+    st = single_turn if single_turn is not None else (~tr["continues"]).astype(np.uint8)
+    arr = {k: np.ascontiguousarray(tr[k]) for k in ("prompt_off", "prompt_len", "decode_off", "decode_len")}
+    sess = np.ascontiguousarray(tr["session"], np.uint32)
+    turn = np.ascontiguousarray(tr["turn"], np.uint32)
+    st = np.ascontiguousarray(st, np.uint8)
+    o = OrcCharStats()
+    rc = lib().orc_characterize(C.byref(c), tr["n"], _p(arr["prompt_off"]), _p(arr["prompt_len"]),
+                                _p(arr["decode_off"]), _p(arr["decode_len"]), _p(tr["tokens"]),
+                                _p(tr["types"]), _p(sess), _p(turn), _p(st), C.byref(o))
+    if rc != 0:
+        raise RuntimeError("oracle characterize rc=%d" % rc)
+    return {k: (list(getattr(o, k)) if not isinstance(getattr(o, k), int) else getattr(o, k))
+            for k, _ in OrcCharStats._fields_}
 
 
 def point_mean_w(params: list, n_points: int) -> list:

@@ -21,6 +21,8 @@
 #include <vector>
 #include <deque>
 #include <unordered_map>
+#include <unordered_set>
+#include <set>
 #include <algorithm>
 #include <tuple>
 #include <thread>
@@ -1089,6 +1091,68 @@ void orc_push_interval(void* h, int s, double ln_dt) {
   Replica& R = *(Replica*)h;
   R.iv[s].push_back(ln_dt);
   while (R.iv[s].size() > R.cfg.interval_ring) R.iv[s].pop_front();
+}
+
+// Characterisation pass (reading A42): an unbounded cache (C = infinity,
+// nothing evicted) over a trace in arrival order.  A block is REUSED if its chained hash
+// occurred in an earlier request (P:158 strict prefix); the reuse is INTRA-session if an
+// earlier occurrence was in the same session, else INTER-session (Fig. 2a/d).
+// Table 1 columns by token type: intra-conv. = reused-intra share of the blocks of
+// later turns (turn > 0, which can reuse their own history); inter-conv. = reused share of
+// the blocks of first turns (turn 0: only other sessions precede them); combined = reused
+// share of all blocks.  Positional reuse (Fig. 2c): prompt blocks of single-turn
+// sessions by bin min(9, 10 j / np).
+typedef struct {
+  uint64_t blocks[6], reused[6];
+  uint64_t later_blocks[6], later_intra[6];
+  uint64_t first_blocks[6], first_inter[6];
+  uint64_t pos_blocks[10], pos_reused[10];
+  uint64_t reuses_intra, reuses_inter;
+} orc_char_stats;
+
+int orc_characterize(const orc_config* cfg, uint64_t n, const uint64_t* poff, const uint32_t* plen,
+                     const uint64_t* doff, const uint32_t* dlen, const uint32_t* tokens,
+                     const uint8_t* types, const uint32_t* session, const uint32_t* turn,
+                     const uint8_t* single_turn, orc_char_stats* out) {
+  std::memset(out, 0, sizeof *out);
+  std::unordered_set<uint64_t> seen;
+  std::set<std::pair<uint64_t, uint32_t>> seen_sess;
+  const uint32_t B = cfg->block_tokens;
+  for (uint64_t i = 0; i < n; ++i) {
+    if (plen[i] < 1) return ORC_E_INVAL;
+    std::vector<uint64_t> H;
+    std::vector<uint8_t> tau, ntok;
+    hash_request(*cfg, tokens + poff[i], types + poff[i], plen[i], tokens + doff[i], dlen[i], H, tau, ntok);
+    const uint32_t np = (plen[i] + B - 1) / B;
+    for (uint32_t j = 0; j < H.size(); ++j) {
+      const int t = tau[j];
+      const bool reused = seen.count(H[j]) > 0;
+      const bool intra = seen_sess.count({H[j], session[i]}) > 0;
+      out->blocks[t]++;
+      if (reused) out->reused[t]++;
+      if (turn[i] > 0) {
+        out->later_blocks[t]++;
+        if (intra) out->later_intra[t]++;
+      } else {
+        out->first_blocks[t]++;
+        if (reused) out->first_inter[t]++;
+      }
+      if (reused) {
+        if (intra) out->reuses_intra++;
+        else out->reuses_inter++;
+      }
+      if (single_turn[i] && j < np) {
+        const uint32_t bin = std::min<uint32_t>(9, (10 * j) / np);
+        out->pos_blocks[bin]++;
+        if (reused) out->pos_reused[bin]++;
+      }
+    }
+    for (uint64_t h : H) {
+      seen.insert(h);
+      seen_sess.insert({h, session[i]});
+    }
+  }
+  return ORC_OK;
 }
 
 // Whole-trace replay of one replica's requests (array order), for parity and

@@ -548,6 +548,87 @@ __device__ __forceinline__ uint64_t sm64(uint64_t x) {
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   return z ^ (z >> 31);
 }
+
+// ---------------------------------------------------------------------------
+// Characterisation pass (A42): unbounded cache over a trace.
+// Two insert-or-find tables keyed by the block hash and by (hash, session) hold the first
+// global block index of each key (atomicMin); a block at index g is reused iff its hash's
+// first index < g, intra-session iff its (hash, session)'s first index < g.
+// ---------------------------------------------------------------------------
+struct CharDev {
+  uint64_t* k1; unsigned long long* v1;   // hash -> first global block index
+  uint64_t* k2; unsigned long long* v2;   // (hash, session) -> first global block index
+  uint32_t mask;
+  const uint32_t* session; const uint32_t* turn; const uint8_t* single;
+  unsigned long long* out;                // sae_char_stats as u64[58]
+};
+__device__ __forceinline__ uint64_t char_key2(uint64_t h, uint32_t sess) {
+  return sm64(h ^ sm64((uint64_t)sess + 0x632BE59BD9B4E019ull));
+}
+__device__ __forceinline__ uint32_t ctab_slot(uint64_t* keys, uint32_t mask, uint64_t k) {
+  uint32_t i = home(k, mask);
+  while (true) {
+    const uint64_t cur = keys[i];
+    if (cur == k) return i;
+    if (cur == KEY_EMPTY) {
+      const unsigned long long prev = atomicCAS((unsigned long long*)&keys[i], KEY_EMPTY, k);
+      if (prev == KEY_EMPTY || prev == k) return i;
+    }
+    i = (i + 1) & mask;
+  }
+}
+__device__ __forceinline__ uint32_t ctab_find(const uint64_t* keys, uint32_t mask, uint64_t k) {
+  uint32_t i = home(k, mask);
+  while (keys[i] != k) i = (i + 1) & mask;   // every looked-up key was inserted
+  return i;
+}
+__global__ void k_char_insert(BatchDev b, CharDev c) {
+  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= b.n || !batch_size_ok(b)) return;
+  const uint64_t b0 = b.boff[w], b1 = b.boff[w + 1];
+  for (uint64_t g = b0 + lane; g < b1; g += 32) {
+    const uint64_t H = b.h[g];
+    atomicMin(&c.v1[ctab_slot(c.k1, c.mask, H)], (unsigned long long)g);
+    atomicMin(&c.v2[ctab_slot(c.k2, c.mask, char_key2(H, c.session[w]))], (unsigned long long)g);
+  }
+}
+// counter layout (sae_char_stats): blocks[6] reused[6] later_blocks[6] later_intra[6]
+// first_blocks[6] first_inter[6] pos_blocks[10] pos_reused[10] reuses_intra reuses_inter
+__global__ void k_char_count(BatchDev b, CharDev c, uint32_t B) {
+  __shared__ unsigned int acc[58];
+  for (int i = threadIdx.x; i < 58; i += blockDim.x) acc[i] = 0;
+  __syncthreads();
+  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w < b.n && batch_size_ok(b)) {
+    const uint64_t b0 = b.boff[w], b1 = b.boff[w + 1];
+    const uint32_t np = (b.plen[w] + B - 1) / B, sess = c.session[w];
+    const bool later = c.turn[w] > 0, single = c.single[w] != 0;
+    for (uint64_t g = b0 + lane; g < b1; g += 32) {
+      const uint64_t H = b.h[g];
+      const uint32_t t = b.tau[g], j = (uint32_t)(g - b0);
+      const bool reused = c.v1[ctab_find(c.k1, c.mask, H)] < g;
+      const bool intra = c.v2[ctab_find(c.k2, c.mask, char_key2(H, sess))] < g;
+      atomicAdd(&acc[t], 1u);
+      if (reused) atomicAdd(&acc[6 + t], 1u);
+      if (later) {
+        atomicAdd(&acc[12 + t], 1u);
+        if (intra) atomicAdd(&acc[18 + t], 1u);
+      } else {
+        atomicAdd(&acc[24 + t], 1u);
+        if (reused) atomicAdd(&acc[30 + t], 1u);
+      }
+      if (reused) atomicAdd(&acc[intra ? 56 : 57], 1u);
+      if (single && j < np) {
+        const uint32_t bin = min(9u, (10u * j) / np);
+        atomicAdd(&acc[36 + bin], 1u);
+        if (reused) atomicAdd(&acc[46 + bin], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 58; i += blockDim.x)
+    if (acc[i]) atomicAdd(&c.out[i], (unsigned long long)acc[i]);
+}
 // K7: synthetic token materialisation, one CTA per piece (input generator)
 __global__ void k_gen_tokens(uint64_t seed, uint64_t np, const uint64_t* stream, const uint64_t* start,
                              const uint32_t* len, const uint64_t* dst, const uint8_t* type,
@@ -857,7 +938,7 @@ static BatchDev batch_dev(const sae_batch* b) {
 
 // carve the per-batch workspace
 static sae_status prepare(sae_ctx* ctx, const sae_batch* b, BatchDev& x, cudaStream_t s,
-                          uint64_t total_blocks) {
+                          uint64_t total_blocks, bool runs = true) {
   const uint64_t n = b->n, R = ctx->d.R;
   const uint32_t ntile = (uint32_t)((n + SCAN_TILE - 1) / SCAN_TILE);
   auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
@@ -891,7 +972,7 @@ static sae_status prepare(sae_ctx* ctx, const sae_batch* b, BatchDev& x, cudaStr
   k_scan_apply<<<ntile, 1024, 0, s>>>(cnt, n, part, x.boff, ntile);
   CK(cudaMemsetAsync(x.run_start, 0xFF, R * 4, s));
   CK(cudaMemsetAsync(x.run_end, 0, R * 4, s));
-  k_runs<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, ctx->d);
+  if (runs) k_runs<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, ctx->d);
   cudaEvent_t h0 = nullptr, h1 = nullptr;
   if (ctx->prof) {
     CK(cudaEventCreate(&h0));
@@ -1231,6 +1312,51 @@ sae_status sae_priority(const sae_params* params, double dt_eps, double z_cut, u
                                                                         dt_in, ob, omax, out);
   CK(cudaGetLastError());
   return SAE_OK;
+}
+
+sae_status sae_characterize(sae_ctx* ctx, const sae_batch* b, const uint32_t* session, const uint32_t* turn,
+                            const uint8_t* single_turn, sae_char_stats* host_out, sae_stream st) {
+  if (!ctx || !b || !host_out) return SAE_E_INVAL;
+  if (b->n && (!b->arrival || !b->prompt_off || !b->prompt_len || !b->decode_off || !b->decode_len ||
+               !b->tokens || !b->types || !session || !turn || !single_turn))
+    return SAE_E_INVAL;
+  std::memset(host_out, 0, sizeof *host_out);
+  if (b->n == 0) return SAE_OK;
+  cudaStream_t s = (cudaStream_t)st;
+  CK(cudaSetDevice(ctx->device));
+  BatchDev x = batch_dev(b);
+  sae_status rc = prepare(ctx, b, x, s, b->total_blocks, false);   // K1 hashes + tau
+  if (rc) return rc;
+  uint64_t slots = 1;
+  while (slots < 2ull * (b->total_blocks ? b->total_blocks : 1)) slots <<= 1;
+  if (slots > (1ull << 31)) return SAE_E_INVAL;
+  CharDev c;
+  CK(cudaMallocAsync(&c.k1, slots * 8, s));
+  CK(cudaMallocAsync(&c.v1, slots * 8, s));
+  CK(cudaMallocAsync(&c.k2, slots * 8, s));
+  CK(cudaMallocAsync(&c.v2, slots * 8, s));
+  CK(cudaMallocAsync(&c.out, 58 * 8, s));
+  CK(cudaMemsetAsync(c.k1, 0xFF, slots * 8, s));
+  CK(cudaMemsetAsync(c.v1, 0xFF, slots * 8, s));
+  CK(cudaMemsetAsync(c.k2, 0xFF, slots * 8, s));
+  CK(cudaMemsetAsync(c.v2, 0xFF, slots * 8, s));
+  CK(cudaMemsetAsync(c.out, 0, 58 * 8, s));
+  c.mask = (uint32_t)(slots - 1);
+  c.session = session; c.turn = turn; c.single = single_turn;
+  const unsigned grid = (unsigned)((b->n * 32ull + 255) / 256);
+  k_char_insert<<<grid, 256, 0, s>>>(x, c);
+  k_char_count<<<grid, 256, 0, s>>>(x, c, ctx->d.B);
+  ctx->launches += 2;
+  CK(cudaGetLastError());
+  static_assert(sizeof(sae_char_stats) == 58 * 8, "sae_char_stats layout");
+  CK(cudaMemcpyAsync(host_out, c.out, 58 * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaFreeAsync(c.k1, s));
+  CK(cudaFreeAsync(c.v1, s));
+  CK(cudaFreeAsync(c.k2, s));
+  CK(cudaFreeAsync(c.v2, s));
+  CK(cudaFreeAsync(c.out, s));
+  CK(cudaStreamSynchronize(s));
+  return take_sticky(ctx, s);
 }
 
 uint64_t sae_launch_count(const sae_ctx* ctx) { return ctx ? ctx->launches : 0; }

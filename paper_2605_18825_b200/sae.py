@@ -83,6 +83,13 @@ class sae_replica_stats(C.Structure):
                 ("params", sae_params), ("stage2_chunks", C.c_uint64)]
 
 
+class sae_char_stats(C.Structure):
+    _fields_ = [(k, C.c_uint64 * 6) for k in ("blocks", "reused", "later_blocks", "later_intra",
+                                               "first_blocks", "first_inter")] + \
+               [("pos_blocks", C.c_uint64 * 10), ("pos_reused", C.c_uint64 * 10),
+                ("reuses_intra", C.c_uint64), ("reuses_inter", C.c_uint64)]
+
+
 class sae_traj(C.Structure):
     _fields_ = [("E", C.c_uint64), ("request", C.c_uint64), ("w", C.c_double * 5),
                 ("alpha", C.c_double * 3), ("mu", C.c_double * 2), ("sigma", C.c_double * 2),
@@ -93,7 +100,7 @@ EXPORTS = ["sae_create", "sae_destroy", "sae_set_params", "sae_params_gather", "
            "sae_batch_blocks", "sae_admit_batch", "sae_admit_batch_host", "sae_lookup", "sae_evict", "sae_update",
            "sae_stats", "sae_get_traj", "sae_sync", "sae_last_error", "sae_gen_tokens",
            "sae_launch_count", "sae_profile", "sae_profile_read", "sae_params_point_mean",
-           "sae_counters_device", "sae_priority", "sae_profile_read_hash"]
+           "sae_counters_device", "sae_priority", "sae_profile_read_hash", "sae_characterize"]
 
 # sae_counters (include/sae.h): field order of the whole-ctx counter totals
 COUNTER_FIELDS = (["requests", "blocks_looked_up", "hit_blocks", "hit_tokens", "prompt_tokens",
@@ -135,6 +142,7 @@ def lib():
             "sae_params_point_mean": (i32, [vp, u32, u32, vp, vp]),
             "sae_profile_read": (i32, [vp, P(C.c_double), P(u64)]),
             "sae_profile_read_hash": (i32, [vp, P(C.c_double), P(u64)]),
+            "sae_characterize": (i32, [vp, P(sae_batch), vp, vp, vp, P(sae_char_stats), vp]),
             "sae_counters_device": (i32, [vp, vp, vp]),
             "sae_priority": (i32, [P(sae_params), C.c_double, C.c_double, u64] + [vp] * 7),
         }
@@ -379,6 +387,23 @@ class SaeCache:
             out = torch.empty(len(COUNTER_FIELDS), dtype=torch.int64, device="cuda")
         self._check(lib().sae_counters_device(self.h, out.data_ptr(), _stream(stream)))
         return out
+
+    def characterize(self, b: dict, session, turn, single_turn, stream=None) -> dict:
+        """Characterisation pass (sae_characterize) of the batch b (device tensors, one trace
+        in arrival order) with per-request session / turn (int32) and single_turn (uint8)
+        device tensors; returns the counters as a dict of lists / ints."""
+        o = sae_char_stats()
+        sb = sae_batch()
+        sb.n = b["n"]
+        sb.total_blocks = b["total_blocks"]
+        for k, f in (("arrival", "arrival"), ("prompt_off", "prompt_off"), ("prompt_len", "prompt_len"),
+                     ("decode_off", "decode_off"), ("decode_len", "decode_len"), ("tokens", "tokens"),
+                     ("types", "types"), ("flags", "flags"), ("spb", "shared_prefix_blocks")):
+            setattr(sb, f, b[k].data_ptr())
+        self._check(lib().sae_characterize(self.h, C.byref(sb), session.data_ptr(), turn.data_ptr(),
+                                           single_turn.data_ptr(), C.byref(o), _stream(stream)))
+        return {k: (list(getattr(o, k)) if not isinstance(getattr(o, k), int) else getattr(o, k))
+                for k, _ in sae_char_stats._fields_}
 
     def sync(self, stream=None):
         self._check(lib().sae_sync(self.h, _stream(stream)))

@@ -15,6 +15,7 @@
 #   sass        cuobjdump -sass of libsae.so (k_replay) -> gpurun_out/sass_k_replay.txt
 #   ablation    scripts/ablation.py on the balanced, multi-turn- and single-turn-dominant mixes
 #   sweep       C5 bench lines over the select's SAE_SLACK / SAE_TRIM knobs
+#   characterize  scripts/characterize.py (unbounded-cache reuse structure of the three mixes)
 # Summaries worth keeping are copied into profiles/ by hand (scripts/profile_summary.py).
 set -u
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
@@ -68,6 +69,8 @@ for step in "$@"; do
         SAE_SLACK=$sl SAE_TRIM=$tr timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/sweep_${sl}_${tr}.json 2>/dev/null
         python -c "import json,sys; d=json.loads(open('$O/sweep_${sl}_${tr}.json').read().strip().splitlines()[-1]); print('slack $sl trim $tr', round(d['value']), d['score_select_phase']['passes_per_request'], round(d['score_select_phase']['cands_per_pass']))"
       done; done ;;
+    characterize)
+      timeout 900 python scripts/characterize.py $O/characterize 200000 > $O/characterize.log 2>&1; tail -40 $O/characterize.log ;;
     *) echo "unknown step $step" ;;
   esac
 done
