@@ -2023,8 +2023,16 @@ __device__ Ctx make_ctx(const Dev& d, uint32_t r, uint32_t rank) {
   Ctx c;
   c.d = &d;
   c.s = reinterpret_cast<Smem*>(g_smem);
-  c.cand = reinterpret_cast<Cand*>(g_smem + ((sizeof(Smem) + 15) / 16) * 16);
-  c.vbuf = c.cand + CAND_MAX;
+  if (CAND_GLOBAL) {
+    // candidate buffer in the replica's own region of global memory (L1-resident: only this
+    // CTA touches it), shared memory keeps the state and the victim staging: a smaller CTA
+    // footprint, so more replicas are resident per SM
+    c.cand = d.cpriv + (uint64_t)r * CAND_MAX;
+    c.vbuf = reinterpret_cast<Cand*>(g_smem + ((sizeof(Smem) + 15) / 16) * 16);
+  } else {
+    c.cand = reinterpret_cast<Cand*>(g_smem + ((sizeof(Smem) + 15) / 16) * 16);
+    c.vbuf = c.cand + CAND_MAX;
+  }
   c.ctl = d.ctl + r;
   c.r = r;
   c.rank = rank;
@@ -2038,7 +2046,7 @@ __device__ Ctx make_ctx(const Dev& d, uint32_t r, uint32_t rank) {
 // Persistent replay: the group of GP CTAs (blockIdx / GP) owns replica r; its leader
 // (rank 0) replays the replica's run of the batch in order, the others execute the
 // leader's group commands (scan / histogram / compact / refresh / rebuild).
-__global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_replay(Dev d, BatchDev b) {
+__global__ void __launch_bounds__(NT, MINB) k_replay(Dev d, BatchDev b) {
   const uint32_t r = blockIdx.x / d.GP, rank = blockIdx.x % d.GP;
   if (r >= d.R) return;
   Ctx c = make_ctx(d, r, rank);
@@ -2063,7 +2071,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_replay(Dev d, BatchDe
 }
 
 // sae_evict: Alg.1 Evict x k with an empty pin set.
-__global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_evict(Dev d, uint32_t r, uint32_t k, double now,
+__global__ void __launch_bounds__(NT, MINB) k_evict(Dev d, uint32_t r, uint32_t k, double now,
                                                  uint32_t* vids, uint32_t* n_out) {
   Ctx c = make_ctx(d, r, blockIdx.x);
   if (blockIdx.x != 0) {
@@ -2095,7 +2103,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_evict(Dev d, uint32_t
   if (c.GP > 1) issue(c, CMD_EXIT);
 }
 
-__global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_update(Dev d, uint32_t r0, uint32_t r1) {
+__global__ void __launch_bounds__(NT, MINB) k_update(Dev d, uint32_t r0, uint32_t r1) {
   const uint32_t r = r0 + blockIdx.x / d.GP, rank = blockIdx.x % d.GP;
   if (r >= r1) return;
   Ctx c = make_ctx(d, r, rank);
@@ -2113,5 +2121,5 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) k_update(Dev d, uint32_
 
 // dynamic shared memory of one replay CTA of this variant
 inline size_t smem_bytes() {
-  return ((sizeof(Smem) + 15) / 16) * 16 + sizeof(Cand) * (CAND_MAX + VCAP);
+  return ((sizeof(Smem) + 15) / 16) * 16 + sizeof(Cand) * ((CAND_GLOBAL ? 0 : CAND_MAX) + VCAP);
 }

@@ -129,6 +129,7 @@ struct Dev {
                         // next to the random-access state), 2 evict_first (they do not)
   Cand* gcand;          // [R*C] global candidate buffer (large pools)
   Cand* gsel;           // [R*CAND_MAX] compacted candidates after narrowing
+  Cand* cpriv;          // [R*CAND_MAX] private candidate buffers of the v256g variant
   GroupCtl* ctl;        // [R]
   uint64_t hash_seed;
   double dt_eps, z_cut;
@@ -422,18 +423,36 @@ __global__ void __launch_bounds__(128) k_hash(BatchDev b, Dev d) {
   }
 }
 
+// The replay kernels in three compiled variants (NT threads, candidate buffer of CAND_MAX
+// records in shared memory or -- CAND_GLOBAL -- in the replica's L1-resident global region,
+// MINB CTAs per SM):
+//   v512  groups / few replicas / large pools: lowest latency per replica
+//   v256  many small replicas, two CTAs per SM
+//   v256g many small replicas, three CTAs per SM (candidates in global memory)
 namespace v512 {
 constexpr int NT = 512;
 constexpr int NW = NT / 32;
 constexpr int CAND_MAX = 4096;
+constexpr bool CAND_GLOBAL = false;
+constexpr int MINB = 1;
 #include "replay_impl.cuh"
 }  // namespace v512
 namespace v256 {
 constexpr int NT = 256;
 constexpr int NW = NT / 32;
 constexpr int CAND_MAX = 2560;
+constexpr bool CAND_GLOBAL = false;
+constexpr int MINB = 2;
 #include "replay_impl.cuh"
 }  // namespace v256
+namespace v256g {
+constexpr int NT = 256;
+constexpr int NW = NT / 32;
+constexpr int CAND_MAX = 2560;
+constexpr bool CAND_GLOBAL = true;
+constexpr int MINB = 3;
+#include "replay_impl.cuh"
+}  // namespace v256g
 
 // read-only probe, one warp per request
 __global__ void k_lookup(Dev d, BatchDev b, uint32_t* out) {
@@ -662,6 +681,9 @@ struct Variant {
   uint32_t cand_max;
 };
 static Variant variant(int nt) {
+  if (nt == 257)   // v256g
+    return {(const void*)v256g::k_replay, (const void*)v256g::k_evict, (const void*)v256g::k_update, 256,
+            v256g::smem_bytes(), (uint32_t)v256g::CAND_MAX};
   if (nt == 256)
     return {(const void*)v256::k_replay, (const void*)v256::k_evict, (const void*)v256::k_update, 256,
             v256::smem_bytes(), (uint32_t)v256::CAND_MAX};
@@ -771,7 +793,7 @@ static sae_status create_impl(const sae_config* cfg, sae_ctx* ctx) {
   // otherwise a co-resident group (cooperative launch) that splits every scan pass
   int nsm = 0, occ = 0;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg->device));
-  for (int vnt : {256, 512}) {
+  for (int vnt : {256, 257, 512}) {
     const Variant v = variant(vnt);
     for (const void* f : {v.replay, v.evict, v.update})
       CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem));
@@ -780,7 +802,15 @@ static sae_status create_impl(const sae_config* cfg, sae_ctx* ctx) {
   // hide each other's per-round latency; few replicas, groups and larger pools the 512-thread
   // one (lower latency per replica)
   const bool small = d.C <= variant(256).cand_max && cfg->ctas_per_replica <= 1 && R > (uint64_t)nsm;
-  ctx->var = variant(small ? 256 : 512);
+  // SAE_VARIANT=256|257|512 forces a variant (measurements); 257 = v256g
+  int vsel = small ? 256 : 512;
+  if (const char* e = getenv("SAE_VARIANT")) {
+    const int v = atoi(e);
+    if (v == 256 || v == 257 || v == 512) vsel = v;
+    if (vsel != 512 && d.C > variant(vsel).cand_max) vsel = 512;
+  }
+  ctx->var = variant(vsel);
+  if (vsel == 257) CK(dalloc(ctx, &d.cpriv, R * (uint64_t)ctx->var.cand_max));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ctx->var.replay, ctx->var.nt, ctx->var.smem));
   const uint64_t coresident = (uint64_t)nsm * (uint64_t)(occ > 0 ? occ : 1);
   uint64_t gp = cfg->ctas_per_replica;

@@ -91,7 +91,7 @@ def test_c5_bench_launch_structure():
 def test_c3_first_50k_requests():
     tr = T.make("c3", n_requests=50_000)
     t0 = time.time()
-    compare_replay(tr, C.policy_config(16384), check_hashes=True, traj=1 << 14)
+    compare_replay(tr, C.policy_config(16384), check_hashes=True, traj=1 << 16)
     print("c3 50K parity in %.0f s" % (time.time() - t0))
 
 
