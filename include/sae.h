@@ -362,6 +362,43 @@ sae_status sae_profile_read(sae_ctx* ctx, double* ms_total, uint64_t* n_launches
  * P:318-320) launched by sae_admit_batch / sae_lookup while profiling is enabled. */
 sae_status sae_profile_read_hash(sae_ctx* ctx, double* ms_total, uint64_t* n_launches);
 
+/* ---------------------------------------------------------------------------------------
+ * Multi-turn session predictor (Eq.(4)).  For a history-free
+ * request the final-layer hidden state h (d wide) of its last prompt token goes through a
+ * three-layer MLP with hidden widths 256 and 64:
+ *     y = W3 relu(W2 relu(W1 h + b1) + b2) + b3,    is_multi_turn = (y > 0)
+ * DESIGN.md readings A43-A45: h, W1, W2 are bf16 (the serving model's activations; tensor-core
+ * operands), b1, b2, W3, b3 fp32; products accumulate in fp32; relu(W1 h + b1) is rounded to
+ * bf16 as GEMM2's operand.  Runs on tcgen05 tensor cores (TMA + TMEM), one persistent CTA per
+ * SM over 256-row tiles.  Errors: SAE_E_INVAL (null pointer, d not a positive multiple of 32,
+ * h not 16-byte aligned), SAE_E_ABI, SAE_E_OOM, SAE_E_CUDA; sae_predictor_last_error() text.
+ * --------------------------------------------------------------------------------------- */
+typedef struct sae_predictor sae_predictor;
+typedef struct {
+  uint32_t abi_version;       /* SAE_ABI_VERSION */
+  uint32_t d;                 /* hidden size of h (multiple of 32); 4096 in DESIGN.md A43 */
+  int32_t device;
+  uint32_t _pad;
+} sae_predictor_config;
+
+/* Create a predictor on cfg->device.  Weights are HOST pointers, copied to the device before
+ * the call returns: w1 bf16 bits [256 x d] row-major (W1[i][j]: output i, input j), b1 f32
+ * [256], w2 bf16 bits [64 x 256], b2 f32 [64], w3 f32 [64], b3.  *out owned by the caller
+ * until sae_predictor_destroy; nothing is leaked on error. */
+sae_status sae_predictor_create(const sae_predictor_config* cfg, const uint16_t* w1, const float* b1,
+                                const uint16_t* w2, const float* b2, const float* w3, float b3,
+                                sae_predictor** out);
+sae_status sae_predictor_destroy(sae_predictor* p);
+/* Predict n requests, stream-ordered and asynchronous.  h: DEVICE bf16 bits [n x d]
+ * row-major (16-byte aligned), read-only.  Outputs (DEVICE, either may be NULL but not both):
+ * logit[o] = y (f32) and flags[o] = (flags[o] & ~1) | (y > 0) -- bit 0 of sae_batch.flags,
+ * is_multi_turn -- with o = rows[i] when rows (DEVICE u32 [n], distinct) is given, else i. */
+sae_status sae_predict(sae_predictor* p, const uint16_t* h, uint32_t n, const uint32_t* rows, float* logit,
+                       uint8_t* flags, sae_stream s);
+uint64_t sae_predictor_launch_count(const sae_predictor* p);
+/* Text of the last error of p; of the last failed sae_predictor_create when p is NULL. */
+const char* sae_predictor_last_error(const sae_predictor* p);
+
 #ifdef __cplusplus
 }
 #endif

@@ -453,6 +453,17 @@ constexpr bool CAND_GLOBAL = true;
 constexpr int MINB = 3;
 #include "replay_impl.cuh"
 }  // namespace v256g
+#ifndef SAE_V128_MINB
+#define SAE_V128_MINB 7
+#endif
+namespace v128g {
+constexpr int NT = 128;
+constexpr int NW = NT / 32;
+constexpr int CAND_MAX = 2560;
+constexpr bool CAND_GLOBAL = true;
+constexpr int MINB = SAE_V128_MINB;
+#include "replay_impl.cuh"
+}  // namespace v128g
 
 // read-only probe, one warp per request
 __global__ void k_lookup(Dev d, BatchDev b, uint32_t* out) {
@@ -681,6 +692,9 @@ struct Variant {
   uint32_t cand_max;
 };
 static Variant variant(int nt) {
+  if (nt == 129)   // v128g
+    return {(const void*)v128g::k_replay, (const void*)v128g::k_evict, (const void*)v128g::k_update, 128,
+            v128g::smem_bytes(), (uint32_t)v128g::CAND_MAX};
   if (nt == 257)   // v256g
     return {(const void*)v256g::k_replay, (const void*)v256g::k_evict, (const void*)v256g::k_update, 256,
             v256g::smem_bytes(), (uint32_t)v256g::CAND_MAX};
@@ -793,7 +807,7 @@ static sae_status create_impl(const sae_config* cfg, sae_ctx* ctx) {
   // otherwise a co-resident group (cooperative launch) that splits every scan pass
   int nsm = 0, occ = 0;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg->device));
-  for (int vnt : {256, 257, 512}) {
+  for (int vnt : {129, 256, 257, 512}) {
     const Variant v = variant(vnt);
     for (const void* f : {v.replay, v.evict, v.update})
       CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem));
@@ -806,11 +820,11 @@ static sae_status create_impl(const sae_config* cfg, sae_ctx* ctx) {
   int vsel = small ? 256 : 512;
   if (const char* e = getenv("SAE_VARIANT")) {
     const int v = atoi(e);
-    if (v == 256 || v == 257 || v == 512) vsel = v;
+    if (v == 129 || v == 256 || v == 257 || v == 512) vsel = v;
     if (vsel != 512 && d.C > variant(vsel).cand_max) vsel = 512;
   }
   ctx->var = variant(vsel);
-  if (vsel == 257) CK(dalloc(ctx, &d.cpriv, R * (uint64_t)ctx->var.cand_max));
+  if (vsel == 257 || vsel == 129) CK(dalloc(ctx, &d.cpriv, R * (uint64_t)ctx->var.cand_max));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ctx->var.replay, ctx->var.nt, ctx->var.smem));
   const uint64_t coresident = (uint64_t)nsm * (uint64_t)(occ > 0 ? occ : 1);
   uint64_t gp = cfg->ctas_per_replica;

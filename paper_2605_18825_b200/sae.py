@@ -90,6 +90,10 @@ class sae_char_stats(C.Structure):
                 ("reuses_intra", C.c_uint64), ("reuses_inter", C.c_uint64)]
 
 
+class sae_predictor_config(C.Structure):
+    _fields_ = [("abi_version", C.c_uint32), ("d", C.c_uint32), ("device", C.c_int32), ("_pad", C.c_uint32)]
+
+
 class sae_traj(C.Structure):
     _fields_ = [("E", C.c_uint64), ("request", C.c_uint64), ("w", C.c_double * 5),
                 ("alpha", C.c_double * 3), ("mu", C.c_double * 2), ("sigma", C.c_double * 2),
@@ -100,7 +104,9 @@ EXPORTS = ["sae_create", "sae_destroy", "sae_set_params", "sae_params_gather", "
            "sae_batch_blocks", "sae_admit_batch", "sae_admit_batch_host", "sae_lookup", "sae_evict", "sae_update",
            "sae_stats", "sae_get_traj", "sae_sync", "sae_last_error", "sae_gen_tokens",
            "sae_launch_count", "sae_profile", "sae_profile_read", "sae_params_point_mean",
-           "sae_counters_device", "sae_priority", "sae_profile_read_hash", "sae_characterize"]
+           "sae_counters_device", "sae_priority", "sae_profile_read_hash", "sae_characterize",
+           "sae_predictor_create", "sae_predictor_destroy", "sae_predict", "sae_predictor_launch_count",
+           "sae_predictor_last_error"]
 
 # sae_counters (include/sae.h): field order of the whole-ctx counter totals
 COUNTER_FIELDS = (["requests", "blocks_looked_up", "hit_blocks", "hit_tokens", "prompt_tokens",
@@ -145,6 +151,11 @@ def lib():
             "sae_characterize": (i32, [vp, P(sae_batch), vp, vp, vp, P(sae_char_stats), vp]),
             "sae_counters_device": (i32, [vp, vp, vp]),
             "sae_priority": (i32, [P(sae_params), C.c_double, C.c_double, u64] + [vp] * 7),
+            "sae_predictor_create": (i32, [P(sae_predictor_config), vp, vp, vp, vp, vp, C.c_float, P(vp)]),
+            "sae_predictor_destroy": (i32, [vp]),
+            "sae_predict": (i32, [vp, vp, u32, vp, vp, vp, vp]),
+            "sae_predictor_launch_count": (u64, [vp]),
+            "sae_predictor_last_error": (C.c_char_p, [vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -468,3 +479,57 @@ def gen_tokens(seed: int, pieces: dict, dst: np.ndarray, n_tokens: int, device="
     if rc != 0:
         raise SaeError(rc, "sae_gen_tokens")
     return tokens, types
+
+
+class SessionPredictor:
+    """Multi-turn session predictor, Eq.(4), on the tensor cores (csrc/predictor.cu).
+
+    Weights as produced by ``predgen.weights`` (host numpy): w1 / w2 bf16 bit patterns
+    (uint16), b1 / b2 / w3 float32, b3 a float.  ``predict`` takes the hidden states as a
+    CUDA tensor of bf16 (or their uint16 bit patterns) shaped [n, d]."""
+
+    def __init__(self, w1, b1, w2, b2, w3, b3, device: int | None = None):
+        L = lib()
+        if not torch.cuda.is_available():
+            raise RuntimeError("SessionPredictor needs a CUDA device (no CPU fallback)")
+        w1 = np.ascontiguousarray(w1, np.uint16)
+        self.d = int(w1.shape[1])
+        cfg = sae_predictor_config()
+        cfg.abi_version, cfg.d = SAE_ABI_VERSION, self.d
+        cfg.device = torch.cuda.current_device() if device is None else device
+        self._keep = [w1, np.ascontiguousarray(b1, np.float32), np.ascontiguousarray(w2, np.uint16),
+                      np.ascontiguousarray(b2, np.float32), np.ascontiguousarray(w3, np.float32)]
+        h = C.c_void_p()
+        rc = L.sae_predictor_create(C.byref(cfg), *[a.ctypes.data_as(C.c_void_p) for a in self._keep],
+                                    C.c_float(float(b3)), C.byref(h))
+        if rc != 0:
+            raise SaeError(rc, L.sae_predictor_last_error(None).decode())
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().sae_predictor_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def predict(self, hidden: torch.Tensor, rows: torch.Tensor | None = None, logit: torch.Tensor | None = None,
+                flags: torch.Tensor | None = None, stream=None):
+        """logit [n] float32 (allocated when neither logit nor flags is given) and/or flags
+        (uint8, bit 0 := prediction), indexed by rows (int32) when given."""
+        assert hidden.is_cuda and hidden.dim() == 2 and hidden.shape[1] == self.d and hidden.is_contiguous()
+        n = int(hidden.shape[0])
+        if logit is None and flags is None:
+            logit = torch.empty(n, dtype=torch.float32, device=hidden.device)
+        rc = lib().sae_predict(self.h, C.c_void_p(hidden.data_ptr()), n, _ptr(rows), _ptr(logit), _ptr(flags),
+                               _stream(stream))
+        if rc != 0:
+            raise SaeError(rc, lib().sae_predictor_last_error(self.h).decode())
+        return logit
+
+    def launches(self) -> int:
+        return int(lib().sae_predictor_launch_count(self.h))
