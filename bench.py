@@ -61,6 +61,7 @@ WORKLOADS = {
     "c5": dict(cfg="c5", per_step=250, ref_step=100,
                desc="C5 parameter-sweep replicas: balanced trace, C=2304, 32 points x seeds, "
                     "replicas per GPU = 1024/N"),
+    "predictor": dict(cfg="predictor", desc="session predictor Eq.(4)"),
 }
 
 
@@ -70,6 +71,152 @@ def peaks():
         d = json.load(open(p))
         return float(d["hbm_gbs"]), "measured"
     return 6650.0, "fallback"
+
+
+def bf16_peak():
+    """Dense bf16 tensor peak (TFLOP/s): the measured burst figure (a kernel timed alone)."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        if d.get("bf16_tflops"):
+            return float(d["bf16_tflops"]), "measured (cuBLAS bf16 8192^3, burst)"
+    return 2250.0, "fallback (nominal dense bf16)"
+
+
+PRED_D, PRED_N = 4096, 1 << 17       # DESIGN.md A43: d = 4096; 2^17 hidden states (1 GiB > L2)
+PAPER_PRED_PER_S = 1137.0            # P:430-431: "1,137 predictions per second" (other hardware)
+
+
+def predictor_phase(dev, n: int = PRED_N, d: int = PRED_D, steps: int = 20, warmup: int = 3) -> dict:
+    """Session predictor (Eq.(4)) timed alone: one sae_predict launch over n
+    synthetic hidden states per step, CUDA events on the launching stream; its inputs (1 GiB)
+    exceed L2, so every launch streams them from HBM.  Roofline: algorithmic HBM bytes (h,
+    weights once, logits) and tensor flops per launch; the binding one is `bound`."""
+    import torch
+    from paper_2605_18825_b200 import predgen as PG
+    from paper_2605_18825_b200 import sae as S
+    W = PG.weights(d)
+    P = S.SessionPredictor(W["w1"], W["b1"], W["w2"], W["b2"], W["w3"], W["b3"])
+    g = torch.Generator(device=dev).manual_seed(0x5AEC2001)
+    h = torch.randn(n, d, device=dev, generator=g).to(torch.bfloat16).view(torch.int16)
+    y = torch.empty(n, dtype=torch.float32, device=dev)
+    for _ in range(warmup):
+        P.predict(h, logit=y)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = P.launches()
+    e0.record()
+    for _ in range(steps):
+        P.predict(h, logit=y)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    launches = P.launches() - l0
+    byts = n * d * 2 + (256 * d + 64 * 256) * 2 + (256 + 64 + 64) * 4 + n * 4
+    flops = 2.0 * n * (d * 256 + 256 * 64 + 64)
+    hbm, hsrc = peaks()
+    tfl, tsrc = bf16_peak()
+    gbs = byts / (ms * 1e-3) / 1e9
+    tfs = flops / (ms * 1e-3) / 1e12
+    f_h, f_t = gbs / hbm, tfs / tfl
+    del h, y, P
+    torch.cuda.empty_cache()
+    return {"kernel": "k_predict (tcgen05.mma kind::f16 + TMA + TMEM)", "n": n, "d": d,
+            "predictions_per_s": n / (ms * 1e-3), "ms_per_launch": ms, "launches": int(launches),
+            "paper_predictions_per_s": PAPER_PRED_PER_S,
+            "roofline": {"bound": "tensor" if f_t >= f_h else "hbm",
+                         "tensor": {"achieved": tfs, "peak": tfl, "unit": "TFLOP/s", "frac": f_t,
+                                    "peak_source": tsrc},
+                         "hbm": {"achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": f_h,
+                                 "peak_source": hsrc},
+                         "flops_per_launch": flops, "bytes_per_launch": byts}}
+
+
+def run_predictor(args, ws, rank, local):
+    """--workload predictor: the session predictor as its own bench line (weak scaling: every
+    rank predicts its own PRED_N hidden states).  value = device-timed predictions/s over all
+    ranks; e2e = the same through pinned host memory (H2D of the hidden states, D2H of the
+    logits inside the timed region)."""
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist_
+        dist_.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = dist_
+    from paper_2605_18825_b200 import predgen as PG
+    from paper_2605_18825_b200 import sae as S
+    dev = torch.device("cuda", local)
+    K, Wu = args.steps, args.warmup
+    clk = Clocks(local)
+    clk.start()
+    clk.mark()
+    ph = predictor_phase(dev, steps=K, warmup=Wu)
+    # e2e: pinned host hidden states -> device -> logits -> host, per step
+    n, d = PRED_N, PRED_D
+    Wt = PG.weights(d)
+    P = S.SessionPredictor(Wt["w1"], Wt["b1"], Wt["w2"], Wt["b2"], Wt["w3"], Wt["b3"])
+    g = torch.Generator(device=dev).manual_seed(0x5AEC2002)
+    hh = torch.randn(n, d, device=dev, generator=g).to(torch.bfloat16).view(torch.int16).cpu().pin_memory()
+    hd = torch.empty_like(hh, device=dev)
+    yd = torch.empty(n, dtype=torch.float32, device=dev)
+    yh = torch.empty(n, dtype=torch.float32).pin_memory()
+    for _ in range(Wu):
+        hd.copy_(hh, non_blocking=True); P.predict(hd, logit=yd); yh.copy_(yd, non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(K):
+        hd.copy_(hh, non_blocking=True)
+        P.predict(hd, logit=yd)
+        yh.copy_(yd, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / K
+    clocks = clk.stop()
+
+    def allmax(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms = allmax(ph["ms_per_launch"])
+    e2e_ms = allmax(e2e_ms)
+    if rank == 0:
+        rf = ph["roofline"]
+        b = rf["bound"]
+        line = {"metric": "predictions/s", "value": ws * n / (ms * 1e-3), "unit": "pred/s", "n_gpus": ws,
+                "steps": K, "warmup": Wu, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "bf16 (fp32 accumulate)", "data": "synthetic",
+                "config": {"workload": "session predictor Eq.(4) (P:344-363): MLP d=%d -> 256 -> 64 -> 1 over "
+                                       "%d synthetic last-token hidden states per GPU per step, random-init "
+                                       "weights (DESIGN.md A43-A45)" % (d, n),
+                           "l2": "inputs (1 GiB) exceed L2; no flush needed", "parallelism": "rows%d" % ws},
+                "gpu_launches": int(ph["launches"]), "clocks": clocks,
+                "roofline": dict(rf[b], bound=b, kernel=ph["kernel"], traffic=None,
+                                 other={k: rf[k] for k in ("tensor", "hbm") if k != b}),
+                "paper_predictions_per_s": PAPER_PRED_PER_S,
+                "e2e": {"value": ws * n / (e2e_ms * 1e-3), "unit": "pred/s", "h2d_bytes_per_step": n * d * 2,
+                        "d2h_bytes_per_step": n * 4}}
+        if ws == 1 and not args.no_cpu_baseline:
+            import oracle.predictor as OP
+            t0 = time.perf_counter()
+            done = 0
+            hs = PG.hidden(4096, d, seed=11)
+            while time.perf_counter() - t0 < min(args.cpu_seconds, 10.0):
+                OP.predict(hs, Wt)
+                done += hs.shape[0]
+            dt = time.perf_counter() - t0
+            line["cpu_baseline"] = {"value": done / dt, "unit": "pred/s", "cores": os.cpu_count(),
+                                    "kind": "oracle",
+                                    "sample": "fp64 numpy Eq.(4) over batches of 4096 synthetic hidden states "
+                                              "for ~10 s (%d predictions; BLAS threads = host cores)" % done}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 class Clocks:
@@ -217,6 +364,29 @@ def run_reference(args, wl, ws, rank):
     host core (a process pool), every step each core replays ref_step requests of
     its replica; other workloads: the oracle single-threaded (C4: its rescans threaded)."""
     if rank != 0:
+        return
+    if wl["cfg"] == "predictor":
+        import oracle.predictor as OP
+        from paper_2605_18825_b200 import predgen as PG
+        Wt = PG.weights(PRED_D)
+        hs = PG.hidden(2048, PRED_D, seed=11)
+        ts = []
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            OP.predict(hs, Wt)
+            if i >= args.warmup:
+                ts.append(time.perf_counter() - t0)
+        v = hs.shape[0] * len(ts) / sum(ts)
+        print(json.dumps({"impl": "reference", "metric": "predictions/s", "value": v, "unit": "pred/s",
+                          "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": 1e3 * sum(ts) / len(ts), "higher_is_better": True, "scaling": "weak",
+                          "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                          "config": {"workload": "session predictor Eq.(4), d=%d; each step 2048 of the "
+                                                 "workload's hidden states (bounded sample)" % PRED_D},
+                          "cpu_baseline": {"kind": "oracle", "cores": os.cpu_count(), "value": v,
+                                           "sample": "fp64 numpy Eq.(4), 2048 hidden states per step"},
+                          "e2e": {"value": v, "unit": "pred/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+              flush=True)
         return
     import oracle
     n_need = wl["ref_step"] * (args.warmup + args.steps)
@@ -632,6 +802,9 @@ def run_ours(args, wl, ws, rank, local):
         "e2e": {"value": e2e_all / (e2e_tmax * 1e-3), "unit": "req/s",
                 "h2d_bytes_per_step": int(h2d / K), "d2h_bytes_per_step": int(d2h / K)},
     }
+    if not args.no_predictor:
+        # SURVEY 8(f) rank 4, the tensor-core piece: timed alone after the replay steps
+        line["session_predictor"] = predictor_phase(torch.device("cuda", local))
     if ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(wl, tr0, seconds=args.cpu_seconds)
     print(json.dumps(line), flush=True)
@@ -648,6 +821,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-predictor", action="store_true", help="skip the session_predictor sub-record")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--sync", default="none",
                     help="C5 parameter sync: none | mean_w@E (every E requests per replica: NCCL "
@@ -672,6 +846,8 @@ def main():
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
         run_reference(args, wl, ws, rank)
+    elif wl["cfg"] == "predictor":
+        run_predictor(args, ws, rank, local)
     else:
         run_ours(args, wl, ws, rank, local)
 
