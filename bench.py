@@ -132,6 +132,72 @@ def predictor_phase(dev, n: int = PRED_N, d: int = PRED_D, steps: int = 20, warm
                          "flops_per_launch": flops, "bytes_per_launch": byts}}
 
 
+def score_select_phase(dev, capacity: int = 1 << 24, m: int = 64, passes: int = 10, launches: int = 4,
+                       n_requests: int = 440_000) -> dict:
+    """The fused score/select pass alone (K3, sae_select: Alg.1 Evict's choice of the next m
+    victims) on a C4x-shaped pool: the C4 single-turn-dominated trace replayed into
+    a 2^24-block pool until it is full (untimed; its 12-byte scan records, 201 MB, exceed L2),
+    then `launches` launches of `passes` back-to-back read-only passes, timed with CUDA events
+    on the launching stream.  achieved = 12 B x resident blocks per pass / pass time."""
+    import torch
+    from paper_2605_18825_b200 import sae as S
+    t0 = time.perf_counter()
+    cfg = CFG.get("c4", n_requests=n_requests)
+    tr = T.generate(cfg, seed=0x5AEC0004)
+    tr["config"] = cfg
+    allp, dst = T.piece_table(tr)
+    tok, typ = S.gen_tokens(tr["tseed"], allp, dst, tr["n_tokens"], device=dev)   # K7 on the device
+    t_gen = time.perf_counter() - t0
+    pol = CFG.policy_config(capacity)
+    cache = S.SaeCache(capacity, n_replicas=1, policy=pol)
+    lo, per = 0, 40_000
+    resident = 0
+    while lo < tr["n"] and resident < capacity:
+        hi = min(lo + per, tr["n"])
+        hb = {k: tr[k][lo:hi] for k in ("arrival", "prompt_off", "prompt_len", "decode_off", "decode_len",
+                                         "flags", "spb")}
+        hb.update(n=hi - lo, replica=np.zeros(hi - lo, np.uint32), tokens=np.zeros(1, np.uint32),
+                  types=np.zeros(1, np.uint8))
+        b = S.batch_to_torch(hb, device=dev)
+        b["tokens"], b["types"] = tok, typ
+        cache.admit_batch(b)
+        lo = min(lo + per, tr["n"])
+        resident = int(cache.stats(0).resident)
+    t_fill = time.perf_counter() - t0 - t_gen
+    del tok, typ
+    now = float(tr["arrival"][lo - 1]) + 1.0
+    vids = torch.empty(m, dtype=torch.int32, device=dev)
+    nout = torch.zeros(1, dtype=torch.int32, device=dev)
+    cache.select(0, m, now, passes=3, vids=vids, n_out=nout)      # warm-up: thresholds settle
+    torch.cuda.synchronize()
+    st0 = cache.stats(0)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(launches):
+        cache.select(0, m, now, passes=passes, vids=vids, n_out=nout)
+    e1.record()
+    torch.cuda.synchronize()
+    st1 = cache.stats(0)
+    ms = e0.elapsed_time(e1)
+    npass = launches * passes
+    pass_us = 1e3 * ms / npass
+    byts = 12.0 * resident
+    hbm, src = peaks()
+    gbs = byts / (pass_us * 1e-6) / 1e9
+    info = {"kernel": "k_select (fused score/select pass, one cooperative group over all SMs)",
+            "pool_blocks": capacity, "resident_blocks": resident, "victims_per_pass": m,
+            "launches": launches, "passes_per_launch": passes, "us_per_pass": pass_us,
+            "blocks_scored_per_s": resident / (pass_us * 1e-6),
+            "candidates_per_pass": (st1.select_cands - st0.select_cands) / max(st1.select_passes - st0.select_passes, 1),
+            "fill": {"requests": lo, "trace_gen_s": round(t_gen, 1), "fill_s": round(t_fill, 1)},
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "peak_source": src, "unit": "GB/s",
+                         "frac": gbs / hbm, "bytes_per_pass": byts,
+                         "bytes_model": "12 B scan record (meta u32 + key u64) per resident block"}}
+    cache.close()
+    torch.cuda.empty_cache()
+    return info
+
+
 def run_predictor(args, ws, rank, local):
     """--workload predictor: the session predictor as its own bench line (weak scaling: every
     rank predicts its own PRED_N hidden states).  value = device-timed predictions/s over all
@@ -805,6 +871,9 @@ def run_ours(args, wl, ws, rank, local):
     if not args.no_predictor:
         # SURVEY 8(f) rank 4, the tensor-core piece: timed alone after the replay steps
         line["session_predictor"] = predictor_phase(torch.device("cuda", local))
+    if not args.no_score_select:
+        # the north_star's fused score/select kernel on a pool beyond L2, timed alone
+        line["score_select_pass"] = score_select_phase(torch.device("cuda", local))
     if ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(wl, tr0, seconds=args.cpu_seconds)
     print(json.dumps(line), flush=True)
@@ -822,6 +891,7 @@ def main():
     ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-predictor", action="store_true", help="skip the session_predictor sub-record")
+    ap.add_argument("--no-score-select", action="store_true", help="skip the score_select_pass sub-record")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--sync", default="none",
                     help="C5 parameter sync: none | mean_w@E (every E requests per replica: NCCL "

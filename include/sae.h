@@ -281,6 +281,19 @@ sae_status sae_lookup(sae_ctx* ctx, const sae_batch* batch, uint32_t* hit_blocks
 sae_status sae_evict(sae_ctx* ctx, uint32_t replica, uint32_t k, double now,
                      uint32_t* victim_ids, uint32_t* n_out, sae_stream s);
 
+/* The fused score/select pass alone (K3): Alg.1 Evict's choice of the next m <= 96 victims of
+ * one replica at time `now` (>= the replica's time) -- EF by (num_tokens, id), then the
+ * smallest Eq.(3) priorities by (P, last, id) -- with an empty pin set,
+ * computed `passes` >= 1 times back to back in one launch (a measurement of the pass).
+ * READ-ONLY: nothing is evicted, no counter, parameter or clock changes; only the carried
+ * per-segment candidacy thresholds (a performance hint) are kept.  victim_ids
+ * (device, >= m) receive the ids in eviction order -- exactly those sae_evict(m, now) would
+ * remove if no learner fires in between -- and *n_out (device u32, may be NULL) their count
+ * (min(m, resident)).  SAE_E_INVAL for a bad replica, m > 96 or passes == 0; SAE_E_TIME
+ * (sticky) if now is earlier than the replica's time. */
+sae_status sae_select(sae_ctx* ctx, uint32_t replica, uint32_t m, double now, uint32_t passes,
+                      uint32_t* victim_ids, uint32_t* n_out, sae_stream s);
+
 /* Run the learners now -- TokenWeights, QueueWeights, LognormalParams, DecayPower
  * with the replica's learn_flags -- on one replica or on all
  * (UINT32_MAX); E is unchanged; one trajectory snapshot is appended.  Stream-ordered. */

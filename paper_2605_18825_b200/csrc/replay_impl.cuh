@@ -2103,6 +2103,42 @@ __global__ void __launch_bounds__(NT, MINB) k_evict(Dev d, uint32_t r, uint32_t 
   if (c.GP > 1) issue(c, CMD_EXIT);
 }
 
+// sae_select: the fused score/select pass alone (K3, Alg.1 Evict's choice of m victims,
+// P:504-525), `passes` times back to back, read-only: no block is removed and no counter,
+// parameter or clock of the replica changes.  Only the carried per-segment thresholds are
+// written back -- a performance hint that exactness never depends on (§6).
+__global__ void __launch_bounds__(NT, MINB) k_select(Dev d, uint32_t r, uint32_t m, double now,
+                                                  uint32_t passes, uint32_t* vids, uint32_t* n_out) {
+  Ctx c = make_ctx(d, r, blockIdx.x);
+  if (blockIdx.x != 0) {
+    worker_loop(c);
+    return;
+  }
+  group_open(c);
+  load_state(c);
+  RState& st = c.s->st;
+  bool ok = st.err == 0;
+  if (ok && st.has_now && now < st.now) {
+    if (threadIdx.x == 0) raise_err(d, SAE_E_TIME);
+    ok = false;
+  }
+  const uint32_t mm = min(m, st.live);
+  if (ok && mm > 0) {
+    cta_sync();
+    if (threadIdx.x == 0) st.now = now;
+    cta_sync();
+    for (uint32_t p = 0; p < passes; ++p) select_chunk(c, mm, 0xFFFFFFFFu, false);
+    for (uint32_t v = threadIdx.x; v < mm; v += NT)
+      vids[v] = __ldcg(d.bid + c.base + (c.cand[v].ss & SLOT_MASK));
+    cta_sync();
+    // carry the thresholds only (exactness never depends on them)
+    if (threadIdx.x < 16) d.st[c.r].thr[threadIdx.x] = st.thr[threadIdx.x];
+  }
+  if (threadIdx.x == 0 && n_out) *n_out = ok ? mm : 0u;
+  cta_sync();
+  if (c.GP > 1) issue(c, CMD_EXIT);
+}
+
 __global__ void __launch_bounds__(NT, MINB) k_update(Dev d, uint32_t r0, uint32_t r1) {
   const uint32_t r = r0 + blockIdx.x / d.GP, rank = blockIdx.x % d.GP;
   if (r >= r1) return;

@@ -687,21 +687,26 @@ struct Variant {
   const void* replay;
   const void* evict;
   const void* update;
+  const void* select;
   int nt;
   size_t smem;
   uint32_t cand_max;
 };
 static Variant variant(int nt) {
   if (nt == 129)   // v128g
-    return {(const void*)v128g::k_replay, (const void*)v128g::k_evict, (const void*)v128g::k_update, 128,
+    return {(const void*)v128g::k_replay, (const void*)v128g::k_evict, (const void*)v128g::k_update,
+            (const void*)v128g::k_select, 128,
             v128g::smem_bytes(), (uint32_t)v128g::CAND_MAX};
   if (nt == 257)   // v256g
-    return {(const void*)v256g::k_replay, (const void*)v256g::k_evict, (const void*)v256g::k_update, 256,
+    return {(const void*)v256g::k_replay, (const void*)v256g::k_evict, (const void*)v256g::k_update,
+            (const void*)v256g::k_select, 256,
             v256g::smem_bytes(), (uint32_t)v256g::CAND_MAX};
   if (nt == 256)
-    return {(const void*)v256::k_replay, (const void*)v256::k_evict, (const void*)v256::k_update, 256,
+    return {(const void*)v256::k_replay, (const void*)v256::k_evict, (const void*)v256::k_update,
+            (const void*)v256::k_select, 256,
             v256::smem_bytes(), (uint32_t)v256::CAND_MAX};
-  return {(const void*)v512::k_replay, (const void*)v512::k_evict, (const void*)v512::k_update, 512,
+  return {(const void*)v512::k_replay, (const void*)v512::k_evict, (const void*)v512::k_update,
+            (const void*)v512::k_select, 512,
           v512::smem_bytes(), (uint32_t)v512::CAND_MAX};
 }
 
@@ -809,7 +814,7 @@ static sae_status create_impl(const sae_config* cfg, sae_ctx* ctx) {
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg->device));
   for (int vnt : {129, 256, 257, 512}) {
     const Variant v = variant(vnt);
-    for (const void* f : {v.replay, v.evict, v.update})
+    for (const void* f : {v.replay, v.evict, v.update, v.select})
       CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem));
   }
   // many small single-CTA replicas (more than SMs) take the 256-thread variant: two per SM
@@ -1197,6 +1202,24 @@ sae_status sae_evict(sae_ctx* ctx, uint32_t replica, uint32_t k, double now, uin
     CK(cudaLaunchCooperativeKernel(ctx->var.evict, ctx->d.GP, ctx->var.nt, args, ctx->var.smem, (cudaStream_t)st));
   else
     CK(cudaLaunchKernel(ctx->var.evict, 1, ctx->var.nt, args, ctx->var.smem, (cudaStream_t)st));
+  ctx->launches++;
+  CK(cudaGetLastError());
+  return SAE_OK;
+}
+
+sae_status sae_select(sae_ctx* ctx, uint32_t replica, uint32_t m, double now, uint32_t passes,
+                      uint32_t* vids, uint32_t* n_out, sae_stream st) {
+  if (!ctx || replica >= ctx->d.R || m > MSUB || passes == 0 || (m > 0 && !vids)) {
+    if (ctx) ctx->last_error = "sae_select: bad replica, m > 96, passes == 0 or null victim buffer";
+    return SAE_E_INVAL;
+  }
+  ctx->d.epoch++;
+  void* args[] = {(void*)&ctx->d, (void*)&replica, (void*)&m, (void*)&now, (void*)&passes, (void*)&vids,
+                  (void*)&n_out};
+  if (ctx->d.GP > 1)
+    CK(cudaLaunchCooperativeKernel(ctx->var.select, ctx->d.GP, ctx->var.nt, args, ctx->var.smem, (cudaStream_t)st));
+  else
+    CK(cudaLaunchKernel(ctx->var.select, 1, ctx->var.nt, args, ctx->var.smem, (cudaStream_t)st));
   ctx->launches++;
   CK(cudaGetLastError());
   return SAE_OK;

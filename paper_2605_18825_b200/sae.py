@@ -105,7 +105,7 @@ EXPORTS = ["sae_create", "sae_destroy", "sae_set_params", "sae_params_gather", "
            "sae_stats", "sae_get_traj", "sae_sync", "sae_last_error", "sae_gen_tokens",
            "sae_launch_count", "sae_profile", "sae_profile_read", "sae_params_point_mean",
            "sae_counters_device", "sae_priority", "sae_profile_read_hash", "sae_characterize",
-           "sae_predictor_create", "sae_predictor_destroy", "sae_predict", "sae_predictor_launch_count",
+           "sae_select", "sae_predictor_create", "sae_predictor_destroy", "sae_predict", "sae_predictor_launch_count",
            "sae_predictor_last_error"]
 
 # sae_counters (include/sae.h): field order of the whole-ctx counter totals
@@ -137,6 +137,7 @@ def lib():
                                            P(u64), P(u64), vp]),
             "sae_lookup": (i32, [vp, P(sae_batch), vp, vp]),
             "sae_evict": (i32, [vp, u32, u32, C.c_double, vp, vp, vp]),
+            "sae_select": (i32, [vp, u32, u32, C.c_double, u32, vp, vp, vp]),
             "sae_update": (i32, [vp, u32, vp]),
             "sae_stats": (i32, [vp, u32, P(sae_replica_stats), vp]),
             "sae_get_traj": (i32, [vp, u32, vp, u64, P(u64), vp]),
@@ -360,6 +361,16 @@ class SaeCache:
         self._check(lib().sae_evict(self.h, replica, k, float(now), ids.data_ptr(), n.data_ptr(),
                                     _stream(stream)))
         return ids, n
+
+    def select(self, replica: int, m: int, now: float, passes: int = 1, vids: torch.Tensor | None = None,
+               n_out: torch.Tensor | None = None, stream=None):
+        """Read-only fused score/select (sae_select): the ids of the next m victims."""
+        if vids is None:
+            vids = torch.empty(max(m, 1), dtype=torch.int32, device="cuda")
+        if n_out is None:
+            n_out = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self._check(lib().sae_select(self.h, replica, m, now, passes, _ptr(vids), _ptr(n_out), _stream(stream)))
+        return vids, n_out
 
     def update(self, replica: int | None = None, stream=None):
         r = 0xFFFFFFFF if replica is None else replica

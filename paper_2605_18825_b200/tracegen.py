@@ -338,6 +338,24 @@ def materialize(tr: dict, chunk: int = 1 << 23) -> dict:
     return tr
 
 
+def piece_table(tr: dict):
+    """The trace's token pieces (prompt then decode) and each piece's destination in the
+    arena, in the layout materialize() fills -- the input of the device generator K7
+    (sae_gen_tokens), which writes the same bytes on the GPU."""
+    def dst_of(pk, off, base):
+        po = tr[off]
+        req = np.repeat(np.arange(tr["n"]), np.diff(po))
+        cs = np.cumsum(tr[pk]["len"])
+        first = np.concatenate([[0], cs])[po[:-1]]
+        within = np.concatenate([[0], cs[:-1]]) - first[req]
+        return tr[base][req].astype(np.int64) + within
+    P, D = tr["pieces"], tr["dpieces"]
+    allp = {k: np.concatenate([P[k], D[k]]) for k in ("stream", "start", "len", "type")}
+    dst = np.concatenate([dst_of("pieces", "piece_off", "prompt_off"),
+                          dst_of("dpieces", "dpiece_off", "decode_off")])
+    return allp, dst
+
+
 def make(name: str, materialize_tokens: bool = True, **over) -> dict:
     cfg = C.get(name, **over)
     tr = generate(cfg)

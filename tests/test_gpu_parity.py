@@ -158,19 +158,7 @@ def test_multi_replica_parameter_points():
 def test_gen_tokens_matches_numpy():
     tr = T.generate(C.get("c2", n_requests=500))
     T.materialize(tr)
-    import numpy as np
-    P, D = tr["pieces"], tr["dpieces"]
-    # destination of each piece (same layout as tracegen.materialize)
-    def dst_of(pk, off, base):
-        po = tr[off]
-        req = np.repeat(np.arange(tr["n"]), np.diff(po))
-        cs = np.cumsum(tr[pk]["len"])
-        first = np.concatenate([[0], cs])[po[:-1]]
-        within = np.concatenate([[0], cs[:-1]]) - first[req]
-        return tr[base][req].astype(np.int64) + within
-    allp = {k: np.concatenate([P[k], D[k]]) for k in ("stream", "start", "len", "type")}
-    dst = np.concatenate([dst_of("pieces", "piece_off", "prompt_off"),
-                          dst_of("dpieces", "dpiece_off", "decode_off")])
+    allp, dst = T.piece_table(tr)
     tok, ty = S.gen_tokens(tr["tseed"], allp, dst, tr["n_tokens"])
     assert np.array_equal(u32(tok)[:tr["n_tokens"]], tr["tokens"])
     assert np.array_equal(ty.cpu().numpy()[:tr["n_tokens"]], tr["types"])
