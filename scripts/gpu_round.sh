@@ -12,7 +12,8 @@
 #   ncu_c4      launch list + full capture of a C4 200-request k_replay launch
 #   ncu_c4x     full capture of a C4x 200-request k_replay launch
 #   sanitize    compute-sanitizer memcheck / racecheck / synccheck on small replays
-#   sass        cuobjdump -sass of libsae.so (k_replay) -> gpurun_out/sass_k_replay.txt
+#   sass        cuobjdump -sass of libsae.so -> per-kernel counts of the TMA / mbarrier / tcgen05
+#               mnemonics (gpurun_out/sass_summary.txt)
 #   ablation    scripts/ablation.py on the balanced, multi-turn- and single-turn-dominant mixes
 #   sweep       C5 bench lines over the select's SAE_SLACK / SAE_TRIM knobs
 #   characterize  scripts/characterize.py (unbounded-cache reuse structure of the three mixes)
@@ -21,6 +22,15 @@ set -u
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
 O=gpurun_out
+# gpurun copies gpurun_out/ back only when it stays under 64 MiB: each ncu report is reduced
+# on the box to its raw-metrics CSV, the hot-source-lines text and a gzipped source page.
+shrink_rep() {   # $1 = report path without .ncu-rep
+  ncu -i $1.ncu-rep --page raw --csv > $1_raw.csv 2>/dev/null
+  python scripts/ncu_hot_lines.py $1.ncu-rep 60 > $1_hot.txt 2>&1
+  ncu -i $1.ncu-rep --page source --csv --print-source cuda,sass 2>/dev/null | gzip -9 > $1_source.csv.gz
+  [ -n "${KEEP_REP:-}" ] || rm -f $1.ncu-rep
+  ls -la $1_*
+}
 for step in "$@"; do
   echo "== $step"
   case "$step" in
@@ -42,23 +52,26 @@ for step in "$@"; do
         python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
       timeout 1200 ncu --set full --import-source on --clock-control none -k regex:k_replay -s 3 -c 1 -f -o $O/full_c5 \
         python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-      ls -la $O/full_c5.ncu-rep ;;
+      shrink_rep $O/full_c5 ;;
     ncu_c4)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c4.csv \
         python bench.py --workload c4 --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
       timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_replay -s 5 -c 1 -f -o $O/full_c4 \
-        python scripts/prof_c4.py > $O/prof_c4.log 2>&1 ;;
+        python scripts/prof_c4.py > $O/prof_c4.log 2>&1
+      shrink_rep $O/full_c4 ;;
     ncu_c4x)
       timeout 1500 ncu --set full --import-source on --clock-control none -k regex:k_replay -s 30 -c 1 -f -o $O/full_c4x \
-        python scripts/prof_c4x.py > $O/prof_c4x.log 2>&1 ;;
+        python scripts/prof_c4x.py > $O/prof_c4x.log 2>&1
+      shrink_rep $O/full_c4x ;;
     sanitize)
       for tool in memcheck racecheck synccheck; do
         timeout 900 compute-sanitizer --tool $tool python scripts/sanitize.py > $O/sanitize_$tool.log 2>&1
         tail -3 $O/sanitize_$tool.log
       done ;;
     sass)
-      cuobjdump -sass paper_2605_18825_b200/libsae.so > $O/sass_all.txt 2>&1
-      grep -cE 'UBLKCP|SYNCS' $O/sass_all.txt ;;
+      cuobjdump -sass paper_2605_18825_b200/libsae.so > /tmp/sass_all.txt 2>&1
+      python scripts/sass_summary.py /tmp/sass_all.txt > $O/sass_summary.txt
+      cat $O/sass_summary.txt | head -30 ;;
     ablation)
       for w in c5 c2 c4s; do
         timeout 900 python scripts/ablation.py --workload $w --out $O/ablation_$w > $O/ablation_$w.log 2>&1

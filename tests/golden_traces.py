@@ -25,6 +25,8 @@ def fixtures() -> list[dict]:
     out = []
     for p in sorted(glob.glob(os.path.join(GOLDEN, "*.json"))):
         d = json.load(open(p))
+        if "ops" not in d:            # not a replay micro-trace (e.g. predictor_hand.json)
+            continue
         d["_path"] = p
         out.append(d)
     return out
