@@ -792,6 +792,7 @@ def run_ours(args, wl, ws, rank, local):
             dist.barrier()
             dist.destroy_process_group()
         return
+    lay = cache.layout()
     hbm, src = peaks()
     alg_bytes = 12.0 * scored                            # meta u32 + key u64
     # device-timer view of the fused score/select scan (multi-CTA groups: worker 1's
@@ -837,7 +838,7 @@ def run_ours(args, wl, ws, rank, local):
         "config": {"workload": wl["desc"], "requests_per_step_per_gpu": int(req / K),
                    "replicas_per_gpu": R, "capacity_blocks": int(pol["capacity"]),
                    "l2": "flushed between timed steps (256 MiB device write)",
-                   "parallelism": "replicas%d" % ws},
+                   "parallelism": "replicas%d" % ws, "replay_layout": lay},
         "blocks_scored_per_s": scored_all / (tmax * 1e-3),
         # hit rates of the whole job (all ranks, all steps so far) from the int64 all-reduced
         # counters; the timed-window rates of rank 0 alongside

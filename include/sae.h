@@ -366,6 +366,17 @@ sae_status sae_gen_tokens(uint64_t seed, uint64_t n_pieces, const uint64_t* stre
 /* Counts of device kernels launched by this ctx so far (for bench accounting). */
 uint64_t sae_launch_count(const sae_ctx* ctx);
 
+/* How sae_create laid the replay out on the device (for reports and tests; no device work).
+ * threads: per replay CTA (128 / 256 / 512); ctas_per_replica: group size GP; ctas_per_sm:
+ * co-resident replay CTAs per SM (occupancy); coresident: ctas_per_sm x SMs; chunks: > 1 when
+ * single-CTA replicas outnumber the co-resident CTAs and each replica's run is replayed as
+ * that many consecutive tasks by a persistent grid (wave balancing); cand_global: 1 when the
+ * candidate buffer lives in global memory instead of shared memory.  host_out: HOST. */
+typedef struct {
+  uint32_t threads, ctas_per_replica, ctas_per_sm, chunks, cand_global, coresident;
+} sae_layout_info;
+sae_status sae_layout(const sae_ctx* ctx, sae_layout_info* host_out);
+
 /* Profiling (bench roofline): when enabled, every replay-kernel launch is bracketed
  * by CUDA events on its stream; sae_profile_read synchronizes, returns the summed
  * elapsed milliseconds and the number of launches since the last read, and resets. */

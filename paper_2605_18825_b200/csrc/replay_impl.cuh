@@ -213,6 +213,14 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ unsigned long long cmd_tag(uint32_t epoch, uint32_t seq) {
   return ((unsigned long long)(epoch & 0xFFFFFFu) << 32) | seq;
 }
@@ -2046,7 +2054,59 @@ __device__ Ctx make_ctx(const Dev& d, uint32_t r, uint32_t rank) {
 // Persistent replay: the group of GP CTAs (blockIdx / GP) owns replica r; its leader
 // (rank 0) replays the replica's run of the batch in order, the others execute the
 // leader's group commands (scan / histogram / compact / refresh / rebuild).
+// Task-split replay (d.nchunk > 1; single-CTA replicas only): a persistent grid of at most
+// the co-resident CTAs takes tasks t = chunk * R + r in increasing order from one counter;
+// task (k, r) replays the k-th of nchunk consecutive pieces of replica r's run.  Chunk k > 0
+// first waits (acquire) for rflag[r] = (epoch, k), which the CTA that ran chunk k - 1 stored
+// (release) after its state: the replica's requests stay in order, and its state may move
+// between SMs (the acquire orders every later load of this CTA after the other CTA's
+// stores).  Every waited-for task was taken earlier by a running CTA whose own waits are on
+// still earlier tasks, so the chain ends at a chunk 0 (no deadlock, no co-residency needed).
+// Balances the waves: R x nchunk tasks over G CTAs instead of ceil(R / G) whole replicas.
+__device__ void replay_tasks(const Dev& d, const BatchDev& b) {
+  Smem& s = *reinterpret_cast<Smem*>(g_smem);
+  const uint32_t R = d.R, nch = d.nchunk;
+  const uint64_t ntask = (uint64_t)R * nch;
+  for (;;) {
+    if (threadIdx.x == 0) s.wcmd = atomicAdd(d.taskctr, 1u);
+    cta_sync();
+    const uint32_t t = s.wcmd;
+    cta_sync();                                   // (s.wcmd is rewritten by the next task)
+    if ((uint64_t)t >= ntask) return;
+    const uint32_t k = t / R, r = t % R;
+    Ctx c = make_ctx(d, r, 0);
+    const uint32_t lo = b.run_start[r];
+    if (k > 0 && threadIdx.x == 0) {
+      const uint32_t want = (d.epoch << 8) | k;
+      while (ld_acquire_u32(&d.rflag[r]) != want) __nanosleep(64);
+    }
+    cta_sync();
+    if (lo < RUN_INVALID && batch_size_ok(b)) {
+      const uint32_t n = b.run_end[r] - lo;
+      const uint32_t clo = lo + (uint32_t)((uint64_t)n * k / nch);
+      const uint32_t chi = lo + (uint32_t)((uint64_t)n * (k + 1) / nch);
+      if (clo < chi) {
+        load_state(c);
+        if (c.s->st.err == 0) {
+          for (uint32_t i = clo; i < chi; ++i)
+            if (!admit_one(c, b, i)) break;
+        }
+        store_state(c);
+      }
+    }
+    cta_sync();                                   // every thread's stores precede the release
+    if (threadIdx.x == 0 && k + 1 < nch) {
+      __threadfence();
+      st_release_u32(&d.rflag[r], (d.epoch << 8) | (k + 1));
+    }
+  }
+}
+
 __global__ void __launch_bounds__(NT, MINB) k_replay(Dev d, BatchDev b) {
+  if (d.nchunk > 1) {
+    replay_tasks(d, b);
+    return;
+  }
   const uint32_t r = blockIdx.x / d.GP, rank = blockIdx.x % d.GP;
   if (r >= d.R) return;
   Ctx c = make_ctx(d, r, rank);

@@ -127,6 +127,12 @@ struct Dev {
                                // cut to trim_to x want (env SAE_TRIM="at,to"; default 8,4)
   uint32_t scan_l2;     // L2 policy of the streamed scan columns: 1 evict_last (they fit in L2
                         // next to the random-access state), 2 evict_first (they do not)
+  uint32_t nchunk;      // > 1: task-split replay (single-CTA replicas, more replicas than
+                        // co-resident CTAs): each replica's run is cut into nchunk consecutive
+                        // chunks, a persistent grid takes (chunk, replica) tasks in order from
+                        // *taskctr, and chunk k of replica r waits for rflag[r] = (epoch, k)
+  uint32_t* taskctr;    // [1] next task of the current launch (zeroed before each launch)
+  uint32_t* rflag;      // [R] (epoch << 8) | chunks of the replica's run done this launch
   Cand* gcand;          // [R*C] global candidate buffer (large pools)
   Cand* gsel;           // [R*CAND_MAX] compacted candidates after narrowing
   Cand* cpriv;          // [R*CAND_MAX] private candidate buffers of the v256g variant
@@ -817,12 +823,12 @@ static sae_status create_impl(const sae_config* cfg, sae_ctx* ctx) {
     for (const void* f : {v.replay, v.evict, v.update, v.select})
       CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem));
   }
-  // many small single-CTA replicas (more than SMs) take the 256-thread variant: two per SM
-  // hide each other's per-round latency; few replicas, groups and larger pools the 512-thread
-  // one (lower latency per replica)
+  // many small single-CTA replicas (more than SMs) take the 256-thread variant with the
+  // candidate buffer in global memory: three per SM hide each other's per-round latency; few
+  // replicas, groups and larger pools the 512-thread one (lower latency per replica)
   const bool small = d.C <= variant(256).cand_max && cfg->ctas_per_replica <= 1 && R > (uint64_t)nsm;
   // SAE_VARIANT=256|257|512 forces a variant (measurements); 257 = v256g
-  int vsel = small ? 256 : 512;
+  int vsel = small ? 257 : 512;   // v256g: three CTAs per SM (measured 3.05 M vs 2.94 M req/s on C5)
   if (const char* e = getenv("SAE_VARIANT")) {
     const int v = atoi(e);
     if (v == 129 || v == 256 || v == 257 || v == 512) vsel = v;
@@ -866,6 +872,23 @@ static sae_status create_impl(const sae_config* cfg, sae_ctx* ctx) {
     d.scan_l2 = scan_bytes * 2 <= (uint64_t)l2 ? 1u : 2u;
   }
   ctx->coresident = coresident;
+  // task-split replay when single-CTA replicas outnumber the co-resident CTAs: nchunk pieces
+  // per replica run so that R x nchunk tasks fill the last wave best (min ceil(R c / G) / c)
+  d.nchunk = 1;
+  if (d.GP == 1 && R > coresident) {
+    double best = 1e30;
+    for (uint32_t cc = 1; cc <= 8; ++cc) {
+      const double w = (double)((R * cc + coresident - 1) / coresident) / cc;
+      if (w < best - 1e-9) { best = w; d.nchunk = cc; }
+    }
+  }
+  if (const char* e = getenv("SAE_CHUNKS")) {   // measurements: force (1 = whole replicas)
+    const int v = atoi(e);
+    if (v >= 1 && v <= 255 && d.GP == 1) d.nchunk = (uint32_t)v;
+  }
+  CK(dalloc(ctx, &d.taskctr, 1));
+  CK(dalloc(ctx, &d.rflag, R));
+  CK(cudaMemset(d.rflag, 0, R * 4));
   CK(dalloc(ctx, &d.ctl, R));
   CK(cudaMemset(d.ctl, 0, R * sizeof(GroupCtl)));
   if (!d.cand_smem) {
@@ -1084,7 +1107,12 @@ sae_status sae_admit_batch(sae_ctx* ctx, const sae_batch* b, sae_admit_out* o, s
     CK(cudaEventCreate(&e1));
     CK(cudaEventRecord(e0, s));
   }
-  CK(launch_group(ctx->var, ctx->var.replay, ctx->d.R * ctx->d.GP, ctx->d.GP > 1, s, ctx->d, &x));
+  uint32_t grid = ctx->d.R * ctx->d.GP;
+  if (ctx->d.nchunk > 1) {            // task-split replay: a persistent grid, tasks from a counter
+    CK(cudaMemsetAsync(ctx->d.taskctr, 0, 4, s));
+    grid = (uint32_t)std::min<uint64_t>(ctx->coresident, (uint64_t)ctx->d.R * ctx->d.nchunk);
+  }
+  CK(launch_group(ctx->var, ctx->var.replay, grid, ctx->d.GP > 1, s, ctx->d, &x));
   ctx->launches++;
   if (ctx->prof) {
     CK(cudaEventRecord(e1, s));
@@ -1427,6 +1455,19 @@ sae_status sae_characterize(sae_ctx* ctx, const sae_batch* b, const uint32_t* se
 }
 
 uint64_t sae_launch_count(const sae_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+sae_status sae_layout(const sae_ctx* ctx, sae_layout_info* o) {
+  if (!ctx || !o) return SAE_E_INVAL;
+  int nsm = 1;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
+  o->threads = ctx->var.nt;
+  o->ctas_per_replica = ctx->d.GP;
+  o->coresident = (uint32_t)ctx->coresident;
+  o->ctas_per_sm = (uint32_t)(ctx->coresident / (uint64_t)(nsm > 0 ? nsm : 1));
+  o->chunks = ctx->d.nchunk;
+  o->cand_global = ctx->d.cpriv != nullptr ? 1u : 0u;
+  return SAE_OK;
+}
 
 sae_status sae_params_point_mean(const sae_params* all_dev, uint32_t n_total, uint32_t n_points,
                                  sae_params* out_dev, sae_stream st) {

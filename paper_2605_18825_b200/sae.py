@@ -100,13 +100,18 @@ class sae_traj(C.Structure):
                 ("gamma", C.c_double)]
 
 
+class sae_layout_info(C.Structure):
+    _fields_ = [(k, C.c_uint32) for k in ("threads", "ctas_per_replica", "ctas_per_sm", "chunks",
+                                          "cand_global", "coresident")]
+
+
 EXPORTS = ["sae_create", "sae_destroy", "sae_set_params", "sae_params_gather", "sae_params_scatter",
            "sae_batch_blocks", "sae_admit_batch", "sae_admit_batch_host", "sae_lookup", "sae_evict", "sae_update",
            "sae_stats", "sae_get_traj", "sae_sync", "sae_last_error", "sae_gen_tokens",
            "sae_launch_count", "sae_profile", "sae_profile_read", "sae_params_point_mean",
            "sae_counters_device", "sae_priority", "sae_profile_read_hash", "sae_characterize",
            "sae_select", "sae_predictor_create", "sae_predictor_destroy", "sae_predict", "sae_predictor_launch_count",
-           "sae_predictor_last_error"]
+           "sae_predictor_last_error", "sae_layout"]
 
 # sae_counters (include/sae.h): field order of the whole-ctx counter totals
 COUNTER_FIELDS = (["requests", "blocks_looked_up", "hit_blocks", "hit_tokens", "prompt_tokens",
@@ -157,6 +162,7 @@ def lib():
             "sae_predict": (i32, [vp, vp, u32, vp, vp, vp, vp]),
             "sae_predictor_launch_count": (u64, [vp]),
             "sae_predictor_last_error": (C.c_char_p, [vp]),
+            "sae_layout": (i32, [vp, P(sae_layout_info)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -429,6 +435,13 @@ class SaeCache:
 
     def sync(self, stream=None):
         self._check(lib().sae_sync(self.h, _stream(stream)))
+
+    def layout(self) -> dict:
+        """sae_layout: threads per CTA, CTAs per replica / per SM, co-resident CTAs, replay
+        chunks per replica run (task-split persistent replay when > 1), candidate buffer place."""
+        o = sae_layout_info()
+        self._check(lib().sae_layout(self.h, C.byref(o)))
+        return {k: int(getattr(o, k)) for k, _ in o._fields_}
 
     def launches(self) -> int:
         return int(lib().sae_launch_count(self.h))

@@ -16,6 +16,7 @@
 #               mnemonics (gpurun_out/sass_summary.txt)
 #   ablation    scripts/ablation.py on the balanced, multi-turn- and single-turn-dominant mixes
 #   sweep       C5 bench lines over the select's SAE_SLACK / SAE_TRIM knobs
+#   variants    C5 bench lines of the v256 / v256g replay variants over SAE_TRIM
 #   characterize  scripts/characterize.py (unbounded-cache reuse structure of the three mixes)
 # Summaries worth keeping are copied into profiles/ by hand (scripts/profile_summary.py).
 set -u
@@ -81,6 +82,11 @@ for step in "$@"; do
       for sl in 16 8 4; do for tr in 8,4 4,2 3,2; do
         SAE_SLACK=$sl SAE_TRIM=$tr timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/sweep_${sl}_${tr}.json 2>/dev/null
         python -c "import json,sys; d=json.loads(open('$O/sweep_${sl}_${tr}.json').read().strip().splitlines()[-1]); print('slack $sl trim $tr', round(d['value']), d['score_select_phase']['passes_per_request'], round(d['score_select_phase']['cands_per_pass']))"
+      done; done ;;
+    variants)
+      for v in 256 257; do for tr in 8,4 4,2 3,2; do
+        SAE_VARIANT=$v SAE_TRIM=$tr timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-score-select > $O/var_${v}_${tr}.json 2>/dev/null
+        python -c "import json,sys; d=json.loads(open('$O/var_${v}_${tr}.json').read().strip().splitlines()[-1]); print('variant $v trim $tr', round(d['value']), d['score_select_phase']['passes_per_request'], round(d['score_select_phase']['cands_per_pass']), d['score_select_phase']['phase_ms_per_step'])"
       done; done ;;
     characterize)
       timeout 900 python scripts/characterize.py $O/characterize 200000 > $O/characterize.log 2>&1; tail -40 $O/characterize.log ;;

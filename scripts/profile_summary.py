@@ -1,8 +1,14 @@
 """Summarise an ncu --set full report (per-kernel metrics) and a launch-list CSV into
-profiles/ (markdown + json).  Usage: profile_summary.py <rep> <launches.csv> <out_prefix> <label>"""
-import csv, io, json, subprocess, sys
+profiles/ (markdown + json).  Usage: profile_summary.py <rep | raw.csv> <launches.csv> <out_prefix>
+<label> [hot_lines.txt]   (a *_raw.csv is the `ncu -i rep --page raw --csv` export that
+scripts/gpu_round.sh writes on the box; the optional hot-lines text is appended)"""
+import csv, io, json, os, subprocess, sys
 rep, launches, out, label = sys.argv[1:5]
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+hot = sys.argv[5] if len(sys.argv) > 5 else None
+if rep.endswith(".csv"):
+    raw = open(rep).read()
+else:
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, data = rows[0], rows[1], rows[2:]
 want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -12,7 +18,11 @@ want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
         "launch__grid_size", "launch__block_size", "sm__inst_executed_pipe_fp64.sum",
         "smsp__inst_executed.sum", "launch__shared_mem_per_block_dynamic",
-        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct",
+        "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem"]
+want += [h for h in rows[0] if h.startswith("smsp__average_warps_issue_stalled_") and
+         h.endswith("_per_issue_active.ratio")]
 idx = {k: hdr.index(k) for k in want if k in hdr}
 kern = []
 for r in data:
@@ -53,4 +63,8 @@ with open(out + ".md", "w") as f:
             if m != "Kernel Name":
                 f.write("- %s = %s %s\n" % (m, v, summ["units"].get(m, "")))
         f.write("\n")
+    if hot and os.path.exists(hot):
+        f.write("## hottest source lines (warp-stall samples; scripts/ncu_hot_lines.py)\n\n```\n")
+        f.write("".join(open(hot).readlines()[:41]))
+        f.write("```\n")
 print(open(out + ".md").read())

@@ -1,9 +1,11 @@
 """-m gpu parity on the horizons the bench times, in its launch configurations, plus edge
 cases driven through the C ABI and the score function itself:
 
-* C5 exactly as bench.py runs it on one GPU: 1024 replicas in the 256-thread, two-CTAs-per-
-  SM variant, 25 launches of 250 requests per replica (the default 5 warm-up + 20 timed
-  steps); sampled replicas replayed by the oracle over all 6 250 requests;
+* C5 exactly as bench.py runs it on one GPU: 1024 replicas in the default layout (256-thread
+  CTAs, three per SM, each replica's 250-request run replayed as consecutive tasks of a
+  persistent grid, so a replica's state moves between SMs inside a launch), 25 launches of
+  250 requests per replica (the default 5 warm-up + 20 timed steps); sampled replicas
+  replayed by the oracle over all 6 250 requests;
 * C3 (balanced, 16 384-block pool, multi-CTA group) over its first 50 000 requests;
 * C4 on its full 4M-block pool from the empty pool through the first eviction rounds the
   bench's C4 workload times (SAE_LONG=1 extends this to 1 200 rounds past the fill);
@@ -43,7 +45,11 @@ def test_c5_bench_launch_structure():
     cache = S.SaeCache(2304, n_replicas=R, policy=pol, traj_capacity=256)
     for r in range(R):
         cache.set_params(r, C.c5_point_params(RP.layout(r)[1]))
-    sample = (0, 31, 32, 517, 1023)
+    lay = cache.layout()
+    assert lay["ctas_per_replica"] == 1 and lay["threads"] == 256, lay
+    if lay["coresident"] < R:            # (every B200: 148 SMs x 3 < 1024)
+        assert lay["chunks"] > 1, lay
+    sample = (0, 1, 31, 32, 300, 443, 444, 517, 700, 887, 1022, 1023)
     got = {r: ([], []) for r in sample}
     # one device-resident token arena of the 32 seeds (as bench.py); per step only the
     # request arrays of the 1024 replicas are built

@@ -155,6 +155,54 @@ def test_multi_replica_parameter_points():
         off += n
 
 
+@pytest.mark.parametrize("chunks", [2, 7])
+def test_task_split_replay_matches_oracle(chunks, monkeypatch):
+    """Task-split persistent replay (sae.cu d.nchunk, forced with SAE_CHUNKS): each replica's
+    run is replayed as consecutive chunks taken from one task counter by whichever CTA is
+    free, the state crossing SMs through release/acquire flags; uneven and empty chunks
+    (runs shorter than the chunk count) included.  Every replica equals its oracle replay."""
+    monkeypatch.setenv("SAE_CHUNKS", str(chunks))
+    traces = []
+    for sd in range(3):
+        t = T.generate(C.get("c5", n_requests=500), seed=0x5AEC2000 + sd)
+        T.materialize(t)
+        traces.append(t)
+    R = 9
+    rep_of = [r % 3 for r in range(R)]
+    pol = C.policy_config(256, K=40)
+    cache = S.SaeCache(256, n_replicas=R, policy=pol, traj_capacity=1 << 14)
+    assert cache.layout()["chunks"] == chunks
+    for r in range(R):
+        cache.set_params(r, C.c5_point_params((5 * r) % 32))
+    # three launches per replica run: 3 requests (fewer than 7 chunks), then the rest in two
+    cuts = [0, 3, 200, 500]
+    got = {r: ([], []) for r in range(R)}
+    for a, z in zip(cuts[:-1], cuts[1:]):
+        part = [{**{k: t[k][a:z] for k in ("arrival", "prompt_off", "prompt_len", "decode_off",
+                                            "decode_len", "flags", "spb")},
+                 "n": z - a, "tokens": t["tokens"], "types": t["types"], "n_tokens": t["n_tokens"]}
+                for t in traces]
+        batch = T.replicate(part, rep_of)
+        out = cache.admit_batch(S.batch_to_torch(batch))
+        torch.cuda.synchronize()
+        o4, _ = unpack(out, batch["n"])
+        vo = out["victim_off"].cpu().numpy()
+        vids = u32(out["victim_ids"])
+        for r in range(R):
+            off = r * (z - a)
+            got[r][0].append(o4[off:off + z - a])
+            got[r][1].extend(int(v) for i in range(z - a) for v in vids[vo[off + i]:vo[off + i] + o4[off + i, 3]])
+    for r in range(R):
+        p = dict(pol)
+        p["params"] = C.c5_point_params((5 * r) % 32)
+        O = oracle.Replica(p)
+        ref = O.replay(traces[rep_of[r]])
+        assert np.array_equal(np.concatenate(got[r][0]), ref.out4), r
+        assert got[r][1] == [int(v) for v in ref.victims], r
+        assert_stats_equal(cache.stats(r), ref.stats)
+        assert_traj_equal(cache.traj(r), ref.traj)
+
+
 def test_gen_tokens_matches_numpy():
     tr = T.generate(C.get("c2", n_requests=500))
     T.materialize(tr)
