@@ -739,30 +739,50 @@ def run_ours(args, wl, ws, rank, local):
 
     # ---- end to end through the public API with pinned host inputs (continuing the trace)
     e2e_ms, h2d, d2h, e2e_req = 0.0, 0, 0, 0
-    # one untimed warm-up call first (staging buffers, pinned output buffers), then K timed
+    # K timed calls of sae_admit_batch_host back to back (after one untimed warm-up call that
+    # sizes the staging and the pinned output buffers).  The library pipelines them: a call's
+    # host->device copies run on its copy stream while the previous call replays (at most two
+    # calls in flight); each step's result is read on the host (its hit count) once the step
+    # is done, while the next one runs.  Every copy of every timed step is inside the region
+    # [e0, e1] on the device clock.  No L2 flush between these steps: each step's inputs
+    # (~0.5 GB of tokens) exceed L2.
     host_steps = [step_batch(s) for s in range(W + K, W + 2 * K + 1)]
     tok_h = torch.from_numpy(arena_tok.view(np.int32)).pin_memory()
     typ_h = torch.from_numpy(arena_typ).pin_memory()
-    for si, hb in enumerate(host_steps):
+    pinned = []
+    for hb in host_steps:
         hp = S.batch_to_torch({**hb, "tokens": np.zeros(1, np.uint32), "types": np.zeros(1, np.uint8)},
                               pin=True)
         a = int(hb["prompt_off"].min())
         z = int((hb["decode_off"] + hb["decode_len"].astype(np.uint64)).max())
-        flush.zero_()
-        barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
+        pinned.append((hp, a, z, hb["n"]))
+    hp, a, z, _ = pinned[0]
+    cache.admit_batch_host(hp, tok_h, typ_h, tok_d, typ_d, a, z)
+    flush.zero_()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    pend, e2e_hits = [], 0
+    for hp, a, z, n in pinned[1:]:
         res, nbytes_in, nbytes_out = cache.admit_batch_host(hp, tok_h, typ_h, tok_d, typ_d, a, z)
-        e1.record()
-        torch.cuda.synchronize()
-        barrier()
-        if si == 0:
-            continue
-        e2e_ms += e0.elapsed_time(e1)
+        ev = torch.cuda.Event()
+        ev.record()
+        pend.append((ev, res))
         h2d += nbytes_in
         d2h += nbytes_out
-        e2e_req += hb["n"]
+        e2e_req += n
+        if len(pend) > 1:                    # the previous step's result, read on the host
+            evp, rp = pend.pop(0)
+            evp.synchronize()
+            e2e_hits += int(rp["hit_blocks"].sum())
+    e1.record()
+    torch.cuda.synchronize()
+    for evp, rp in pend:
+        e2e_hits += int(rp["hit_blocks"].sum())
+    e2e_ms = e0.elapsed_time(e1)
+    barrier()
 
     # ---- reduce over ranks (max time, summed work)
     def allmax(x):
@@ -867,7 +887,10 @@ def run_ours(args, wl, ws, rank, local):
                      "algorithmic_bytes_per_launch": alg_bytes / max(rep_n, 1),
                      "avg_launch_ms": avg_ms, "kernel_share_of_step": rep_ms / max(tot_ms, 1e-9)},
         "e2e": {"value": e2e_all / (e2e_tmax * 1e-3), "unit": "req/s",
-                "h2d_bytes_per_step": int(h2d / K), "d2h_bytes_per_step": int(d2h / K)},
+                "h2d_bytes_per_step": int(h2d / K), "d2h_bytes_per_step": int(d2h / K),
+                "pipeline": "sae_admit_batch_host, two calls in flight (copies of step s+1 overlap "
+                            "the replay of step s); no L2 flush (each step's inputs exceed L2)",
+                "hit_blocks_read_on_host": e2e_hits},
     }
     if not args.no_predictor:
         # SURVEY 8(f) rank 4, the tensor-core piece: timed alone after the replay steps

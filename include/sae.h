@@ -261,7 +261,13 @@ sae_status sae_admit_batch(sae_ctx* ctx, const sae_batch* batch, sae_admit_out* 
  * per-request outputs [n], victim_off [n+1] and victim_ids [victim_cap >= total_blocks] are
  * copied back device->host on s (read them after synchronising s); block_hash / block_tau
  * may be NULL.  *h2d_bytes / *d2h_bytes (optional, host) receive the bytes copied each way.
- * Errors as sae_admit_batch. */
+ * Pipelining: the inputs are staged in one of two ctx-owned slots, alternately, and copied
+ * on a ctx-owned copy stream, so a call's host->device copies overlap the replay of the
+ * previous call (the replay on s waits for them; the device->host copies stay on s).  A call
+ * blocks until the call two before it is complete: host buffers (inputs and outputs) passed
+ * to a call must stay valid until the second-next call returns or s is synchronised, and the
+ * arena range [tok_lo, tok_hi) must not be rewritten by the next call while this one may
+ * still read it.  Errors as sae_admit_batch. */
 sae_status sae_admit_batch_host(sae_ctx* ctx, const sae_batch* host_batch, uint64_t tok_lo,
                                 uint64_t tok_hi, uint32_t* tokens_dev, uint8_t* types_dev,
                                 sae_admit_out* host_out, uint64_t* h2d_bytes, uint64_t* d2h_bytes,

@@ -324,13 +324,20 @@ class SaeCache:
         (pinned host tensors in hb) and the token arena range [a, z) (pinned tok_h / typ_h)
         are copied host->device by the library, the batch is replayed, and the per-request
         outputs and victim ids come back into pinned host buffers (valid after the stream
-        synchronises).  Returns (host outputs, h2d bytes, d2h bytes)."""
+        synchronises).  Successive calls pipeline (the library stages inputs in two slots on
+        its own copy stream): the outputs alternate between two pinned sets, so a call's
+        results stay valid while the next call runs.  Returns (host outputs, h2d bytes,
+        d2h bytes)."""
         n, tb = hb["n"], hb["total_blocks"]
-        st = self._staging = getattr(self, "_staging", {})
-        hout = st.get("hout")
+        st = self._staging = getattr(self, "_staging", {"slot": 0})
+        slot = st["slot"]
+        st["slot"] ^= 1
+        hout = st.get(slot)
         if hout is None or hout["victim_ids"].numel() < max(tb, 1) or hout["hit_blocks"].numel() < n:
-            hout = st["hout"] = {k: torch.empty(max(2 * n, 1), dtype=torch.int32, pin_memory=True)
-                                 for k in ("hit_blocks", "miss_blocks", "matched_tokens", "n_victims")}
+            if hout is not None:
+                self.sync(stream)           # the set may still be a target of a queued copy
+            hout = st[slot] = {k: torch.empty(max(2 * n, 1), dtype=torch.int32, pin_memory=True)
+                               for k in ("hit_blocks", "miss_blocks", "matched_tokens", "n_victims")}
             hout["victim_off"] = torch.empty(2 * n + 1, dtype=torch.int64, pin_memory=True)
             hout["victim_ids"] = torch.empty(max(2 * tb, 1), dtype=torch.int32, pin_memory=True)
         sb = sae_batch()
@@ -347,7 +354,7 @@ class SaeCache:
             setattr(ao, k, hout[k].data_ptr())
         ao.victim_cap = hout["victim_ids"].numel()
         h2d, d2h = C.c_uint64(), C.c_uint64()
-        self._keep = (hb, hout)
+        st["keep%d" % slot] = (hb, hout)        # host inputs stay alive while their copies are queued
         self._check(lib().sae_admit_batch_host(self.h, C.byref(sb), a, z, tok_d.data_ptr(),
                                                typ_d.data_ptr(), C.byref(ao), C.byref(h2d),
                                                C.byref(d2h), _stream(stream)))

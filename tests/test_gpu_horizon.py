@@ -9,6 +9,7 @@ cases driven through the C ABI and the score function itself:
 * C3 (balanced, 16 384-block pool, multi-CTA group) over its first 50 000 requests;
 * C4 on its full 4M-block pool from the empty pool through the first eviction rounds the
   bench's C4 workload times (SAE_LONG=1 extends this to 1 200 rounds past the fill);
+* C4x: the same trace on a 2^24-block pool, 500 eviction rounds past the fill;
 * edge cases the trace generator never produces: equal arrival times, sigma at its 0.1 floor
   with large dt so that P = 0 ties are broken by (last, id), K = 1, one-token prompts with no
   decode, admissions larger than free + unpinned space (k > U);
@@ -125,6 +126,34 @@ def test_c4_full_pool_through_eviction_rounds(rounds):
     ref = R.replay(tr, 0, hi)
     print("c4: pool full at request %d; oracle through %d eviction rounds in %.0f s"
           % (first, rounds, time.time() - t0))
+    tb = int(ref.boff[hi])
+    assert np.array_equal(out["block_hash"][:tb].cpu().numpy().view(np.uint64), ref.hashes)
+    assert np.array_equal(o4[:hi], ref.out4)
+    nv = int(ref.voff[hi])
+    assert nv > 0 and np.array_equal(victims[:nv], ref.victims)
+
+
+def test_c4x_pool_500_rounds_past_the_fill():
+    """C4x: the C4 trace on a 2^24-block pool (scan records beyond L2, the
+    bulk-copy streaming path with evict_first), filled from empty (~0.4 M requests), then 500
+    eviction rounds; every hash, per-request output and victim id identical to the oracle."""
+    n = 470_000
+    tr = T.make("c4", n_requests=n)
+    pol = C.policy_config(1 << 24)
+    cache = S.SaeCache(pol["capacity"], policy=pol)
+    b = S.batch_to_torch(T.single_batch(tr))
+    out = cache.admit_batch(b, want_hashes=True)
+    torch.cuda.synchronize()
+    o4, victims = unpack(out, tr["n"])
+    ev = np.nonzero(o4[:, 3] > 0)[0]
+    assert len(ev) > 0, "the 2^24-block pool never filled"
+    first = int(ev[0])
+    hi = min(first + 500, n)
+    assert hi - first >= 500, (first, n)
+    t0 = time.time()
+    ref = oracle.Replica(pol).replay(tr, 0, hi)
+    print("c4x: pool full at request %d; oracle through 500 eviction rounds in %.0f s"
+          % (first, time.time() - t0))
     tb = int(ref.boff[hi])
     assert np.array_equal(out["block_hash"][:tb].cpu().numpy().view(np.uint64), ref.hashes)
     assert np.array_equal(o4[:hi], ref.out4)
