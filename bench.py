@@ -180,6 +180,13 @@ def score_select_phase(dev, capacity: int = 1 << 24, m: int = 64, passes: int = 
     st1 = cache.stats(0)
     ms = e0.elapsed_time(e1)
     npass = launches * passes
+    dp = max(st1.select_passes - st0.select_passes, 1)
+    # leader phase timers per pass (us): scan = command post + workers' stream + wait; then the
+    # leader's own work on the candidates
+    ph = [(st1.phase_ns[i] - st0.phase_ns[i]) / 1e3 / dp for i in range(16)]
+    phases = {"scan_incl_wait": ph[1], "narrow": ph[2], "select_total": ph[3], "gather": ph[13],
+              "radix": ph[14], "staging_order": ph[15], "threshold_carry": ph[12],
+              "worker1_stream": ph[11], "cmd_post": ph[8], "leader_own_part": ph[9], "wait": ph[10]}
     pass_us = 1e3 * ms / npass
     byts = 12.0 * resident
     hbm, src = peaks()
@@ -188,7 +195,9 @@ def score_select_phase(dev, capacity: int = 1 << 24, m: int = 64, passes: int = 
             "pool_blocks": capacity, "resident_blocks": resident, "victims_per_pass": m,
             "launches": launches, "passes_per_launch": passes, "us_per_pass": pass_us,
             "blocks_scored_per_s": resident / (pass_us * 1e-6),
-            "candidates_per_pass": (st1.select_cands - st0.select_cands) / max(st1.select_passes - st0.select_passes, 1),
+            "candidates_per_pass": (st1.select_cands - st0.select_cands) / dp,
+            "raw_candidates_per_pass": (st1.select_raw - st0.select_raw) / dp,
+            "leader_us_per_pass": phases,
             "fill": {"requests": lo, "trace_gen_s": round(t_gen, 1), "fill_s": round(t_fill, 1)},
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "peak_source": src, "unit": "GB/s",
                          "frac": gbs / hbm, "bytes_per_pass": byts,

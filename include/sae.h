@@ -292,7 +292,8 @@ sae_status sae_evict(sae_ctx* ctx, uint32_t replica, uint32_t k, double now,
  * smallest Eq.(3) priorities by (P, last, id) -- with an empty pin set,
  * computed `passes` >= 1 times back to back in one launch (a measurement of the pass).
  * READ-ONLY: nothing is evicted, no counter, parameter or clock changes; only the carried
- * per-segment candidacy thresholds (a performance hint) are kept.  victim_ids
+ * per-segment candidacy thresholds (a performance hint) and the diagnostics
+ * of sae_replica_stats (phase_ns, select_passes / cands / raw / narrow / big) are kept.  victim_ids
  * (device, >= m) receive the ids in eviction order -- exactly those sae_evict(m, now) would
  * remove if no learner fires in between -- and *n_out (device u32, may be NULL) their count
  * (min(m, resident)).  SAE_E_INVAL for a bad replica, m > 96 or passes == 0; SAE_E_TIME

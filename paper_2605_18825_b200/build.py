@@ -6,6 +6,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+import time
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
@@ -68,17 +69,23 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     tag = ("_" + "_".join(d.replace("=", "-") for d in defines)) if defines else ""
     os.makedirs(OBJ, exist_ok=True)
     objs = []
+    t_first = None
     for tu, deps in SOURCES.items():
         o = os.path.join(OBJ, tu.replace(".cu", tag + ".o"))
         if force or _newer(o, [os.path.join(CSRC, f) for f in deps] + [_hdr()]):
             tmp = o + ".tmp%d" % os.getpid()
+            t0 = time.time()
+            t_first = t0 if t_first is None else min(t_first, t0)
             _run([nvcc(), *NVCC_FLAGS, *["-D" + d for d in defines], "-I", os.path.join(ROOT, "include"),
                   "-c", "-o", tmp, os.path.join(CSRC, tu)], verbose)
             os.replace(tmp, o)
+            os.utime(o, (t0, t0))     # a source edited during the compile stays newer: rebuilt next time
         objs.append(o)
     tmp = dst + ".tmp%d" % os.getpid()
     _run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs], verbose)
     os.replace(tmp, dst)
+    if t_first is not None:
+        os.utime(dst, (t_first, t_first))
     return dst
 
 

@@ -2166,7 +2166,8 @@ __global__ void __launch_bounds__(NT, MINB) k_evict(Dev d, uint32_t r, uint32_t 
 // sae_select: the fused score/select pass alone (K3, Alg.1 Evict's choice of m victims,
 // P:504-525), `passes` times back to back, read-only: no block is removed and no counter,
 // parameter or clock of the replica changes.  Only the carried per-segment thresholds are
-// written back -- a performance hint that exactness never depends on (§6).
+// written back -- a performance hint that exactness never depends on (§6) -- and the
+// diagnostics (phase timers, pass and candidate counts).
 __global__ void __launch_bounds__(NT, MINB) k_select(Dev d, uint32_t r, uint32_t m, double now,
                                                   uint32_t passes, uint32_t* vids, uint32_t* n_out) {
   Ctx c = make_ctx(d, r, blockIdx.x);
@@ -2191,8 +2192,19 @@ __global__ void __launch_bounds__(NT, MINB) k_select(Dev d, uint32_t r, uint32_t
     for (uint32_t v = threadIdx.x; v < mm; v += NT)
       vids[v] = __ldcg(d.bid + c.base + (c.cand[v].ss & SLOT_MASK));
     cta_sync();
-    // carry the thresholds only (exactness never depends on them)
-    if (threadIdx.x < 16) d.st[c.r].thr[threadIdx.x] = st.thr[threadIdx.x];
+    // carry the thresholds only (exactness never depends on them), plus the diagnostics
+    // (phase timers, pass / candidate counts: no replica semantics)
+    if (threadIdx.x < 16) {
+      d.st[c.r].thr[threadIdx.x] = st.thr[threadIdx.x];
+      d.st[c.r].tph[threadIdx.x] = st.tph[threadIdx.x];
+    }
+    if (threadIdx.x == 0) {
+      d.st[c.r].select_passes = st.select_passes;
+      d.st[c.r].select_cands = st.select_cands;
+      d.st[c.r].select_raw = st.select_raw;
+      d.st[c.r].select_narrow = st.select_narrow;
+      d.st[c.r].select_big = st.select_big;
+    }
   }
   if (threadIdx.x == 0 && n_out) *n_out = ok ? mm : 0u;
   cta_sync();
