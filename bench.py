@@ -615,7 +615,7 @@ def run_ours(args, wl, ws, rank, local):
         g0, g1 = RP.shard(1024, ws, rank)
         R = g1 - g0
         per = wl["per_step"]
-        n_req = per * (W + 2 * K + 1)
+        n_req = per * (W + 2 * K + 2)
         traces = []
         seeds = sorted(set(RP.layout(g)[0] for g in range(g0, g1)))
         for sd in seeds:
@@ -655,7 +655,7 @@ def run_ours(args, wl, ws, rank, local):
         R = 1
         per = wl["per_step"]
         pre = wl.get("prefill", 0)
-        tr0 = make_trace(wl, rank, n_requests=(pre + per * (W + 2 * K + 1)) if pre else None)
+        tr0 = make_trace(wl, rank, n_requests=(pre + per * (W + 2 * K + 2)) if pre else None)
         pol = CFG.policy_config(tr0["config"]["capacity"])
         cache = S.SaeCache(pol["capacity"], n_replicas=1, policy=pol)
         fill_at = None                    # first request of the trace that had to evict
@@ -748,14 +748,14 @@ def run_ours(args, wl, ws, rank, local):
 
     # ---- end to end through the public API with pinned host inputs (continuing the trace)
     e2e_ms, h2d, d2h, e2e_req = 0.0, 0, 0, 0
-    # K timed calls of sae_admit_batch_host back to back (after one untimed warm-up call that
-    # sizes the staging and the pinned output buffers).  The library pipelines them: a call's
+    # K timed calls of sae_admit_batch_host back to back (after two untimed warm-up calls that
+    # size both staging slots and both pinned output sets).  The library pipelines them: a call's
     # host->device copies run on its copy stream while the previous call replays (at most two
     # calls in flight); each step's result is read on the host (its hit count) once the step
     # is done, while the next one runs.  Every copy of every timed step is inside the region
     # [e0, e1] on the device clock.  No L2 flush between these steps: each step's inputs
     # (~0.5 GB of tokens) exceed L2.
-    host_steps = [step_batch(s) for s in range(W + K, W + 2 * K + 1)]
+    host_steps = [step_batch(s) for s in range(W + K, W + 2 * K + 2)]
     tok_h = torch.from_numpy(arena_tok.view(np.int32)).pin_memory()
     typ_h = torch.from_numpy(arena_typ).pin_memory()
     pinned = []
@@ -765,8 +765,8 @@ def run_ours(args, wl, ws, rank, local):
         a = int(hb["prompt_off"].min())
         z = int((hb["decode_off"] + hb["decode_len"].astype(np.uint64)).max())
         pinned.append((hp, a, z, hb["n"]))
-    hp, a, z, _ = pinned[0]
-    cache.admit_batch_host(hp, tok_h, typ_h, tok_d, typ_d, a, z)
+    for hp, a, z, _ in pinned[:2]:       # both staging slots / pinned output sets, untimed
+        cache.admit_batch_host(hp, tok_h, typ_h, tok_d, typ_d, a, z)
     flush.zero_()
     torch.cuda.synchronize()
     barrier()
@@ -774,7 +774,7 @@ def run_ours(args, wl, ws, rank, local):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     pend, e2e_hits = [], 0
-    for hp, a, z, n in pinned[1:]:
+    for hp, a, z, n in pinned[2:]:
         res, nbytes_in, nbytes_out = cache.admit_batch_host(hp, tok_h, typ_h, tok_d, typ_d, a, z)
         ev = torch.cuda.Event()
         ev.record()
