@@ -1849,6 +1849,10 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
   if (threadIdx.x < 16) s.pincnt[threadIdx.x] = 0;
   cta_sync();
   const uint32_t stamp = (uint32_t)st.round;
+  if (d.pf_next && c.GP == 1 && i + 1 < b.n && threadIdx.x < 4) {   // next request's hashes -> L2
+    const uint64_t* hn = b.h + b.boff[i + 1];
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(hn + 16 * threadIdx.x));
+  }
   uint64_t tA = gtimer();
   // ---- O4/O5 classify + probe (Alg.1 Classify P:550-564; strict prefix P:158)
   // (the first NT blocks' values stay in registers for the next loop: same thread, same j)
@@ -1966,6 +1970,20 @@ __device__ bool admit_one(Ctx& c, const BatchDev& b, uint32_t i) {
     c.pf_n = (uint32_t)min(b.boff[i + 2] - b.boff[i + 1], (uint64_t)512);
   } else {
     c.pf_n = 0;
+    if (d.pf_next && i + 1 < b.n && b.replica[i + 1] == b.replica[i]) {
+      // private pool: pull the next request's resident-table and ghost-table home lines into
+      // L2 before this request's evictions; its probes then start from L2 (its hashes were
+      // prefetched at this request's start)
+      const uint64_t* hn = b.h + b.boff[i + 1];
+      const uint32_t nn = (uint32_t)min(b.boff[i + 2] - b.boff[i + 1], (uint64_t)NT);
+      if (threadIdx.x < nn) {
+        const uint64_t H = hn[threadIdx.x];
+        const uint64_t tb = (uint64_t)d.tmask + 1, gt = (uint64_t)d.gmask + 1;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(d.tkey + (uint64_t)c.r * tb + home(H, d.tmask)));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(d.tval + (uint64_t)c.r * tb + home(H, d.tmask)));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(d.gkey + (uint64_t)c.r * gt + home(H, d.gmask)));
+      }
+    }
   }
   if (k > 0) evict_k(c, k, stamp, b.o_vids ? b.o_vids + b.boff[i] : nullptr);
   tA = gtimer();

@@ -131,6 +131,8 @@ struct Dev {
                         // co-resident CTAs): each replica's run is cut into nchunk consecutive
                         // chunks, a persistent grid takes (chunk, replica) tasks in order from
                         // *taskctr, and chunk k of replica r waits for rflag[r] = (epoch, k)
+  uint32_t pf_next;     // 1: a private-pool replay prefetches the next request's table home
+                        // lines into L2 before its evictions (env SAE_PREFETCH=0: off)
   uint32_t* taskctr;    // [1] next task of the current launch (zeroed before each launch)
   uint32_t* rflag;      // [R] (epoch << 8) | chunks of the replica's run done this launch
   Cand* gcand;          // [R*C] global candidate buffer (large pools)
@@ -889,6 +891,8 @@ static sae_status create_impl(const sae_config* cfg, sae_ctx* ctx) {
     const int v = atoi(e);
     if (v >= 1 && v <= 255 && d.GP == 1) d.nchunk = (uint32_t)v;
   }
+  d.pf_next = 1;
+  if (const char* e = getenv("SAE_PREFETCH")) d.pf_next = atoi(e) != 0 ? 1u : 0u;
   CK(dalloc(ctx, &d.taskctr, 1));
   CK(dalloc(ctx, &d.rflag, R));
   CK(cudaMemset(d.rflag, 0, R * 4));
