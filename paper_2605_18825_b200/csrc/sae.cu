@@ -100,6 +100,7 @@ struct GroupCtl {          // hot words on separate 128-byte lines (polled / ato
   alignas(128) unsigned long long cmdw;   // posted command word (epoch:24 | seq:32 | cmd:8)
   alignas(128) unsigned long long done;   // cumulative worker completions this launch
   alignas(128) unsigned ncand;
+  alignas(128) unsigned tilectr;          // next tile of the workers' bulk scan (dynamic tiles)
   alignas(128) unsigned nsel;
   alignas(128) unsigned tblcnt;
   alignas(128) unsigned gtblcnt;
@@ -131,8 +132,6 @@ struct Dev {
                         // co-resident CTAs): each replica's run is cut into nchunk consecutive
                         // chunks, a persistent grid takes (chunk, replica) tasks in order from
                         // *taskctr, and chunk k of replica r waits for rflag[r] = (epoch, k)
-  uint32_t pf_next;     // 1: a private-pool replay prefetches the next request's table home
-                        // lines into L2 before its evictions (env SAE_PREFETCH=0: off)
   uint32_t* taskctr;    // [1] next task of the current launch (zeroed before each launch)
   uint32_t* rflag;      // [R] (epoch << 8) | chunks of the replica's run done this launch
   Cand* gcand;          // [R*C] global candidate buffer (large pools)
@@ -796,7 +795,10 @@ static sae_status create_impl(const sae_config* cfg, sae_ctx* ctx) {
   d.hash_seed = cfg->hash_seed;
   d.dt_eps = cfg->dt_eps;
   d.z_cut = cfg->z_cut;
-  const uint64_t TB = pow2_at_least(2ull * d.C), GT = pow2_at_least(2ull * d.G);
+  // open-addressing tables: the smallest power of two with >= C/4 tombstone headroom below
+  // the 75 % rebuild trigger (TB >= 5C/3): C5's 2304-block replicas get 4096 slots (48 KB per
+  // table instead of 96 KB at 2C -- the replicas' working set is what the L2 holds)
+  const uint64_t TB = pow2_at_least((5ull * d.C + 2) / 3), GT = pow2_at_least((5ull * d.G + 2) / 3);
   d.tmask = (uint32_t)(TB - 1);
   d.gmask = (uint32_t)(GT - 1);
   const uint64_t R = d.R, RC = R * d.C;
@@ -891,8 +893,6 @@ static sae_status create_impl(const sae_config* cfg, sae_ctx* ctx) {
     const int v = atoi(e);
     if (v >= 1 && v <= 255 && d.GP == 1) d.nchunk = (uint32_t)v;
   }
-  d.pf_next = 1;
-  if (const char* e = getenv("SAE_PREFETCH")) d.pf_next = atoi(e) != 0 ? 1u : 0u;
   CK(dalloc(ctx, &d.taskctr, 1));
   CK(dalloc(ctx, &d.rflag, R));
   CK(cudaMemset(d.rflag, 0, R * 4));
