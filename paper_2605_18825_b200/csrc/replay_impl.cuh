@@ -162,9 +162,6 @@ struct Smem {
   __align__(16) uint32_t rhist[NSEG * 256];   // radix-select histograms (one 256-bin digit per
                                 // segment); worker scan: its finished candidate records
   __align__(8) uint64_t mbar[24];  // bulk-copy stage barriers (worker scan pipeline): full[12], empty[12]
-  uint32_t stile[12];       // worker scan: tile held by each ring stage (>= ntot: end marker)
-  uint32_t wlast[12];       // worker scan: last armed use (local sequence number) of each stage
-  uint32_t wend, wnarm;     // worker scan: the prologue armed an end marker; stages it armed
   uint64_t wthr[16], wpfx[16], wpmask[16];   // worker copies of the leader's command parameters
   double wcw[15], wmu[2], wsg[2], ww[5];
 };
@@ -491,6 +488,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// (Static equal slices per worker.  Tiles handed out dynamically from one group counter were
+//  measured slower: k_select pass 74.1 vs 66 us on C4x, worker stream 42 vs 37 us.)
 // Worker scan over [lo, hi) (lo a multiple of 4, replica base 16-byte aligned): the two
 // scan columns (meta u32, key u64: 12 B per slot) are streamed tile by tile into shared
 // memory by bulk asynchronous copies, BSTAGES tiles in flight, and scored from shared
@@ -507,87 +506,68 @@ constexpr uint32_t BTILE_BYTES = BTILE * (4 + 8);
 constexpr int BSTAGES = (int)((CAND_MAX * sizeof(Cand)) / BTILE_BYTES) < 12
                             ? (int)((CAND_MAX * sizeof(Cand)) / BTILE_BYTES) : 12;
 static_assert(BSTAGES >= 2, "bulk scan needs two stages");
-// Tiles are handed out dynamically: the group's workers take tile indices from one counter
-// (GroupCtl::tilectr, reset by the leader before every scan command), so a worker that
-// streams faster takes more tiles and all finish together (static equal slices left the
-// pass waiting for the slowest SM).  Stage st of the ring holds tile s.stile[st]; an index
-// >= ntot is the end marker (armed on the full barrier without transaction bytes).
-__device__ __forceinline__ void bulk_arm(Ctx& c, int st, uint32_t tile, uint64_t ntot, uint64_t pol) {
-  const Dev& d = *c.d;
-  Smem& s = *c.s;
-  uint64_t* full = &s.mbar[0];
-  s.stile[st] = tile;
-  if ((uint64_t)tile >= ntot) {           // end marker: completes the phase with no bytes
-    mbar_arrive(&full[st]);
-    return;
-  }
-  const uint64_t t0 = (uint64_t)tile * BTILE;
-  const uint32_t n4 = ((uint32_t)min((uint64_t)BTILE, (uint64_t)d.C - t0) + 3) & ~3u;   // SoA padded
-  unsigned char* b = reinterpret_cast<unsigned char*>(c.cand) + (size_t)st * BTILE_BYTES;
-  mbar_expect_tx(&full[st], n4 * 12u);
-  if (d.scan_l2) {
-    bulk_g2s_pol(b, d.bmeta + c.base + t0, n4 * 4u, &full[st], pol);
-    bulk_g2s_pol(b + BTILE * 4, d.bkey + c.base + t0, n4 * 8u, &full[st], pol);
-  } else {
-    bulk_g2s(b, d.bmeta + c.base + t0, n4 * 4u, &full[st]);
-    bulk_g2s(b + BTILE * 4, d.bkey + c.base + t0, n4 * 8u, &full[st]);
-  }
-}
-__device__ void scan_bulk_begin(Ctx& c) {
+__device__ void scan_bulk_begin(Ctx& c, uint64_t lo, uint64_t hi) {
   const Dev& d = *c.d;
   Smem& s = *c.s;
   if (threadIdx.x != 0) return;
-  const uint64_t ntot = ((uint64_t)d.C + BTILE - 1) / BTILE;
+  unsigned char* buf = reinterpret_cast<unsigned char*>(c.cand);
+  const uint64_t ntiles = (hi - lo + BTILE - 1) / BTILE;
   uint64_t* full = &s.mbar[0];
   uint64_t* empty = &s.mbar[12];
   for (int st = 0; st < BSTAGES; ++st) { mbar_init(&full[st], 1); mbar_init(&empty[st], NW); }
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   const uint64_t pol = d.scan_l2 ? l2_policy(d.scan_l2) : 0ull;
-  const uint32_t t = atomicAdd(&c.ctl->tilectr, (unsigned)BSTAGES);
-  s.wend = 0;
-  for (int st = 0; st < BSTAGES; ++st) {   // arm consecutive stages up to the first end marker
-    bulk_arm(c, st, t + st, ntot, pol);
-    s.wlast[st] = st;
-    if ((uint64_t)(t + st) >= ntot) { s.wend = 1; s.wnarm = st + 1; return; }
+  for (uint64_t t = 0; t < ntiles && t < (uint64_t)BSTAGES; ++t) {
+    const uint64_t t0 = lo + t * BTILE;
+    const uint32_t n4 = ((uint32_t)min((uint64_t)BTILE, hi - t0) + 3) & ~3u;
+    unsigned char* b = buf + (size_t)t * BTILE_BYTES;
+    mbar_expect_tx(&full[t], n4 * 12u);
+    if (d.scan_l2) {
+      bulk_g2s_pol(b, d.bmeta + c.base + t0, n4 * 4u, &full[t], pol);
+      bulk_g2s_pol(b + BTILE * 4, d.bkey + c.base + t0, n4 * 8u, &full[t], pol);
+    } else {
+      bulk_g2s(b, d.bmeta + c.base + t0, n4 * 4u, &full[t]);
+      bulk_g2s(b + BTILE * 4, d.bkey + c.base + t0, n4 * 8u, &full[t]);
+    }
   }
-  s.wnarm = BSTAGES;
 }
-__device__ void scan_range_bulk(Ctx& c, const ScanP& P) {
+__device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P) {
   const Dev& d = *c.d;
   Smem& s = *c.s;
   const int tid = threadIdx.x, lane = tid & 31;
   Cand* gdst = d.gcand + c.base;
-  const unsigned char* buf = reinterpret_cast<const unsigned char*>(c.cand);
-  const uint64_t ntot = ((uint64_t)d.C + BTILE - 1) / BTILE;
+  unsigned char* buf = reinterpret_cast<unsigned char*>(c.cand);
+  const uint64_t ntiles = (hi - lo + BTILE - 1) / BTILE;
   uint64_t* full = &s.mbar[0];
   uint64_t* empty = &s.mbar[12];
-  const uint64_t pol = d.scan_l2 ? l2_policy(d.scan_l2) : 0ull;
-  // producer (thread 0): the tile of the next refill is taken one refill ahead, so the
-  // counter's round trip overlaps the consumption of a tile
-  uint32_t nxt = 0;
-  bool ended = false;
-  if (tid == 0) {
-    ended = s.wend != 0;
-    if (!ended) nxt = atomicAdd(&c.ctl->tilectr, 1u);
-  }
-  // (prologue -- barrier init and the first BSTAGES tiles -- armed by scan_bulk_begin before
-  //  the pass parameters and the candidacy table are staged, so they overlap)
-  for (uint32_t i = 0;; ++i) {
-    const int st = (int)(i % BSTAGES);
-    const uint32_t par = (i / BSTAGES) & 1u;
-    mbar_wait(&full[st], par);
-    const uint32_t tile = s.stile[st];
-    if ((uint64_t)tile >= ntot) {          // end marker (every warp reads it and stops)
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
-      break;
+  auto issue_tile = [&](uint64_t t) {
+    const int st = (int)(t % BSTAGES);
+    const uint64_t t0 = lo + t * BTILE;
+    const uint32_t n = (uint32_t)min((uint64_t)BTILE, hi - t0);
+    const uint32_t n4 = (n + 3) & ~3u;                 // 16-byte multiple (SoA is padded)
+    unsigned char* b = buf + (size_t)st * BTILE_BYTES;
+    mbar_expect_tx(&full[st], n4 * 12u);
+    if (d.scan_l2) {
+      const uint64_t pol = l2_policy(d.scan_l2);
+      bulk_g2s_pol(b, d.bmeta + c.base + t0, n4 * 4u, &full[st], pol);
+      bulk_g2s_pol(b + BTILE * 4, d.bkey + c.base + t0, n4 * 8u, &full[st], pol);
+    } else {
+      bulk_g2s(b, d.bmeta + c.base + t0, n4 * 4u, &full[st]);
+      bulk_g2s(b + BTILE * 4, d.bkey + c.base + t0, n4 * 8u, &full[st]);
     }
+  };
+  // (prologue -- barrier init and the first BSTAGES tiles -- issued by scan_bulk_begin
+  //  before the pass parameters and the candidacy table are staged, so they overlap)
+  for (uint64_t t = 0; t < ntiles; ++t) {
+    const int st = (int)(t % BSTAGES);
+    const uint32_t par = (uint32_t)((t / BSTAGES) & 1);
+    mbar_wait(&full[st], par);
     const unsigned char* b = buf + (size_t)st * BTILE_BYTES;
     const uint32_t* m = reinterpret_cast<const uint32_t*>(b);
     const uint64_t* kk = reinterpret_cast<const uint64_t*>(b + BTILE * 4);
-    const uint64_t t0 = (uint64_t)tile * BTILE;
-    const uint32_t n = (uint32_t)min((uint64_t)BTILE, (uint64_t)d.C - t0);
+    const uint64_t t0 = lo + t * BTILE;
+    const uint32_t n = (uint32_t)min((uint64_t)BTILE, hi - t0);
     uint32_t mv[BTILE / NT];
     uint64_t kv[BTILE / NT];
 #pragma unroll
@@ -622,20 +602,16 @@ __device__ void scan_range_bulk(Ctx& c, const ScanP& P) {
         }
       }
     }
-    if (tid == 0 && !ended) {             // refill stage st once every warp drained it
+    if (tid == 0 && t + BSTAGES < ntiles) {     // refill stage st once every warp drained it
       mbar_wait(&empty[st], par);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads -> async writes
-      bulk_arm(c, st, nxt, ntot, pol);
-      s.wlast[st] = i + BSTAGES;
-      if ((uint64_t)nxt >= ntot) ended = true;
-      else nxt = atomicAdd(&c.ctl->tilectr, 1u);
+      issue_tile(t + BSTAGES);
     }
   }
   cta_sync();
-  if (tid == 0) {       // drain the empty barriers' last armed phases before the next scan re-inits them
-    const int narm = s.wend ? s.wnarm : BSTAGES;
-    for (int st = 0; st < narm; ++st)
-      mbar_wait(&empty[st], (s.wlast[st] / BSTAGES) & 1u);
+  if (tid == 0) {       // drain the empty barriers' last phases before the next scan re-inits them
+    for (uint64_t t = ntiles > (uint64_t)BSTAGES ? ntiles - BSTAGES : 0; t < ntiles; ++t)
+      mbar_wait(&empty[t % BSTAGES], (uint32_t)((t / BSTAGES) & 1));
     for (int st = 0; st < BSTAGES; ++st) {
       asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[st])) : "memory");
       asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&empty[st])) : "memory");
@@ -674,7 +650,7 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
         const uint64_t nw = c.GP - 1, w = c.rank - 1;
         wlo = ((uint64_t)d.C * w / nw) & ~3ull;
         whi = w + 1 == nw ? d.C : (((uint64_t)d.C * (w + 1) / nw) & ~3ull);
-        if (bulk) scan_bulk_begin(c);             // first tiles in flight while staging
+        if (bulk) scan_bulk_begin(c, wlo, whi);   // first tiles in flight while staging
       }
       if (tid < 16) s.cnt[tid] = 0;
       if (tid == 0) { s.ncand = 0; s.nw = 0; }
@@ -708,7 +684,7 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
         // 4-slot-aligned slices and stream it through shared memory
         if (!leader) {
           const uint64_t tw0 = gtimer();
-          if (bulk) scan_range_bulk(c, P);
+          if (bulk) scan_range_bulk(c, wlo, whi, P);
           else scan_range(c, wlo, whi, P);
           if (c.rank == 1 && tid == 0) g->wscan_ns += gtimer() - tw0;
         }
@@ -1346,7 +1322,6 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
       g->stamp = stamp;
       if (gm) {
         g->ncand = 0;
-        g->tilectr = 0;              // dynamic tiles of the workers' bulk scan
         g->now = now;
         for (int i = 0; i < 16; ++i) { g->cnt[i] = 0; g->thr[i] = st.thr[i]; }
         for (int q = 0; q < 3; ++q) for (int t = 0; t < 5; ++t) g->cw[q][t] = s.cw[q][t];

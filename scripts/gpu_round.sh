@@ -50,9 +50,9 @@ for step in "$@"; do
       done ;;
     ncu_c5)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c5.csv \
-        python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+        python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-score-select --no-predictor > /dev/null 2>&1
       timeout 1200 ncu --set full --import-source on --clock-control none -k regex:k_replay -s 3 -c 1 -f -o $O/full_c5 \
-        python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+        python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-score-select --no-predictor > /dev/null 2>&1
       shrink_rep $O/full_c5 ;;
     ncu_c4)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c4.csv \
