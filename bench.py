@@ -186,7 +186,8 @@ def score_select_phase(dev, capacity: int = 1 << 24, m: int = 64, passes: int = 
     ph = [(st1.phase_ns[i] - st0.phase_ns[i]) / 1e3 / dp for i in range(16)]
     phases = {"scan_incl_wait": ph[1], "narrow": ph[2], "select_total": ph[3], "gather": ph[13],
               "radix": ph[14], "staging_order": ph[15], "threshold_carry": ph[12],
-              "worker1_stream": ph[11], "cmd_post": ph[8], "leader_own_part": ph[9], "wait": ph[10]}
+              "worker1_stream": ph[11], "cmd_post": ph[8], "leader_own_part": ph[9], "wait": ph[10],
+              "slots_4_7": ph[4:8]}    # (a SAE_CARRY_TIMERS debug build: the carry's sub-phases)
     pass_us = 1e3 * ms / npass
     byts = 12.0 * resident
     hbm, src = peaks()

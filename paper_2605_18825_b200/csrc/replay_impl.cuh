@@ -1547,8 +1547,15 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
     return;
   }
   // ---- carry thresholds: trim segments holding far more candidates than they use
+#ifdef SAE_CARRY_TIMERS   // debug build: sub-phases of the carry in the apply/learn/insert/rebuild slots
+  uint64_t tC = gtimer();
+#define CARRY_T(k) do { if (tid == 0) { const uint64_t t_ = gtimer(); st.tph[k] += t_ - tC; tC = t_; } } while (0)
+#else
+#define CARRY_T(k) do { } while (0)
+#endif
   for (uint32_t v = tid; v < m; v += NT) atomicAdd(&s.used[c.vbuf[v].seg], 1u);
   cta_sync();
+  CARRY_T(4);
   // small private pools (rescans are cheap) trim hard; large pools trim lazily
   const uint32_t trim_at = d.trim_at, trim_to = d.trim_to;
   uint32_t shrink = 0;
@@ -1563,6 +1570,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
     if (tid < NSEG && ((shrink >> tid) & 1u)) st.thr[tid] = min(st.thr[tid], s.pfx[tid] | ~s.pmask[tid]);
     cta_sync();
   }
+  CARRY_T(5);
   // ---- grow a segment's threshold before its reserve runs dry (avoids refills): double
   //      the key distance from the smallest candidate (keys: EF (ntok,id); class last;
   //      STRUCT P).  Heuristic only -- exactness is re-proved every pass.
@@ -1603,6 +1611,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
     }
     cta_sync();
   }
+  CARRY_T(6);
   if (tid < NSEG && ((growm >> tid) & 1u)) {
     const uint32_t g = tid;
     const uint64_t T = st.thr[g];
@@ -1626,6 +1635,8 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
   }
   cta_sync();
   for (uint32_t v = tid; v < m; v += NT) c.cand[v] = c.vbuf[v];
+  CARRY_T(7);
+#undef CARRY_T
   if (tid == 0) st.tph[12] += gtimer() - tS;
   cta_sync();
 }
