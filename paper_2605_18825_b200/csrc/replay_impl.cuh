@@ -1561,8 +1561,11 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
   uint32_t shrink = 0;
   for (int g = 0; g < NSEG; ++g) {
     const uint32_t want = 3 * s.used[g] + d.slack;
-    if (s.cnt[g] > trim_at * want && (s.fin || g < 9)) shrink |= 1u << g;   // STRUCT keys need scores
+    if (s.cnt[g] > trim_at * want && (s.fin || g < 9) && st.trim_skip[g] == 0)   // STRUCT keys need scores
+      shrink |= 1u << g;
   }
+  cta_sync();                                    // (every thread read trim_skip before it changes)
+  if (tid < NSEG && st.trim_skip[tid]) st.trim_skip[tid]--;
   if (shrink) {
     if (tid < NSEG) s.target[tid] = trim_to * (3 * s.used[tid] + d.slack);
     cta_sync();
@@ -1573,7 +1576,11 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
     for (uint32_t rest = shrink; rest; rest &= rest - 1) {
       const int g = __ffs(rest) - 1;
       radix_select(c.cand, nc, true, 1u << g, s, 0, 0, 0, 2);   // two digits: a bound, not a rank
-      if (tid == g) st.thr[g] = min(st.thr[g], s.pfx[g] | ~s.pmask[g]);
+      if (tid == g) {
+        const uint64_t cut = s.pfx[g] | ~s.pmask[g];
+        if (cut < st.thr[g]) st.thr[g] = cut;
+        else st.trim_skip[g] = 16;               // no cut: back off for 16 passes
+      }
       cta_sync();
     }
   }

@@ -82,6 +82,9 @@ struct RState {
                             // + issue(): start barrier, own partition, end barrier, (spare)
   uint32_t segcnt[16];     // live blocks per segment (maintained at insert / touch / evict)
   uint64_t thr[16];        // per-segment candidate thresholds on k0 (heuristic; exactness never depends on them)
+  uint8_t trim_skip[16];   // passes left before a segment may be trimmed again (a trim that did not
+                           // lower its threshold backs off: STRUCT candidates are a superset of
+                           // the blocks under the threshold, which trimming cannot shrink)
   sae_params par;
 };
 
