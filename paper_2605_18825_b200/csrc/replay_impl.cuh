@@ -162,6 +162,7 @@ struct Smem {
   __align__(16) uint32_t rhist[NSEG * 256];   // radix-select histograms (one 256-bin digit per
                                 // segment); worker scan: its finished candidate records
   __align__(8) uint64_t mbar[24];  // bulk-copy stage barriers (worker scan pipeline): full[12], empty[12]
+  uint64_t wt_pick, wt_end;        // worker: command pickup / stream end times (SAE_WORKER_TIMERS)
   uint64_t wthr[16], wpfx[16], wpmask[16];   // worker copies of the leader's command parameters
   double wcw[15], wmu[2], wsg[2], ww[5];
 };
@@ -617,6 +618,9 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
       asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&empty[st])) : "memory");
     }
   }
+#ifdef SAE_WORKER_TIMERS
+  if (tid == 0) s.wt_end = gtimer();
+#endif
   // publish the CTA's candidates: one reservation in the group buffer, then the records
   // (meta/key re-read from L2; exact Eq.(1)-(3) scores, ids) written contiguously
   const uint32_t nl = min(s.nw, WCAP);
@@ -687,6 +691,15 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
           if (bulk) scan_range_bulk(c, wlo, whi, P);
           else scan_range(c, wlo, whi, P);
           if (c.rank == 1 && tid == 0) g->wscan_ns += gtimer() - tw0;
+#ifdef SAE_WORKER_TIMERS   // debug build: per-pass max pre-stream / max + min stream / max publish
+          if (tid == 0) {
+            const uint64_t tp = gtimer();
+            atomicMax(&g->wdbg[0], (unsigned long long)(tw0 - s.wt_pick));
+            atomicMax(&g->wdbg[1], (unsigned long long)(s.wt_end - tw0));
+            atomicMin(&g->wdbg[2], (unsigned long long)(s.wt_end - tw0));
+            atomicMax(&g->wdbg[3], (unsigned long long)(tp - s.wt_end));
+          }
+#endif
         }
       } else {
         part_range(d.C, c.rank, c.GP, lo, hi);
@@ -842,6 +855,11 @@ __device__ void issue(Ctx& c, unsigned cmd) {
     c.s->st.tph[8] += t1 - t0;
     c.s->st.tph[9] += t2 - t1;
     c.s->st.tph[10] += t3 - t2;
+#ifdef SAE_WORKER_TIMERS
+    if (cmd == CMD_SCAN) {
+      for (int k = 0; k < 4; ++k) { c.s->st.tph[4 + k] += __ldcg(&c.ctl->wdbg[k]); c.ctl->wdbg[k] = k == 2 ? ~0ull : 0ull; }
+    }
+#endif
   }
   cta_sync();
 }
@@ -862,6 +880,9 @@ __device__ void worker_loop(Ctx& c) {
       unsigned long long w;
       while (((w = ld_acquire_u64(&c.ctl->cmdw)) >> 8) != want) __nanosleep(128);
       c.s->wcmd = (unsigned)(w & 0xFFu);
+#ifdef SAE_WORKER_TIMERS
+      c.s->wt_pick = gtimer();
+#endif
     }
     cta_sync();
     const unsigned cmd = c.s->wcmd;

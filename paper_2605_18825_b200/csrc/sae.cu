@@ -111,6 +111,7 @@ struct GroupCtl {          // hot words on separate 128-byte lines (polled / ato
   alignas(128) unsigned selcnt[16];
   alignas(128) unsigned cntq[4];
   unsigned long long wscan_ns;        // worker 1's accumulated scan time (diagnostic)
+  unsigned long long wdbg[4];         // SAE_WORKER_TIMERS debug build: per-pass worker maxima
   alignas(128) unsigned cmd, stamp, shift, active;   // read-only while a command runs
   unsigned long long thr[16], pfx[16], pmask[16];
   double now, gamma, dt_eps, z_cut;
