@@ -165,6 +165,8 @@ struct Smem {
   uint64_t wt_pick, wt_end;        // worker: command pickup / stream end times (SAE_WORKER_TIMERS)
   uint64_t wthr[16], wpfx[16], wpmask[16];   // worker copies of the leader's command parameters
   double wcw[15], wmu[2], wsg[2], ww[5];
+  double wnow, wgam;        // worker copies of the scan's time and gamma
+  uint32_t wmode, wstamp;
 };
 
 struct Ctx {               // per-CTA view of one replica (group)
@@ -331,6 +333,7 @@ __device__ __forceinline__ void finalize_key(const Dev& d, uint64_t base, const 
 // the streaming loop); overflow is scored in place.
 constexpr uint32_t WCAP = NSEG * 256;
 constexpr uint32_t WCAPC = (uint32_t)(NSEG * 256 * 4 / sizeof(Cand));   // records in the same area
+constexpr uint32_t WCAP4 = WCAP / 4;   // bulk scan: (slot, meta, key lo, key hi) records
 __device__ __forceinline__ void note_cand(Ctx& c, const ScanP& P, Cand* gdst, uint32_t pos) {
   const uint32_t w = atomicAdd(&c.s->nw, 1u);
   if (w < WCAP) {
@@ -592,8 +595,9 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
           // stream -- stalling a warp on it here delays its stage release (measured slower)
           const uint32_t sl = (uint32_t)(t0 + u * NT + tid);
           const uint32_t w = basep + __popc(bal & ((1u << lane) - 1u));
-          if (w < WCAP) {
-            s.rhist[w] = sl;
+          if (w < WCAP4) {                // (slot, meta, key): publishing re-reads nothing
+            *reinterpret_cast<uint4*>(&s.rhist[4 * w]) =
+                make_uint4(sl, mv[u], (uint32_t)kv[u], (uint32_t)(kv[u] >> 32));
           } else {                        // list full (rare): append to the group buffer directly
             Cand x = make_cand(mv[u], kv[u], sl);
             finalize_key(d, c.base, P, x);
@@ -622,14 +626,14 @@ __device__ void scan_range_bulk(Ctx& c, uint64_t lo, uint64_t hi, const ScanP& P
   if (tid == 0) s.wt_end = gtimer();
 #endif
   // publish the CTA's candidates: one reservation in the group buffer, then the records
-  // (meta/key re-read from L2; exact Eq.(1)-(3) scores, ids) written contiguously
-  const uint32_t nl = min(s.nw, WCAP);
+  // (meta/key from the smem list; exact Eq.(1)-(3) scores, ids) written contiguously
+  const uint32_t nl = min(s.nw, WCAP4);
   if (tid == 0) s.gbase = atomicAdd(&c.ctl->ncand, nl);
   cta_sync();
   const uint32_t gb0 = s.gbase;
   for (uint32_t i = tid; i < nl; i += NT) {
-    const uint32_t sl = s.rhist[i];
-    Cand x = make_cand(__ldcg(d.bmeta + c.base + sl), __ldcg(d.bkey + c.base + sl), sl);
+    const uint4 rec = *reinterpret_cast<const uint4*>(&s.rhist[4 * i]);
+    Cand x = make_cand(rec.y, ((uint64_t)rec.w << 32) | rec.z, rec.x);
     finalize_key(d, c.base, P, x);
     atomicAdd(&s.cnt[x.seg], 1u);
     gdst[gb0 + i] = x;
@@ -665,18 +669,24 @@ __device__ void run_cmd(Ctx& c, unsigned cmd, bool leader) {
         P.thr = (const unsigned long long*)s.st.thr; P.cw = &s.cw[0][0];
         P.mu = s.st.par.mu; P.sg = s.st.par.sigma;
         P.mode = s.st.par.mode; P.w = s.st.par.w;
-      } else {        // published by the leader before the command: stage into smem
+      } else {        // published by the leader before the command: stage into smem, every
+                      // value by its own thread (one L2 round trip, one barrier)
         if (tid < 16) s.wthr[tid] = __ldcg(&g->thr[tid]);
-        if (tid < 15) s.wcw[tid] = __ldcg(&g->cw[0][0] + tid);
-        if (tid < 5) s.ww[tid] = __ldcg(&g->w[tid]);
-        if (tid < 2) { s.wmu[tid] = __ldcg(&g->mu[tid]); s.wsg[tid] = __ldcg(&g->sigma[tid]); }
+        else if (tid < 31) s.wcw[tid - 16] = __ldcg(&g->cw[0][0] + (tid - 16));
+        else if (tid < 36) s.ww[tid - 31] = __ldcg(&g->w[tid - 31]);
+        else if (tid < 38) s.wmu[tid - 36] = __ldcg(&g->mu[tid - 36]);
+        else if (tid < 40) s.wsg[tid - 38] = __ldcg(&g->sigma[tid - 38]);
+        else if (tid == 40) s.wnow = __ldcg(&g->now);
+        else if (tid == 41) s.wgam = __ldcg(&g->gamma);
+        else if (tid == 42) s.wmode = __ldcg(&g->mode);
+        else if (tid == 43) s.wstamp = __ldcg(&g->stamp);
         cta_sync();
-        P.now = __ldcg(&g->now);
+        P.now = s.wnow;
         P.thr = (const unsigned long long*)s.wthr; P.cw = s.wcw; P.mu = s.wmu; P.sg = s.wsg;
-        P.mode = __ldcg(&g->mode); P.w = s.ww;
+        P.mode = s.wmode; P.w = s.ww;
       }
-      P.stamp = __ldcg(&g->stamp);
-      P.gamma = leader ? s.st.par.gamma : __ldcg(&g->gamma);
+      P.stamp = leader ? __ldcg(&g->stamp) : s.wstamp;
+      P.gamma = leader ? s.st.par.gamma : s.wgam;
       P.dt_eps = d.dt_eps;
       P.z_cut = d.z_cut;
       if (c.GP == 1 || !leader) {
