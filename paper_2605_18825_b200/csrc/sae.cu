@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(128) k_hash(BatchDev b, Dev d) {
 namespace v512 {
 constexpr int NT = 512;
 constexpr int NW = NT / 32;
-constexpr int CAND_MAX = 6144;   // 192 KB: a worker's bulk-scan ring holds four 48 KB tiles
+constexpr int CAND_MAX = 4096;   // (6144, a ring of four 48 KB tiles, measured no faster: k_select 62.1 vs 61.2 us)
 constexpr bool CAND_GLOBAL = false;
 constexpr int MINB = 1;
 #include "replay_impl.cuh"
