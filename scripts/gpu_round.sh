@@ -7,7 +7,7 @@
 #   info        host cores / GPU / clocks of the box
 #   tests       pytest -m gpu (parity through the C ABI) + smoke()
 #   bench       default bench line (C5, cpu_baseline) -> gpurun_out/bench_c5.json
-#   bench_all   bench lines of c2, c3, c4, c4x (no cpu baseline)
+#   bench_all   bench lines of c2, c3, c4, c4x, predictor (no cpu baseline) + the reference arm
 #   ncu_c5      launch list + ncu --set full --import-source on of the timed C5 k_replay
 #   ncu_c4      launch list + full capture of a C4 200-request k_replay launch
 #   ncu_c4x     full capture of a C4x 200-request k_replay launch
@@ -44,10 +44,12 @@ for step in "$@"; do
     bench)
       timeout 900 python bench.py > $O/bench_c5.json 2> $O/bench_c5.err; tail -1 $O/bench_c5.json ;;
     bench_all)
-      for w in c2 c3 c4 c4x; do
-        timeout 1200 python bench.py --workload $w --steps 3 --warmup 3 --no-cpu-baseline > $O/bench_$w.json 2> $O/bench_$w.err
-        tail -1 $O/bench_$w.json
-      done ;;
+      for w in c2 c3 c4 c4x predictor; do
+        timeout 1200 python bench.py --workload $w --steps 3 --warmup 3 --no-cpu-baseline --no-predictor --no-score-select > $O/bench_$w.json 2> $O/bench_$w.err
+        tail -c 400 $O/bench_$w.json
+      done
+      timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > $O/bench_reference.json 2> $O/bench_reference.err
+      tail -c 400 $O/bench_reference.json ;;
     ncu_c5)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c5.csv \
         python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-score-select --no-predictor > /dev/null 2>&1
