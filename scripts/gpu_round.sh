@@ -11,7 +11,8 @@
 #   ncu_c5      launch list + ncu --set full --import-source on of the timed C5 k_replay
 #   ncu_c4      launch list + full capture of a C4 200-request k_replay launch
 #   ncu_c4x     full capture of a C4x 200-request k_replay launch
-#   sanitize    compute-sanitizer memcheck / racecheck / synccheck on small replays
+#   sanitize    compute-sanitizer memcheck / racecheck / synccheck on small replays (closed on
+#               the GPU pool since round 2: it left GPUs needing a reset)
 #   sass        cuobjdump -sass of libsae.so -> per-kernel counts of the TMA / mbarrier / tcgen05
 #               mnemonics (gpurun_out/sass_summary.txt)
 #   ablation    scripts/ablation.py on the balanced, multi-turn- and single-turn-dominant mixes
