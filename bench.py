@@ -891,7 +891,7 @@ def run_ours(args, wl, ws, rank, local):
                      "traffic": traffic,
                      "traffic_source": "profiles/ncu_traffic.json (archived ncu --set full capture of "
                                        "this workload's k_replay; not measured in this run)",
-                     "limiter": ("per-round latency of one CTA per replica (state L1/L2-resident); "
+                     "limiter": ("per-round latency of one CTA per replica (CTA barriers, dependent L2/DRAM accesses); "
                                  "the HBM roofline does not bind") if wl["cfg"] in ("c2", "c5") else
                                 "scan pass HBM/L2 bandwidth + the leader CTA's serial phases",
                      "algorithmic_bytes_per_launch": alg_bytes / max(rep_n, 1),
