@@ -7,8 +7,9 @@ cases driven through the C ABI and the score function itself:
   250 requests per replica (the default 5 warm-up + 20 timed steps); sampled replicas
   replayed by the oracle over all 6 250 requests;
 * C3 (balanced, 16 384-block pool, multi-CTA group) over its first 50 000 requests;
-* C4 on its full 4M-block pool from the empty pool through the first eviction rounds the
-  bench's C4 workload times (SAE_LONG=1 extends this to 1 200 rounds past the fill);
+* C4 on its full 4M-block pool from the empty pool through 500 eviction rounds past the fill
+  (SAE_LONG=1: 11 000 rounds, through the window the bench's C4 workload times -- its pool
+  fills at request ~91 K, the timed steps are requests 106 K-112 K);
 * C4x: the same trace on a 2^24-block pool, 500 eviction rounds past the fill;
 * edge cases the trace generator never produces: equal arrival times, sigma at its 0.1 floor
   with large dt so that P = 0 ties are broken by (last, id), K = 1, one-token prompts with no
@@ -114,7 +115,7 @@ def _c4_first_rounds(extra):
     return tr, pol, cache, out, o4, victims, first
 
 
-@pytest.mark.parametrize("rounds", [60] + ([1200] if os.environ.get("SAE_LONG") else []))
+@pytest.mark.parametrize("rounds", [500] + ([11000] if os.environ.get("SAE_LONG") else []))
 def test_c4_full_pool_through_eviction_rounds(rounds):
     """The empty 4M-block pool filled by the trace (~90K requests), then `rounds` eviction
     rounds; every hash, per-request output and victim id identical to the oracle (its rescans
