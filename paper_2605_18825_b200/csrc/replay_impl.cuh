@@ -128,7 +128,7 @@ __device__ void sort_reg(Cand* a, int N) {
   cta_sync();
 }
 
-__device__ SAE_COLD void sort_cands(Cand* a, int N) {
+__device__ void sort_cands(Cand* a, int N) {
   if (N <= NT) sort_reg<1>(a, N);
   else if (N <= 2 * NT) sort_reg<2>(a, N);
   else if (N <= 4 * NT) sort_reg<4>(a, N);
@@ -299,7 +299,7 @@ __device__ __forceinline__ Cand make_cand(uint32_t meta, uint64_t key, uint32_t 
 
 // Exact score of a scored candidate: Eq.(1) survival (multi-turn) or Eq.(2) (STRUCT),
 // then Eq.(3) P = ((alpha_q * w_tau) * p) / dt, fixed op order (SURVEY c.4).
-__device__ SAE_COLD void finalize_key(const Dev& d, uint64_t base, const ScanP& P, Cand& x) {
+__device__ __forceinline__ void finalize_key(const Dev& d, uint64_t base, const ScanP& P, Cand& x) {
   if (x.seg == 0 || x.seg >= 16) return;
   x.k2 = __ldcg(d.bid + base + (x.ss & SLOT_MASK));
   const double last = from_obits(x.k1);
@@ -906,7 +906,7 @@ __device__ void worker_loop(Ctx& c) {
 }
 
 // Rebuild the resident table (tombstone cleanup) from the live SoA.
-__device__ SAE_COLD void rebuild_table(Ctx& c) {
+__device__ void rebuild_table(Ctx& c) {
   if (threadIdx.x == 0) c.ctl->tblcnt = 0;
   cta_sync();
   issue(c, CMD_CLEAR_T);
@@ -914,7 +914,7 @@ __device__ SAE_COLD void rebuild_table(Ctx& c) {
   if (threadIdx.x == 0) c.s->st.tbl_used = __ldcg(&c.ctl->tblcnt);
   cta_sync();
 }
-__device__ SAE_COLD void rebuild_ghost(Ctx& c) {
+__device__ void rebuild_ghost(Ctx& c) {
   if (threadIdx.x == 0) c.ctl->gtblcnt = 0;
   cta_sync();
   issue(c, CMD_CLEAR_G);
@@ -951,7 +951,7 @@ __device__ __forceinline__ double clampd(double x, double lo, double hi) {
 }
 
 // LEARN (SURVEY c.3): TokenWeights -> QueueWeights -> LognormalParams -> DecayPower.
-__device__ SAE_COLD void learn(Ctx& c) {
+__device__ void learn(Ctx& c) {
   const Dev& d = *c.d;
   Smem& s = *c.s;
   RState& st = s.st;
@@ -1159,12 +1159,12 @@ __device__ SAE_COLD void learn(Ctx& c) {
 // be a victim (else the segment is rescanned), thresholds are re-carried.
 // Output: the victims' slots in eviction order in cand[0..m).
 // ---------------------------------------------------------------------------
-__device__ SAE_COLD void narrow(Ctx& c, uint32_t e, uint32_t mp);
+__device__ void narrow(Ctx& c, uint32_t e, uint32_t mp);
 
 // Block-wide MSB radix select over a[0..n): for every class g in `active` find the key of
 // rank s.target[g] (1-based) -> s.pfx[g], and the number of smaller keys -> s.below[g].
 // Global mode: one class (0), key k0.  Per-segment mode: class = segment, key = seg_key.
-__device__ SAE_COLD void radix_select(const Cand* a, uint32_t n, bool per_seg, uint32_t active, Smem& s,
+__device__ void radix_select(const Cand* a, uint32_t n, bool per_seg, uint32_t active, Smem& s,
                              int tie = 0, uint64_t K0 = 0, uint64_t K1 = 0, int digits = 8,
                              uint32_t early = 0, int tier = -1) {
   // tier >= 0 (global mode): only candidates of that tier (0 EF, 1 scored) take part
@@ -1278,7 +1278,7 @@ __device__ SAE_COLD void radix_select(const Cand* a, uint32_t n, bool per_seg, u
 
 // Stage the candidates with k0 <= Ub (at most VCAP) into vbuf and sort them by (k0, k1, k2);
 // also the per-segment minimum keys (kmin) over all candidates, for threshold growth.
-__device__ SAE_COLD void stage_victims(Ctx& c, uint32_t nc, uint64_t Ub) {
+__device__ void stage_victims(Ctx& c, uint32_t nc, uint64_t Ub) {
   Smem& s = *c.s;
   RState& st = s.st;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -1690,7 +1690,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
 // of rank target_s by a group-parallel MSB radix select over the candidate buffer, then
 // compact the candidates at or below the new thresholds.  The new thresholds are exact
 // bounds (every dropped candidate has a larger key), so the exactness check still holds.
-__device__ SAE_COLD void narrow(Ctx& c, uint32_t e, uint32_t mp) {
+__device__ void narrow(Ctx& c, uint32_t e, uint32_t mp) {
   Smem& s = *c.s;
   RState& st = s.st;
   GroupCtl* g = c.ctl;

@@ -223,21 +223,13 @@ __device__ __forceinline__ double from_obits(uint64_t o) {
 // Policy arithmetic (fixed op order, explicit RN intrinsics; SURVEY c.4)
 // ---------------------------------------------------------------------------
 // Eq.(1): p = 1 - F_LN(dt) = 0.5*erfc(z/sqrt2), z = (ln dt - mu)/sigma (A36)
-// Large, multiply-called device functions are kept out of line (SAE_COLD): the replay kernel
-// inlined everything into ~1 MB of SASS, and its instruction fetch stalled warps
-// ("no_instruction", profiles/r02c_c5.md); -DSAE_INLINE_ALL restores full inlining.
-#ifdef SAE_INLINE_ALL
-#define SAE_COLD
-#else
-#define SAE_COLD __noinline__
-#endif
-__device__ SAE_COLD double survival(double dt, double mu, double sg, double z_cut) {
+__device__ double survival(double dt, double mu, double sg, double z_cut) {
   double z = __ddiv_rn(__dsub_rn(dm::ln(dt), mu), sg);
   if (z > z_cut) return 0.0;
   return __dmul_rn(0.5, dm::erfc(__dmul_rn(z, INV_SQRT2)));
 }
 // Eq.(2): p = 1 - (o/o_max)^gamma with pow(x,y) = exp(y ln x)
-__device__ SAE_COLD double p_struct(uint32_t ob, uint32_t omax, double gam) {
+__device__ double p_struct(uint32_t ob, uint32_t omax, double gam) {
   if (ob == 0) return 1.0;
   double r = __ddiv_rn((double)ob, (double)omax);
   return __dsub_rn(1.0, dm::ex(__dmul_rn(gam, dm::ln(r))));
