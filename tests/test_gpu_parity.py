@@ -269,3 +269,51 @@ def test_c2_prefix_adaptive_beta():
     p = dict(C.DEFAULT_PARAMS)
     p["learn_flags"] = C.L_DEFAULT | C.L_ADAPTIVE_BETA
     compare_replay(T.make("c2", n_requests=6000), C.policy_config(2304, params=p))
+
+
+def test_admit_batch_host_pipelined_matches_oracle():
+    """The end-to-end call sae_admit_batch_host (host buffers, inputs staged in two slots on
+    the library's copy stream, the next call's copies overlapping the current replay), issued
+    back to back with two calls in flight exactly as bench.py's e2e loop does, reading each
+    call's pinned outputs only after the next call is queued: per-request outputs and the
+    victim-id sequence equal the oracle's replay of the same trace."""
+    tr = T.make("c2", n_requests=3000)
+    pol = C.policy_config(2304, K=100)
+    cache = S.SaeCache(2304, policy=pol)
+    tok_h = torch.from_numpy(tr["tokens"].view(np.int32)).pin_memory()
+    typ_h = torch.from_numpy(tr["types"]).pin_memory()
+    tok_d = torch.zeros(tr["n_tokens"], dtype=torch.int32, device="cuda")
+    typ_d = torch.zeros(tr["n_tokens"], dtype=torch.uint8, device="cuda")
+    cuts = [0, 1, 400, 401, 1200, 2000, 3000]        # incl. one-request batches
+    pend, got4, gotv = [], [], []
+
+    def take(res, n):
+        o4 = np.stack([res[k].numpy()[:n].view(np.uint32) for k in
+                       ("hit_blocks", "miss_blocks", "matched_tokens", "n_victims")], 1)
+        vo = res["victim_off"].numpy()
+        vids = res["victim_ids"].numpy().view(np.uint32)
+        got4.append(o4.copy())
+        gotv.extend(int(v) for i in range(n) for v in vids[vo[i] - vo[0]:vo[i] - vo[0] + o4[i, 3]])
+
+    for a, z in zip(cuts[:-1], cuts[1:]):
+        hb = {k: tr[k][a:z] for k in ("arrival", "prompt_off", "prompt_len", "decode_off",
+                                       "decode_len", "flags", "spb")}
+        hb.update(n=z - a, replica=np.zeros(z - a, np.uint32), tokens=np.zeros(1, np.uint32),
+                  types=np.zeros(1, np.uint8))
+        hp = S.batch_to_torch(hb, pin=True)
+        lo = int(hb["prompt_off"].min())
+        hi = int((hb["decode_off"] + hb["decode_len"].astype(np.uint64)).max())
+        res, _, _ = cache.admit_batch_host(hp, tok_h, typ_h, tok_d, typ_d, lo, hi)
+        ev = torch.cuda.Event()
+        ev.record()
+        pend.append((ev, res, z - a))
+        if len(pend) > 1:
+            evp, rp, n = pend.pop(0)
+            evp.synchronize()
+            take(rp, n)
+    torch.cuda.synchronize()
+    for evp, rp, n in pend:
+        take(rp, n)
+    ref = oracle.Replica(pol).replay(tr, 0, 3000)
+    assert np.array_equal(np.concatenate(got4), ref.out4)
+    assert gotv == [int(v) for v in ref.victims]
