@@ -1431,7 +1431,7 @@ __device__ void select_chunk(Ctx& c, uint32_t m, uint32_t stamp, bool count_pass
       if (tid == 0) s.target[0] = in_ef ? m : m - ef;
       cta_sync();
       const uint32_t lim = in_ef ? VCAP / 2 : (ef + 16 < VCAP / 2 ? VCAP / 2 - ef : 16u);
-      radix_select(c.cand, nc, false, 1u, s, 0, 0, 0, 8, lim / 2, in_ef ? 0 : 1);
+      radix_select(c.cand, nc, false, 1u, s, 0, 0, 0, 8, lim * d.early_q / 4, in_ef ? 0 : 1);
       staged = (in_ef ? 0u : ef) + s.below[0] + s.binc[0] <= VCAP;
       if (!staged) {               // rare: fall back to the exact global rank m
         if (tid == 0) s.target[0] = m;

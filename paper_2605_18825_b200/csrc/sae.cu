@@ -135,6 +135,8 @@ struct Dev {
                         // co-resident CTAs): each replica's run is cut into nchunk consecutive
                         // chunks, a persistent grid takes (chunk, replica) tasks in order from
                         // *taskctr, and chunk k of replica r waits for rflag[r] = (epoch, k)
+  uint32_t early_q;     // the select's radix stops once the chosen prefix set holds at most
+                        // early_q/4 of the staging limit (env SAE_EARLY = 1..4; default 2)
   uint32_t* taskctr;    // [1] next task of the current launch (zeroed before each launch)
   uint32_t* rflag;      // [R] (epoch << 8) | chunks of the replica's run done this launch
   Cand* gcand;          // [R*C] global candidate buffer (large pools)
@@ -896,6 +898,11 @@ static sae_status create_impl(const sae_config* cfg, sae_ctx* ctx) {
   if (const char* e = getenv("SAE_CHUNKS")) {   // measurements: force (1 = whole replicas)
     const int v = atoi(e);
     if (v >= 1 && v <= 255 && d.GP == 1) d.nchunk = (uint32_t)v;
+  }
+  d.early_q = 2;
+  if (const char* e = getenv("SAE_EARLY")) {
+    const int v = atoi(e);
+    if (v >= 1 && v <= 4) d.early_q = (uint32_t)v;
   }
   CK(dalloc(ctx, &d.taskctr, 1));
   CK(dalloc(ctx, &d.rflag, R));
