@@ -706,6 +706,19 @@ def run_ours(args, wl, ws, rank, local):
         sync_every = int(args.sync.split("@")[1])
         assert sync_every % per == 0, "the sync period must be a multiple of the %d-request step" % per
     n_syncs = 0
+    if args.prewarm_s > 0:
+        # bring the GPU to its steady state before the warm-up steps (a fresh box's first GPU
+        # process measured slower): a large memset + matmul loop for prewarm_s seconds, untimed
+        t_end = time.perf_counter() + args.prewarm_s
+        a = torch.randn(4096, 4096, device=dev)
+        junk = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
+        while time.perf_counter() < t_end:
+            junk.fill_(1)
+            for _ in range(8):
+                a = torch.tanh(a @ a)
+            torch.cuda.synchronize()
+        del a, junk
+        torch.cuda.empty_cache()
     clk = Clocks(local)
     clk.start()           # before the warm-up: its start-up must not overlap the timed steps
     # ---- device-resident timed steps
@@ -862,6 +875,7 @@ def run_ours(args, wl, ws, rank, local):
     line = {
         "metric": "requests replayed/s", "value": req_all / (tmax * 1e-3), "unit": "req/s",
         "n_gpus": ws, "steps": K, "warmup": W, "ms_per_step": tmax / K,
+        "step_ms": [round(t, 3) for t in times],
         "higher_is_better": True, "scaling": "strong" if wl["cfg"] == "c5" else "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
@@ -927,6 +941,8 @@ def main():
     ap.add_argument("--no-predictor", action="store_true", help="skip the session_predictor sub-record")
     ap.add_argument("--no-score-select", action="store_true", help="skip the score_select_pass sub-record")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--prewarm-s", type=float, default=0.0,
+                    help="untimed GPU pre-warm (memset + matmul loop) before the warm-up steps")
     ap.add_argument("--sync", default="none",
                     help="C5 parameter sync: none | mean_w@E (every E requests per replica: NCCL "
                          "all-gather of the learned weights + fixed-order mean over seeds)")
