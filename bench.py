@@ -26,6 +26,7 @@ the same workload on the host cores; it is the reference arm of this tier.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -105,11 +106,14 @@ def predictor_phase(dev, n: int = PRED_N, d: int = PRED_D, steps: int = 20, warm
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = P.launches()
+    gc.collect()
+    gc.disable()
     e0.record()
     for _ in range(steps):
         P.predict(h, logit=y)
     e1.record()
     torch.cuda.synchronize()
+    gc.enable()
     ms = e0.elapsed_time(e1) / steps
     launches = P.launches() - l0
     byts = n * d * 2 + (256 * d + 64 * 256) * 2 + (256 + 64 + 64) * 4 + n * 4
@@ -172,11 +176,14 @@ def score_select_phase(dev, capacity: int = 1 << 24, m: int = 64, passes: int = 
     torch.cuda.synchronize()
     st0 = cache.stats(0)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    gc.collect()
+    gc.disable()
     e0.record()
     for _ in range(launches):
         cache.select(0, m, now, passes=passes, vids=vids, n_out=nout)
     e1.record()
     torch.cuda.synchronize()
+    gc.enable()
     st1 = cache.stats(0)
     ms = e0.elapsed_time(e1)
     npass = launches * passes
@@ -724,7 +731,11 @@ def run_ours(args, wl, ws, rank, local):
         torch.cuda.empty_cache()
     clk = Clocks(local)
     clk.start()           # before the warm-up: its start-up must not overlap the timed steps
-    # ---- device-resident timed steps
+    # ---- device-resident timed steps (Python's cyclic GC off while steps are enqueued: a
+    # collection between e0.record() and the launches stalls the host for 100+ ms and the
+    # device clock counts it -- measured as one 90-250 ms step among 65-80 ms ones)
+    gc.collect()
+    gc.disable()
     times = []
     st0 = None
     for s in range(W + K):
@@ -749,6 +760,7 @@ def run_ours(args, wl, ws, rank, local):
         barrier()
         if s >= W:
             times.append(e0.elapsed_time(e1))
+    gc.enable()
     clocks = clk.stop()
     launches = cache.launches() - l0
     rep_ms, rep_n = cache.profile_read()
@@ -789,6 +801,8 @@ def run_ours(args, wl, ws, rank, local):
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    gc.collect()
+    gc.disable()
     e0.record()
     pend, e2e_hits = [], 0
     for hp, a, z, n in pinned[2:]:
@@ -808,6 +822,7 @@ def run_ours(args, wl, ws, rank, local):
     for evp, rp in pend:
         e2e_hits += int(rp["hit_blocks"].sum())
     e2e_ms = e0.elapsed_time(e1)
+    gc.enable()
     barrier()
 
     # ---- reduce over ranks (max time, summed work)
