@@ -787,6 +787,16 @@ static sae_status create_impl(const sae_config* cfg, sae_ctx* ctx) {
   ctx->cfg = *cfg;
   ctx->device = cfg->device;
   CK(cudaSetDevice(cfg->device));
+  {
+    // the per-batch workspace comes from the device's default stream-ordered pool: keep freed
+    // blocks in the pool (the default threshold 0 hands them back to the driver at every
+    // synchronisation, and re-mapping them inside a later step stalled it by 100+ ms)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, cfg->device) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   Dev& d = ctx->d;
   std::memset(&d, 0, sizeof d);
   d.R = cfg->n_replicas;
@@ -1042,7 +1052,7 @@ static sae_status prepare(sae_ctx* ctx, const sae_batch* b, BatchDev& x, cudaStr
   if (need > ctx->ws_cap) {
     if (ctx->ws) CK(cudaFreeAsync(ctx->ws, s));
     ctx->ws = nullptr;
-    size_t cap = need + need / 4;
+    size_t cap = need + need / 2;
     CK(cudaMallocAsync(&ctx->ws, cap, s));
     ctx->ws_cap = cap;
   }
