@@ -136,7 +136,7 @@ struct Dev {
                         // chunks, a persistent grid takes (chunk, replica) tasks in order from
                         // *taskctr, and chunk k of replica r waits for rflag[r] = (epoch, k)
   uint32_t early_q;     // the select's radix stops once the chosen prefix set holds at most
-                        // early_q/4 of the staging limit (env SAE_EARLY = 1..4; default 4)
+                        // early_q/4 of the staging limit (env SAE_EARLY = 1..8; default 4)
   uint32_t* taskctr;    // [1] next task of the current launch (zeroed before each launch)
   uint32_t* rflag;      // [R] (epoch << 8) | chunks of the replica's run done this launch
   Cand* gcand;          // [R*C] global candidate buffer (large pools)
@@ -912,7 +912,7 @@ static sae_status create_impl(const sae_config* cfg, sae_ctx* ctx) {
   d.early_q = 4;    // measured on C5 (select phase per step): 1: 14.9 ms, 2: 13.5-13.9, 3: 13.2, 4: 12.8
   if (const char* e = getenv("SAE_EARLY")) {
     const int v = atoi(e);
-    if (v >= 1 && v <= 4) d.early_q = (uint32_t)v;
+    if (v >= 1 && v <= 8) d.early_q = (uint32_t)v;   // up to 8: twice the limit = the whole staging buffer
   }
   CK(dalloc(ctx, &d.taskctr, 1));
   CK(dalloc(ctx, &d.rflag, R));
