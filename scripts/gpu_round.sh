@@ -11,6 +11,7 @@
 #   ncu_c5      launch list + ncu --set full --import-source on of the timed C5 k_replay
 #   ncu_c4      launch list + full capture of a C4 200-request k_replay launch
 #   ncu_c4x     full capture of a C4x 200-request k_replay launch
+#   ncu_select  full capture of one 10-pass sae_select launch on the full 2^24-block pool
 #   sanitize    compute-sanitizer memcheck / racecheck / synccheck on small replays (closed on
 #               the GPU pool since round 2: it left GPUs needing a reset)
 #   sass        cuobjdump -sass of libsae.so -> per-kernel counts of the TMA / mbarrier / tcgen05
@@ -67,6 +68,10 @@ for step in "$@"; do
       timeout 1500 ncu --set full --import-source on --clock-control none -k regex:k_replay -s 30 -c 1 -f -o $O/full_c4x \
         python scripts/prof_c4x.py > $O/prof_c4x.log 2>&1
       shrink_rep $O/full_c4x ;;
+    ncu_select)
+      timeout 1500 ncu --set full --import-source on --clock-control none -k regex:k_select -s 2 -c 1 -f -o $O/full_select \
+        python scripts/prof_select.py > $O/prof_select.log 2>&1
+      shrink_rep $O/full_select ;;
     sanitize)
       for tool in memcheck racecheck synccheck; do
         timeout 900 compute-sanitizer --tool $tool python scripts/sanitize.py > $O/sanitize_$tool.log 2>&1
