@@ -136,6 +136,15 @@ def predictor_phase(dev, n: int = PRED_N, d: int = PRED_D, steps: int = 20, warm
                          "flops_per_launch": flops, "bytes_per_launch": byts}}
 
 
+def _archived_traffic(key):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        v = json.load(open(p)).get(key)
+        return float(v) if v is not None else None
+    except (OSError, ValueError):
+        return None
+
+
 def score_select_phase(dev, capacity: int = 1 << 24, m: int = 64, passes: int = 10, launches: int = 4,
                        n_requests: int = 440_000) -> dict:
     """The fused score/select pass alone (K3, sae_select: Alg.1 Evict's choice of the next m
@@ -209,7 +218,10 @@ def score_select_phase(dev, capacity: int = 1 << 24, m: int = 64, passes: int = 
             "fill": {"requests": lo, "trace_gen_s": round(t_gen, 1), "fill_s": round(t_fill, 1)},
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "peak_source": src, "unit": "GB/s",
                          "frac": gbs / hbm, "bytes_per_pass": byts,
-                         "bytes_model": "12 B scan record (meta u32 + key u64) per resident block"}}
+                         "bytes_model": "12 B scan record (meta u32 + key u64) per resident block",
+                         "traffic": _archived_traffic("select_pass"),
+                         "traffic_source": "profiles/ncu_traffic.json select_pass (archived ncu --set full "
+                                           "capture of one 10-pass launch, per pass; not measured in this run)"}}
     cache.close()
     torch.cuda.empty_cache()
     return info
